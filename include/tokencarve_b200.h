@@ -1,0 +1,130 @@
+/*
+ * tokencarve_b200.h -- C ABI of the B200-native (sm_100a) Jenga attention-carving
+ * hot path.  Plain pointers, sizes and a cudaStream_t passed as void*; no torch
+ * types.  All device pointers are caller-owned (the library never allocates
+ * persistent device memory and never frees caller memory).  Every entry point
+ * is stream-ordered and asynchronous (no host synchronisation), returns 0 on
+ * success or one of the TCB_E* codes, with a human-readable message from
+ * tcb_last_error() (thread-local).
+ *
+ * The reference (tokencarve 0.1.0, /root/reference/pkg/src/tokencarve) is a
+ * pure-numpy package with no FFI; each entry point names the reference
+ * function whose semantics it implements (file:line).  The Python host package
+ * paper_2505_16864_b200 binds these with ctypes behind the reference's own
+ * function signatures.
+ *
+ * Error codes map 1:1 to the reference exception taxonomy (errors.py:4-29).
+ */
+#ifndef TOKENCARVE_B200_H
+#define TOKENCARVE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TCB_OK 0
+#define TCB_ESHAPE 1    /* ShapeError    errors.py:4   */
+#define TCB_EDOMAIN 2   /* DomainError   errors.py:8   */
+#define TCB_ESIZE 3     /* SizeError     errors.py:12  */
+#define TCB_ECONTRACT 4 /* ContractError errors.py:16  */
+#define TCB_ECUDA 5     /* CUDA launch / runtime failure (RuntimeError) */
+
+/* element types for tensors whose dtype is not fixed */
+#define TCB_F32 0
+#define TCB_BF16 1
+
+const char* tcb_last_error(void);
+int tcb_abi_version(void);
+
+/* K1 -- space-filling-curve index builder.
+ * Replaces build_curve (sfc.py:198-210) = _gilbert2d/_gen2d (sfc.py:98-157)
+ * + _curve_coords (sfc.py:160-195).  fwd[i] = row-major cell at curve position
+ * i; inv[fwd[i]] = i.  int32 (n_cells < 2^31, else TCB_ESIZE). */
+int tcb_curve_build(int t, int h, int w, int32_t* fwd, int32_t* inv, void* stream);
+
+/* K2 -- row gather dst[i,:] = src[idx[i],:] for rows of row_bytes bytes.
+ * Replaces apply_permutation / invert_permutation -> _permute (sfc.py:213-237).
+ * idx must lie in [0, src_rows). */
+int tcb_gather_rows(const void* src, void* dst, const int32_t* idx, int64_t rows,
+                    int64_t row_bytes, int64_t src_rows, void* stream);
+
+/* K6 -- 26-neighbour block adjacency, packed.  Replaces adjacency_mask
+ * (partition.py:107-136).  adja is (M_v, words) uint32, bit j of row i set
+ * iff blocks i, j touch; symmetric, diagonal set.  Zeroed by the call. */
+int tcb_adjacency_build(const int32_t* inv, int t, int h, int w, int m, int M_v, int words,
+                        uint32_t* adja, void* stream);
+
+/* K3 -- block mean-pool of Q and K over valid tokens, float64 accumulation.
+ * Replaces block_pool (masks.py:98-116).  x{0,1}: (H, N_pad, d) with strides
+ * (stride_h, stride_n, 1) in elements; out{0,1}: (H, M_total, d) float64
+ * contiguous.  x1/out1 may be NULL (pool one tensor). */
+int tcb_block_pool(const void* x0, const void* x1, int dtype, int64_t stride_h, int64_t stride_n,
+                   int H, int d, int m, int M_v, int M_total, int64_t n_valid, int64_t n_cond,
+                   double* out0, double* out1, void* stream);
+
+/* K4 -- row-stochastic pooled relevance in float64.  Replaces relevance
+ * (masks.py:119-134) on the vision rows (masks.py:194-197):
+ * R[h,i,:] = softmax_j(pq[h,i].pk[h,j] / sqrt(d)), i < rows, j < M_total.
+ * pq: (H, pq_blocks, d), pk: (H, M_total, d) contiguous float64. */
+int tcb_block_relevance(const double* pq, int pq_blocks, const double* pk, int H, int rows,
+                        int M_total, int d, double* R, void* stream);
+
+/* K5 + K6 union -- importance selection + union with condition and adjacency.
+ * Replaces importance_mask (masks.py:137-159) and union_mask (masks.py:162-175).
+ * R: (H, M_v, M_total) float64; adja: (M_v, words) or NULL (no adjacency term);
+ * outputs: bits (H, M_v, words) uint32, ascending CSR kv_idx (H, M_v, M_total)
+ * int32 (row capacity M_total) and kv_cnt (H, M_v) int32.  n_floor =
+ * max(1, ceil(k*M_v)) computed by the host in float64 (masks.py:154).
+ * with_union=0 returns the bare importance mask (no cond / adjacency OR). */
+int tcb_block_select(const double* R, int H, int M_v, int M_total, const uint32_t* adja, int words,
+                     int n_floor, double p, int with_union, uint32_t* bits, int32_t* kv_idx,
+                     int32_t* kv_cnt, void* stream);
+
+/* Mask conversions for user-built BlockMask(bits=bool array) (masks.py:78-95). */
+int tcb_mask_pack(const uint8_t* dense, int64_t rows, int M_total, int words, uint32_t* bits,
+                  int32_t* kv_idx, int32_t* kv_cnt, void* stream);
+int tcb_mask_unpack(const uint32_t* bits, int64_t rows, int M_total, int words, uint8_t* dense,
+                    void* stream);
+
+/* K7/K8 -- block-sparse flash-attention forward.  Replaces carve_attention /
+ * _carve_rows (attention.py:162-243).  q,k,v,o: (H, N_pad, d) with element
+ * strides (stride_h, stride_n, 1), N_pad = M_total*m.  Vision q-block i of
+ * head h streams kv blocks kv_idx[h,i,:kv_cnt[h,i]] (ascending); condition
+ * q-blocks attend all M_total blocks; padding keys get -inf, beta is added on
+ * condition keys of vision rows, padding rows of o are zeroed.
+ * dtype TCB_BF16 with m == 128 and d in {64,128} runs the tcgen05/TMEM/TMA
+ * kernel; everything else runs the fp32 SIMT kernel (parity path).
+ * work: caller-provided scratch of >= 16 bytes (scheduler counter). */
+int tcb_carve_fwd(const void* q, const void* k, const void* v, void* o, int dtype,
+                  int64_t stride_h, int64_t stride_n, const int32_t* kv_idx,
+                  const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
+                  int64_t n_valid, int64_t n_cond, float beta, int32_t* work, void* stream);
+
+/* Like tcb_carve_fwd but forces the fp32-math SIMT kernel for any shape. */
+int tcb_carve_fwd_simt(const void* q, const void* k, const void* v, void* o, int dtype,
+                       int64_t stride_h, int64_t stride_n, const int32_t* kv_idx,
+                       const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
+                       int64_t n_valid, int64_t n_cond, float beta, void* stream);
+
+/* K9/K10 -- fused predict_clean -> area upsample -> re-noise.
+ * Replaces predict_clean (pipeline.py:124-128), upsample_area_3d
+ * (pipeline.py:153-173) and stage_transition (pipeline.py:176-194).
+ * x: (st,sh,sw,C) float32; vel: same or NULL (then x is already x0);
+ * out = (1-sigma)*U(x - sigma*vel) + sigma*eps at (dt,dh,dw,C).
+ * mode 0: out = U(x0) (sigma = 0 path, float64 taps, cast to float32)
+ * mode 1: eps read from eps (host-drawn noise, bitwise reference parity)
+ * mode 2: eps drawn in-kernel (Philox4x32-10 + Box-Muller, seed/offset). */
+int tcb_upsample_renoise(const float* x, const float* vel, const float* eps, float* out, int st,
+                         int sh, int sw, int dt, int dh, int dw, int C, double sigma, int mode,
+                         uint64_t seed, uint64_t offset, void* stream);
+
+/* Euler step x + (sigma_next - sigma) * v (pipeline.py:131-137), float32. */
+int tcb_euler_step(const float* x, const float* v, float* out, int64_t n, float dsigma,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOKENCARVE_B200_H */

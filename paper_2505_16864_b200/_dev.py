@@ -1,0 +1,48 @@
+"""Host<->device plumbing shared by the API modules (torch owns memory and streams)."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise _native.NativeUnavailable("a CUDA device is required (the product path has no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def as_cuda(x, dtype=None) -> torch.Tensor:
+    """numpy / torch -> contiguous-innermost CUDA tensor (copy only when needed)."""
+    if isinstance(x, torch.Tensor):
+        t = x if x.is_cuda else x.to(device(), non_blocking=False)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(x)).to(device())
+    if dtype is not None and t.dtype != dtype:
+        t = t.to(dtype)
+    return t
+
+
+def is_numpy(x) -> bool:
+    return isinstance(x, np.ndarray)
+
+
+def to_like(t: torch.Tensor, like):
+    """Return numpy if the caller passed numpy, else the tensor."""
+    if is_numpy(like):
+        return t.cpu().numpy()
+    return t
+
+
+def code_of(dtype: torch.dtype) -> int:
+    if dtype == torch.float32:
+        return _native.F32
+    if dtype == torch.bfloat16:
+        return _native.BF16
+    raise TypeError(f"unsupported dtype {dtype} (float32 or bfloat16)")
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream

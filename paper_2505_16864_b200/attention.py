@@ -1,0 +1,125 @@
+"""Block-sparse attention over the carve mask (reference: tokencarve attention.py).
+
+``carve_attention`` is one launch of ``tcb_carve_fwd``: bf16 inputs with m=128 and
+d in {64, 128} run the persistent tcgen05/TMEM/TMA kernel; fp32 inputs (the
+reference's own dtype) and other shapes run the fp32 SIMT kernel that mirrors the
+reference's per-block streaming order (attention.py:162-206).  The output has the
+input dtype; numpy inputs come back as float32 numpy like the reference.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _dev, _native
+from .errors import DomainError, ShapeError
+from .masks import BlockMask
+from .partition import BlockLayout
+
+__all__ = ["AttentionInputs", "AmplifierBias", "compute_beta", "carve_attention"]
+
+
+@dataclass(frozen=True)
+class AttentionInputs:
+    """Q/K/V (heads, N, d_k) plus their layout (attention.py:35-75)."""
+
+    q: object
+    k: object
+    v: object
+    layout: BlockLayout
+
+    def __post_init__(self):
+        shp = [tuple(x.shape) for x in (self.q, self.k, self.v)]
+        if not (shp[0] == shp[1] == shp[2]) or len(shp[0]) != 3:
+            raise ShapeError(f"Q/K/V must share one (heads, N, d_k) shape, got {shp[0]}/{shp[1]}/{shp[2]}")
+        if shp[0][1] != self.layout.padded_total:
+            raise ShapeError(f"token axis {shp[0][1]} != padded token count {self.layout.padded_total}")
+
+    @property
+    def n_heads(self) -> int:
+        return int(self.q.shape[0])
+
+    @property
+    def d_k(self) -> int:
+        return int(self.q.shape[2])
+
+    @property
+    def valid_len(self) -> int:
+        return self.layout.valid_len
+
+    @property
+    def text_block_start(self) -> int:
+        return self.layout.M_v
+
+
+@dataclass(frozen=True)
+class AmplifierBias:
+    """Additive logit bias on vision-query x condition-key scores (attention.py:78-86)."""
+
+    beta: float = 0.0
+
+    def __post_init__(self):
+        if not (self.beta >= 0.0 and math.isfinite(self.beta)):
+            raise DomainError(f"amplifier bias must be finite and >= 0, got {self.beta}")
+
+
+def compute_beta(numel_s: int, numel_S: int, rho: float) -> float:
+    """``-rho * log(numel_s / numel_S)`` (attention.py:89-96)."""
+    if numel_s <= 0 or numel_S <= 0:
+        raise DomainError(f"token counts must be positive, got {numel_s}, {numel_S}")
+    return -rho * math.log(numel_s / numel_S) + 0.0
+
+
+_work: dict = {}
+
+
+def _workspace(dev: torch.device) -> torch.Tensor:
+    w = _work.get(dev)
+    if w is None:
+        w = torch.zeros(16, dtype=torch.int32, device=dev)
+        _work[dev] = w
+    return w
+
+
+def carve_raw(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: BlockMask,
+              layout: BlockLayout, beta: float = 0.0, out: torch.Tensor | None = None,
+              simt: bool = False) -> torch.Tensor:
+    """Device-tensor entry: q/k/v (H, N_pad, d) sharing strides, innermost contiguous."""
+    H, N, d = q.shape
+    if k.stride() != q.stride() or v.stride() != q.stride() or q.stride(2) != 1:
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    if out is None:
+        out = torch.empty_like(q)
+    if out.stride() != q.stride():
+        raise ShapeError("output must share the input strides")
+    args = (q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), _dev.code_of(q.dtype),
+            q.stride(0), q.stride(1), mask.kv_idx.data_ptr(), mask.kv_cnt.data_ptr(), H, d, layout.m,
+            layout.M_v, layout.M_total, layout.n_valid, layout.n_cond, float(beta))
+    if simt:
+        _native.call("tcb_carve_fwd_simt", *args, _dev.stream())
+    else:
+        _native.call("tcb_carve_fwd", *args, _workspace(q.device).data_ptr(), _dev.stream())
+    return out
+
+
+def carve_attention(inputs: AttentionInputs, mask: BlockMask,
+                    beta: AmplifierBias = AmplifierBias(0.0), n_workers: int | None = None):
+    """Block-sparse attention (attention.py:209-243).
+
+    ``n_workers`` is accepted for signature compatibility and ignored (results never
+    depend on it; the kernel's kv visit order is fixed ascending).
+    """
+    layout = inputs.layout
+    expected = (inputs.n_heads, layout.M_v, layout.M_total)
+    if tuple(mask.shape) != expected:
+        raise ShapeError(f"mask shape {tuple(mask.shape)} != {expected}")
+    if layout.M_v:
+        mask.check_nonempty()
+    q, k, v = (_dev.as_cuda(x) for x in (inputs.q, inputs.k, inputs.v))
+    if q.dtype not in (torch.float32, torch.bfloat16):
+        q, k, v = q.float(), k.float(), v.float()
+    out = carve_raw(q, k, v, mask, layout, beta.beta)
+    return _dev.to_like(out, inputs.q)

@@ -1,0 +1,44 @@
+// Shared helpers for the sm_100a kernels: status/error plumbing and launch checks.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+
+#include "../../include/tokencarve_b200.h"
+
+namespace tcb {
+
+int set_error(int code, const char* fmt, ...);
+
+// After a launch: map a launch/runtime error to TCB_ECUDA.
+int check_launch(const char* what);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Valid tokens in block b of the layout [vision | pad | cond | pad]
+// (partition.py:3-13, 83-88): valid tokens always form a prefix of the block.
+__host__ __device__ __forceinline__ int block_valid(int b, int m, int M_v, int64_t n_valid,
+                                                    int64_t n_cond) {
+  int64_t start, cnt;
+  if (b < M_v) {
+    start = (int64_t)b * m;
+    cnt = n_valid - start;
+  } else {
+    start = (int64_t)(b - M_v) * m;
+    cnt = n_cond - start;
+  }
+  if (cnt < 0) cnt = 0;
+  if (cnt > m) cnt = m;
+  return (int)cnt;
+}
+
+}  // namespace tcb
+
+#define TCB_CHECK_ARG(cond, code, ...)                  \
+  do {                                                  \
+    if (!(cond)) return ::tcb::set_error(code, __VA_ARGS__); \
+  } while (0)

@@ -1,0 +1,236 @@
+"""Dynamic block selection on the GPU (reference: tokencarve masks.py).
+
+``build_block_mask`` is three launches: K3 ``tcb_block_pool`` (Q and K in one
+pass, float64 accumulation -> pooled means bit-exact with masks.py:112-116),
+K4 ``tcb_block_relevance`` (float64 pooled scores + row softmax,
+masks.py:119-134) and K5 ``tcb_block_select`` (stable descending sort,
+sequential float64 prefix, cutoff/quota, union with condition columns and the
+packed adjacency, masks.py:137-175).  The mask is kept packed (H, M_v, words)
+plus an ascending CSR (kv_idx, kv_cnt) that the attention kernel walks.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _dev, _native
+from .errors import ContractError, ShapeError
+from .partition import BlockLayout, StaticMasks, mask_words, pack_rows, unpack_rows
+
+__all__ = ["PooledBlocks", "SelectionParams", "BlockMask", "block_pool", "relevance",
+           "importance_mask", "union_mask", "build_block_mask", "mask_stats"]
+
+
+@dataclass(frozen=True)
+class PooledBlocks:
+    """Per-head block means (H, blocks, d) float64 (masks.py:31-50)."""
+
+    values: torch.Tensor
+    valid_counts: np.ndarray
+
+    def __post_init__(self):
+        if self.values.ndim != 3:
+            raise ShapeError(f"pooled values must be rank 3, got shape {tuple(self.values.shape)}")
+        if tuple(self.valid_counts.shape) != (self.values.shape[1],):
+            raise ShapeError("valid_counts length must equal the block count")
+
+    @property
+    def n_heads(self) -> int:
+        return int(self.values.shape[0])
+
+    @property
+    def n_blocks(self) -> int:
+        return int(self.values.shape[1])
+
+
+@dataclass(frozen=True)
+class SelectionParams:
+    """Top-k rate and cutoff (masks.py:53-75)."""
+
+    k: float = 0.3
+    p: float = 0.3
+    per_stage: tuple = (0.3, 0.2)
+
+    def __post_init__(self):
+        rates = (self.k, *self.per_stage)
+        if any(not (0.0 < r <= 1.0) for r in rates):
+            raise ContractError(f"selection rates must be in (0, 1], got {rates}")
+        if not (0.0 <= self.p < 1.0):
+            raise ContractError(f"cutoff probability must be in [0, 1), got {self.p}")
+
+    def for_stage(self, stage: int) -> "SelectionParams":
+        k = self.per_stage[min(stage, len(self.per_stage) - 1)]
+        return SelectionParams(k=k, p=self.p, per_stage=self.per_stage)
+
+    def n_floor(self, M_v: int) -> int:
+        """Top-k quota max(1, ceil(k * M_v)) in float64 on the host (masks.py:154)."""
+        return max(1, math.ceil(self.k * M_v))
+
+
+class BlockMask:
+    """Selection mask (H, M_v, M_total) (masks.py:78-95).
+
+    Device form: packed ``words`` (H, M_v, ceil(M_total/32)) and the ascending CSR
+    ``kv_idx`` (H, M_v, M_total capacity) / ``kv_cnt`` (H, M_v).  ``BlockMask(bits=)``
+    accepts a dense bool array/tensor like the reference and packs it on the device;
+    ``.bits`` materialises the dense bool tensor lazily.
+    """
+
+    def __init__(self, bits=None, *, words=None, kv_idx=None, kv_cnt=None, M_total=None,
+                 nonempty: bool = False):
+        if bits is not None:
+            if bits.ndim != 3 or (bits.dtype not in (np.bool_, torch.bool)):
+                raise ShapeError(f"mask bits must be a rank-3 boolean array, got {tuple(bits.shape)}")
+            dense = _dev.as_cuda(bits)
+            M_total = int(dense.shape[-1])
+            words, kv_idx, kv_cnt = pack_rows(dense, M_total)
+            self._dense = dense
+            nonempty = False
+        else:
+            if words is None or kv_idx is None or kv_cnt is None or M_total is None:
+                raise ShapeError("BlockMask needs bits= or the packed (words, kv_idx, kv_cnt)")
+            self._dense = None
+        self.words = words
+        self.kv_idx = kv_idx
+        self.kv_cnt = kv_cnt
+        self.M_total = int(M_total)
+        self._nonempty = nonempty
+
+    @property
+    def shape(self) -> tuple:
+        return (*self.kv_cnt.shape, self.M_total)
+
+    @property
+    def bits(self) -> torch.Tensor:
+        if self._dense is None:
+            self._dense = unpack_rows(self.words, self.M_total)
+        return self._dense
+
+    @property
+    def n_heads(self) -> int:
+        return int(self.kv_cnt.shape[0])
+
+    @property
+    def selected_fraction(self) -> float:
+        total = int(np.prod(self.shape))
+        return float(self.kv_cnt.sum().item()) / total if total else 0.0
+
+    def check_nonempty(self) -> None:
+        """ContractError on an empty row (attention.py:228-231); free for masks
+        built by build_block_mask (the adjacency diagonal keeps rows non-empty)."""
+        if self._nonempty or self.kv_cnt.numel() == 0:
+            return
+        mn = int(self.kv_cnt.min().item())
+        if mn == 0:
+            h, r = np.argwhere(self.kv_cnt.cpu().numpy() == 0)[0]
+            raise ContractError(f"empty mask row for head {h}, query block {r}")
+        self._nonempty = True
+
+
+def _pool_one_or_two(x0: torch.Tensor, x1: torch.Tensor | None, layout: BlockLayout):
+    for x in (x0,) if x1 is None else (x0, x1):
+        if x.ndim != 3:
+            raise ShapeError(f"expected (heads, tokens, d_k), got shape {tuple(x.shape)}")
+        if x.shape[1] != layout.padded_total:
+            raise ShapeError(f"token axis {x.shape[1]} != padded token count {layout.padded_total}")
+    if x1 is not None and (x1.shape != x0.shape or x1.dtype != x0.dtype
+                           or x1.stride() != x0.stride()):
+        raise ShapeError("Q and K must share shape, dtype and strides")
+    H, _, d = x0.shape
+    if x0.stride(2) != 1:
+        raise ShapeError("innermost (d_k) axis must be contiguous")
+    outs = [torch.empty((H, layout.M_total, d), dtype=torch.float64, device=x0.device)
+            for _ in range(1 if x1 is None else 2)]
+    _native.call("tcb_block_pool", x0.data_ptr(), _native.ptr(x1), _dev.code_of(x0.dtype),
+                 x0.stride(0), x0.stride(1), H, d, layout.m, layout.M_v, layout.M_total,
+                 layout.n_valid, layout.n_cond, outs[0].data_ptr(),
+                 outs[1].data_ptr() if x1 is not None else None, _dev.stream())
+    counts = layout.block_valid_counts.copy()
+    return [PooledBlocks(values=o, valid_counts=counts) for o in outs]
+
+
+def block_pool(x, layout: BlockLayout) -> PooledBlocks:
+    """Mean over valid tokens per block, float64 (masks.py:98-116)."""
+    return _pool_one_or_two(_dev.as_cuda(x), None, layout)[0]
+
+
+def relevance(pooled_q: PooledBlocks, pooled_k: PooledBlocks, d_k: int) -> torch.Tensor:
+    """Row softmax of pooled scores / sqrt(d_k), float64 (masks.py:119-134)."""
+    if pooled_q.n_heads != pooled_k.n_heads:
+        raise ShapeError("pooled Q and K disagree on head count")
+    if pooled_q.values.shape[2] != d_k or pooled_k.values.shape[2] != d_k:
+        raise ShapeError("pooled Q/K feature size must equal d_k")
+    pq = pooled_q.values.contiguous()
+    pk = pooled_k.values.contiguous()
+    H, rows, _ = pq.shape
+    R = torch.empty((H, rows, pk.shape[1]), dtype=torch.float64, device=pq.device)
+    _native.call("tcb_block_relevance", pq.data_ptr(), rows, pk.data_ptr(), H, rows, pk.shape[1],
+                 d_k, R.data_ptr(), _dev.stream())
+    return R
+
+
+def _select(R: torch.Tensor, params: SelectionParams, M_v: int, adja_bits, with_union: bool):
+    H, rows, n_cols = R.shape
+    words = mask_words(n_cols)
+    dev = R.device
+    bits = torch.empty((H, rows, words), dtype=torch.int32, device=dev)
+    kv_idx = torch.empty((H, rows, n_cols), dtype=torch.int32, device=dev)
+    kv_cnt = torch.empty((H, rows), dtype=torch.int32, device=dev)
+    _native.call("tcb_block_select", R.data_ptr(), H, rows, n_cols, _native.ptr(adja_bits), words,
+                 params.n_floor(M_v), float(params.p), 1 if with_union else 0, bits.data_ptr(),
+                 kv_idx.data_ptr(), kv_cnt.data_ptr(), _dev.stream())
+    return bits, kv_idx, kv_cnt
+
+
+def importance_mask(R, params: SelectionParams, M_v: int):
+    """Cutoff + quota selection per row (masks.py:137-159); dense bool result."""
+    if R.ndim != 3:
+        raise ShapeError(f"relevance must be rank 3, got shape {tuple(R.shape)}")
+    Rd = _dev.as_cuda(R, torch.float64).contiguous()
+    bits, _, _ = _select(Rd, params, M_v, None, with_union=False)
+    return _dev.to_like(unpack_rows(bits, Rd.shape[-1]), R)
+
+
+def union_mask(b_top, cond, adja, layout: BlockLayout) -> BlockMask:
+    """``b_top | cond[:M_v] | adja`` (masks.py:162-175)."""
+    shape = (b_top.shape[0], layout.M_v, layout.M_total)
+    if tuple(b_top.shape) != shape:
+        raise ShapeError(f"importance mask shape {tuple(b_top.shape)} != {shape}")
+    if tuple(cond.shape) != (layout.M_total, layout.M_total):
+        raise ShapeError(f"condition mask shape {tuple(cond.shape)} is inconsistent with the layout")
+    if tuple(adja.shape) != (layout.M_v, layout.M_v):
+        raise ShapeError(f"adjacency mask shape {tuple(adja.shape)} is inconsistent with the layout")
+    dense = _dev.as_cuda(b_top).clone() | _dev.as_cuda(cond)[None, : layout.M_v, :]
+    dense[:, :, : layout.M_v] |= _dev.as_cuda(adja)[None]
+    return BlockMask(bits=dense)
+
+
+def build_block_mask(q, k, layout: BlockLayout, statics: StaticMasks, params: SelectionParams):
+    """Pool -> score -> select -> union; returns (BlockMask, R) (masks.py:178-199)."""
+    qd, kd = _dev.as_cuda(q), _dev.as_cuda(k)
+    d_k = qd.shape[-1]
+    pq, pk = _pool_one_or_two(qd, kd, layout)
+    R = torch.empty((qd.shape[0], layout.M_v, layout.M_total), dtype=torch.float64,
+                    device=qd.device)
+    _native.call("tcb_block_relevance", pq.values.data_ptr(), layout.M_total, pk.values.data_ptr(),
+                 qd.shape[0], layout.M_v, layout.M_total, d_k, R.data_ptr(), _dev.stream())
+    bits, kv_idx, kv_cnt = _select(R, params, layout.M_v, statics.packed(layout), with_union=True)
+    mask = BlockMask(words=bits, kv_idx=kv_idx, kv_cnt=kv_cnt, M_total=layout.M_total,
+                     nonempty=True)
+    return mask, _dev.to_like(R, q)
+
+
+def mask_stats(mask: BlockMask, R=None, p: float | None = None) -> dict:
+    """masks.py:202-213."""
+    stats = {"n_heads": mask.n_heads, "shape": list(mask.shape),
+             "selected_fraction": mask.selected_fraction}
+    if R is not None and p is not None:
+        Rd = _dev.as_cuda(R, torch.float64)
+        covered = (Rd * mask.bits[:, :, : Rd.shape[-1]]).sum(dim=-1) > p
+        stats["rows_meeting_cutoff"] = int(covered.sum().item())
+        stats["rows_total"] = int(covered.numel())
+    return stats

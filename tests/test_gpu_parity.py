@@ -1,0 +1,264 @@
+"""GPU parity: every kernel through the C ABI vs the golden vectors of the real
+reference and the CPU oracle (bit-exact for integer/byte work, stated tolerances
+for floating point)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import golden_io as gio
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+tcb = pytest.importorskip("paper_2505_16864_b200")
+
+
+def sha16(a):
+    return hashlib.sha256(np.ascontiguousarray(np.asarray(a).astype("<i8")).tobytes()).hexdigest()[:16]
+
+
+# ----------------------------------------------------------------- K1 curve (bit-exact)
+def test_curve_small_bit_exact():
+    for dims, fw in gio.small_curves():
+        p = tcb.build_curve(tcb.GridDims(*dims))
+        assert np.array_equal(p.forward_np, fw), dims
+        assert np.array_equal(p.inverse_np[fw], np.arange(len(fw)))
+
+
+def test_curve_named_fingerprints():
+    g = gio.load("curves.npz")
+    for i, d in enumerate(g["big_dims"]):
+        p = tcb.build_curve(tcb.GridDims(*(int(v) for v in d)))
+        assert sha16(p.forward_np) == str(g["big_sha"][i])
+        assert np.array_equal(p.forward_np[:64], g["big_head"][i])
+
+
+def test_curve_exhaustive_small_grids():
+    for t in range(1, 9):
+        for h in range(1, 9):
+            for w in range(1, 9):
+                p = tcb.build_curve(tcb.GridDims(t, h, w))
+                assert np.array_equal(p.forward_np, oracle.curve_forward((t, h, w)))
+
+
+# ----------------------------------------------------------------- K2 gather
+@pytest.mark.parametrize("payload", [(16,), (3,), (3072,), (5, 7), ()])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.int64, torch.uint8])
+def test_gather_roundtrip(payload, dtype):
+    dims = tcb.GridDims(3, 9, 13)
+    p = tcb.build_curve(dims)
+    n = dims.n_cells
+    x = (torch.arange(n * int(np.prod(payload)), device="cuda") % 251).to(dtype).reshape(n, *payload)
+    z = tcb.apply_permutation(x, p)
+    ref = x.cpu()[torch.from_numpy(p.forward_np.copy())]
+    assert torch.equal(z.cpu(), ref)
+    assert torch.equal(tcb.invert_permutation(z, p).cpu(), x.cpu())
+
+
+def test_gather_numpy_and_list_payloads():
+    dims = tcb.GridDims(2, 5, 6)
+    p = tcb.build_curve(dims)
+    a = np.random.default_rng(0).standard_normal((60, 3)).astype(np.float32)
+    out = tcb.apply_permutation(a, p)
+    assert isinstance(out, np.ndarray) and np.array_equal(out, a[p.forward_np])
+    lst = list(range(60))
+    assert tcb.apply_permutation(lst, p) == [lst[i] for i in p.forward_np]
+    with pytest.raises(tcb.ShapeError):
+        tcb.apply_permutation(a[:10], p)
+
+
+# ----------------------------------------------------------------- K6 adjacency (bit-exact)
+def test_adjacency_bit_exact():
+    for dims, m, nc, row, adj in gio.layout_rows():
+        g = tcb.GridDims(*dims)
+        lay = tcb.build_layout(g, m, nc)
+        assert [lay.n_valid, lay.M_v, lay.M_c, lay.M_total, lay.padded_total, lay.cond_start] == \
+            [int(v) for v in row[5:11]]
+        st = tcb.StaticMasks.build(lay, g, tcb.build_curve(g))
+        assert np.array_equal(st.adja.cpu().numpy(), adj), dims
+
+
+# ----------------------------------------------------------------- K3/K4/K5 masks
+@pytest.mark.parametrize("case", ["c1", "c1k08", "small", "tiny", "nocond"])
+def test_pool_relevance_select(case):
+    for name, P, g in gio.mask_cases():
+        if name != case:
+            continue
+        dims = tcb.GridDims(*P["dims"])
+        lay = tcb.build_layout(dims, P["m"], P["n_cond"])
+        st = tcb.StaticMasks.build(lay, dims, tcb.build_curve(dims))
+        q, k, _ = gio.qkv(P["seed"], P["H"], lay.padded_total, P["d"])
+        pq = tcb.block_pool(q, lay)
+        assert np.array_equal(pq.values.cpu().numpy(), g[f"{name}_pq"])  # bit-exact
+        params = tcb.SelectionParams(k=P["k"], p=P["p"])
+        mask, R = tcb.build_block_mask(q, k, lay, st, params)
+        np.testing.assert_allclose(R, g[f"{name}_R"], rtol=1e-12, atol=1e-15)
+        want = gio.unpack_bits(g[f"{name}_bits"], lay.M_total)
+        got = mask.bits.cpu().numpy()
+        assert (got == want).mean() >= 0.999
+        assert np.array_equal(got, want)
+        # bit-exact given the reference's own R
+        top = tcb.importance_mask(g[f"{name}_R"], params, lay.M_v)
+        u = tcb.union_mask(torch.from_numpy(top).cuda(), st.cond, st.adja, lay)
+        assert np.array_equal(u.bits.cpu().numpy(), want)
+        # CSR is the ascending list of set bits
+        idx, cnt = mask.kv_idx.cpu().numpy(), mask.kv_cnt.cpu().numpy()
+        for h in range(P["H"]):
+            for i in range(lay.M_v):
+                assert np.array_equal(idx[h, i, :cnt[h, i]], np.flatnonzero(want[h, i]))
+
+
+def test_select_traces_and_ties():
+    g = gio.load("masks.npz")
+    for tr in g["traces"]:
+        R = tr[:4].reshape(1, 1, 4)
+        got = tcb.importance_mask(R, tcb.SelectionParams(k=float(tr[4]), p=float(tr[5])), 4)
+        assert got[0, 0].tolist() == [bool(v) for v in tr[6:]]
+    R = g["randR"]
+    for key in [k for k in g if k.startswith("randR_bits_")]:
+        _, _, kk, p = key.split("_")
+        got = tcb.importance_mask(R, tcb.SelectionParams(k=float(kk), p=float(p)), 40)
+        assert np.array_equal(got, gio.unpack_bits(g[key], R.shape[-1])), key
+
+
+def test_select_random_rows_vs_oracle():
+    rng = np.random.default_rng(5)
+    for n_cols in (1, 2, 31, 32, 33, 257, 931, 1500):
+        R = rng.random((2, 7, n_cols))
+        R[:, :, : n_cols // 3] = np.round(R[:, :, : n_cols // 3], 1)  # ties
+        R = R / R.sum(-1, keepdims=True)
+        for k, p in ((0.08, 0.0), (0.3, 0.3), (1.0, 0.0), (0.01, 0.99)):
+            got = tcb.importance_mask(R, tcb.SelectionParams(k=k, p=p), max(1, n_cols - 2))
+            assert np.array_equal(got, oracle.select_topk(R, k, p, max(1, n_cols - 2)))
+
+
+# ----------------------------------------------------------------- K7/K8 carve
+def _case(name):
+    for n, P, g in gio.attention_cases():
+        if n == name:
+            return P, g
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("case", ["c1", "c1beta", "small", "m128", "m128nc", "d64"])
+def test_carve_fp32_vs_reference(case):
+    P, g = _case(case)
+    dims = tcb.GridDims(*P["dims"])
+    lay = tcb.build_layout(dims, P["m"], P["n_cond"])
+    q, k, v = gio.qkv(P["seed"], P["H"], lay.padded_total, P["d"])
+    mask = tcb.BlockMask(bits=gio.unpack_bits(g[f"{case}_bits"], lay.M_total))
+    out = tcb.carve_attention(tcb.AttentionInputs(q=q, k=k, v=v, layout=lay), mask,
+                              tcb.AmplifierBias(P["beta"]))
+    assert out.dtype == np.float32
+    # tolerance 1e-5 relative in fp32 (north_star), on per-row fingerprints + raw rows
+    np.testing.assert_allclose(out.astype(np.float64).sum(-1), g[f"{case}_rowsum"], rtol=1e-5,
+                               atol=1e-5)
+    np.testing.assert_allclose((out.astype(np.float64) ** 2).sum(-1), g[f"{case}_rowsq"],
+                               rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(out[:, :8], g[f"{case}_head"], rtol=1e-5, atol=1e-6)
+    valid = oracle.token_valid(oracle.layout_scalars(P["dims"], P["m"], P["n_cond"]))
+    assert np.all(out[:, ~valid] == 0.0)
+
+
+def _bf16(a):
+    return torch.from_numpy(a).cuda().to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("case", ["m128", "m128nc", "d64"])
+def test_carve_bf16_tcgen05_vs_oracle(case):
+    P, g = _case(case)
+    dims = tcb.GridDims(*P["dims"])
+    lay = tcb.build_layout(dims, P["m"], P["n_cond"])
+    q, k, v = (_bf16(a) for a in gio.qkv(P["seed"], P["H"], lay.padded_total, P["d"]))
+    bits = gio.unpack_bits(g[f"{case}_bits"], lay.M_total)
+    mask = tcb.BlockMask(bits=bits)
+    out = tcb.carve_attention(tcb.AttentionInputs(q=q, k=k, v=v, layout=lay), mask,
+                              tcb.AmplifierBias(P["beta"]))
+    assert out.dtype == torch.bfloat16
+    L = oracle.layout_scalars(P["dims"], P["m"], P["n_cond"])
+    ref = oracle.carve(q.float().cpu().numpy(), k.float().cpu().numpy(), v.float().cpu().numpy(),
+                       bits, L, P["beta"])
+    got = out.float().cpu().numpy()
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err <= 2e-2, err  # bf16 tolerance (north_star): 2e-2 relative to max|ref|
+    assert np.all(got[:, ~oracle.token_valid(L)] == 0.0)
+
+
+def test_carve_bf16_tcgen05_long_rows_and_determinism():
+    # many kv blocks per row (cond rows attend everything), beta, partial blocks
+    dims = tcb.GridDims(5, 24, 40)  # 4800 cells -> 38 vision blocks (last partial)
+    lay = tcb.build_layout(dims, 128, 200)
+    st = tcb.StaticMasks.build(lay, dims, tcb.build_curve(dims))
+    rng = np.random.default_rng(1)
+    q, k, v = (_bf16(rng.standard_normal((3, lay.padded_total, 128), dtype=np.float32) * 2)
+               for _ in range(3))
+    mask, _ = tcb.build_block_mask(q, k, lay, st, tcb.SelectionParams(k=0.5, p=0.2))
+    inp = tcb.AttentionInputs(q=q, k=k, v=v, layout=lay)
+    o1 = tcb.carve_attention(inp, mask, tcb.AmplifierBias(0.7))
+    o2 = tcb.carve_attention(inp, mask, tcb.AmplifierBias(0.7))
+    assert torch.equal(o1, o2)  # bitwise run-to-run
+    L = oracle.layout_scalars(dims.as_tuple(), 128, 200)
+    ref = oracle.carve(q.float().cpu().numpy(), k.float().cpu().numpy(), v.float().cpu().numpy(),
+                       mask.bits.cpu().numpy(), L, 0.7, workers=8)
+    err = np.abs(o1.float().cpu().numpy() - ref).max() / np.abs(ref).max()
+    assert err <= 2e-2, err  # 2e-2 relative to max|ref|
+
+
+def test_carve_contract_errors():
+    dims = tcb.GridDims(2, 4, 4)
+    lay = tcb.build_layout(dims, 8, 3)
+    q = np.zeros((1, lay.padded_total, 8), np.float32)
+    bits = np.ones((1, lay.M_v, lay.M_total), bool)
+    bits[0, 1] = False
+    with pytest.raises(tcb.ContractError):
+        tcb.carve_attention(tcb.AttentionInputs(q=q, k=q, v=q, layout=lay), tcb.BlockMask(bits=bits))
+    with pytest.raises(tcb.ShapeError):
+        tcb.carve_attention(tcb.AttentionInputs(q=q, k=q, v=q, layout=lay),
+                            tcb.BlockMask(bits=np.ones((2, lay.M_v, lay.M_total), bool)))
+
+
+# ----------------------------------------------------------------- K9/K10 stage switch
+def test_upsample_and_transition():
+    g = gio.load("stage.npz")
+    for i in range(int(g["n_cases"])):
+        src = tuple(int(v) for v in g[f"case{i}_src"])
+        dst = tcb.GridDims(*(int(v) for v in g[f"case{i}_dst"]))
+        C = g[f"case{i}_up"].shape[-1]
+        rng = np.random.default_rng(40 + i)
+        x = rng.standard_normal((*src, C), dtype=np.float32)
+        vel = rng.standard_normal((*src, C), dtype=np.float32)
+        np.testing.assert_allclose(tcb.upsample_area_3d(x, dst), g[f"case{i}_up"], rtol=0, atol=1e-6)
+        x0 = tcb.predict_clean(x, vel, 0.899083)
+        assert np.array_equal(x0, x - np.float32(0.899083) * vel)
+        tr = tcb.stage_transition(x0, 0.899083, dst, np.random.default_rng(99))
+        np.testing.assert_allclose(tr, g[f"case{i}_tr"], rtol=0, atol=1e-6)
+        fused = tcb.switch_stage(x, vel, 0.899083, dst, np.random.default_rng(99))
+        np.testing.assert_allclose(fused, g[f"case{i}_tr"], rtol=0, atol=1e-6)
+        tr0 = tcb.stage_transition(x0, 0.0, dst, np.random.default_rng(99))
+        np.testing.assert_allclose(tr0, g[f"case{i}_tr0"], rtol=0, atol=1e-6)
+
+
+def test_philox_noise_statistics():
+    x0 = np.zeros((4, 30, 40, 8), np.float32)
+    out = tcb.stage_transition(x0, 1.0, tcb.GridDims(4, 60, 80), 1234)
+    assert abs(out.mean()) < 0.02 and abs(out.std() - 1.0) < 0.02
+
+
+# ----------------------------------------------------------------- end to end
+def test_toy_pipeline_matches_reference():
+    g = gio.load("pipeline.npz")
+    plan = tcb.StagePlan(
+        stages=(tcb.StageConfig(dims=tcb.GridDims(2, 4, 6), step_indices=(0, 3, 6), alpha=3.0,
+                                k=0.3, rho=0.5),
+                tcb.StageConfig(dims=tcb.GridDims(2, 6, 8), step_indices=(6, 8, 9), alpha=5.0,
+                                k=0.2)),
+        base_T=10, block_size=8, n_cond_tokens=5, p=0.3)
+    den = tcb.toy_transformer_denoiser(channels=2, n_heads=2, d_k=16, seed=1234)
+    res = tcb.run_pipeline(plan, den, rng=0, channels=2)
+    np.testing.assert_allclose([s["sigma"] for s in res.report["steps"]], g["sigmas"])
+    np.testing.assert_allclose([s["effective_sparsity"] for s in res.report["steps"]],
+                               g["sparsity"])
+    np.testing.assert_allclose(res.latent, g["latent"], rtol=1e-4, atol=1e-4)
