@@ -1,0 +1,414 @@
+"""Benchmark: ms per carved-attention layer at HunyuanVideo 720p (BASELINE.json).
+
+One step = one carved-attention layer on synthetic bf16 Q/K/V of the C2 shape
+(33x45x80 = 118,800 video + 256 text tokens, H=24, d=128, m=128, k=0.08, p=0):
+K3 block pool (Q,K) -> K4 pooled relevance -> K5 select/union -> K7/K8 carve.
+With --gpus N>1 (torchrun) the layer is head-parallel: all-to-all (seq -> head
+shard), the local layer on H/N heads, all-to-all back; value = max over ranks.
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle port of
+the reference (the reference is pure numpy; oracle/port.py restates it) on a
+bounded sample and prints the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# C2
+DIMS = (33, 45, 80)
+M = 128
+N_COND = 256
+H = 24
+D = 128
+K_RATE = 0.08
+P_CUT = 0.0
+METRIC = "ms per carved-attention layer at HunyuanVideo 720p"
+WORKLOAD = ("C2 HunyuanVideo-13B attention layer: 720p 33x45x80=118,800 video + 256 text tokens, "
+            "H=24, d=128, m=128 blocks (M_total=931), k=0.08 p=0 (~10% kept), bf16")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.result = None
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            return
+        rows = [r.split(", ") for r in out.strip().splitlines() if r.count(",") >= 6]
+        if not rows:
+            return
+        sm = [float(r[0]) for r in rows]
+        mx = max(float(r[1]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].strip() == "Active"})
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        self.result = {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": reasons,
+                       "samples": len(rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_16864_b200 as tcb
+    from paper_2505_16864_b200 import _native
+    from paper_2505_16864_b200.attention import _workspace
+    from paper_2505_16864_b200.partition import mask_words
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _native.load()
+
+    dims = tcb.GridDims(*DIMS)
+    layout = tcb.build_layout(dims, M, N_COND)
+    perm = tcb.build_curve(dims)
+    statics = tcb.StaticMasks.build(layout, dims, perm)
+    adja = statics.packed(layout)
+    params = tcb.SelectionParams(k=K_RATE, p=P_CUT)
+    Np, Mt, Mv = layout.padded_total, layout.M_total, layout.M_v
+    Hl = H // world
+    words = mask_words(Mt)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    if world == 1:
+        # head-major (H, N, d) bf16, the layout carve_attention takes
+        q, k, v = (torch.randn((H, Np, D), generator=g, device=dev, dtype=torch.float32)
+                   .to(torch.bfloat16) for _ in range(3))
+    else:
+        n_loc = Np // world
+        q, k, v = (torch.randn((n_loc, H, D), generator=g, device=dev, dtype=torch.float32)
+                   .to(torch.bfloat16) for _ in range(3))
+
+    pq = torch.empty((Hl, Mt, D), dtype=torch.float64, device=dev)
+    pk = torch.empty_like(pq)
+    R = torch.empty((Hl, Mv, Mt), dtype=torch.float64, device=dev)
+    bits = torch.empty((Hl, Mv, words), dtype=torch.int32, device=dev)
+    kv_idx = torch.empty((Hl, Mv, Mt), dtype=torch.int32, device=dev)
+    kv_cnt = torch.empty((Hl, Mv), dtype=torch.int32, device=dev)
+    work = _workspace(dev)
+    n_floor = params.n_floor(Mv)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def layer(qh, kh, vh, out, marks=None):
+        """The four launches of one carved-attention layer on head-major views."""
+        sh, sn = qh.stride(0), qh.stride(1)
+        if marks: marks[0].record()
+        _native.call("tcb_block_pool", qh.data_ptr(), kh.data_ptr(), 1, sh, sn, Hl, D, M, Mv, Mt,
+                     layout.n_valid, layout.n_cond, pq.data_ptr(), pk.data_ptr(), sptr)
+        if marks: marks[1].record()
+        _native.call("tcb_block_relevance", pq.data_ptr(), Mt, pk.data_ptr(), Hl, Mv, Mt, D,
+                     R.data_ptr(), sptr)
+        if marks: marks[2].record()
+        _native.call("tcb_block_select", R.data_ptr(), Hl, Mv, Mt, adja.data_ptr(), words, n_floor,
+                     float(P_CUT), 1, bits.data_ptr(), kv_idx.data_ptr(), kv_cnt.data_ptr(), sptr)
+        if marks: marks[3].record()
+        _native.call("tcb_carve_fwd", qh.data_ptr(), kh.data_ptr(), vh.data_ptr(), out.data_ptr(), 1,
+                     sh, sn, kv_idx.data_ptr(), kv_cnt.data_ptr(), Hl, D, M, Mv, Mt, layout.n_valid,
+                     layout.n_cond, 0.0, work.data_ptr(), sptr)
+        if marks: marks[4].record()
+        return out
+
+    if world == 1:
+        o = torch.empty_like(q)
+
+        def step(marks=None):
+            return layer(q, k, v, o, marks)
+    else:
+        from paper_2505_16864_b200.ulysses import head_to_seq, seq_to_head
+
+        oh = torch.empty((Np, Hl, D), dtype=torch.bfloat16, device=dev)
+
+        def step(marks=None):
+            qh, kh, vh = seq_to_head([q, k, v])
+            layer(qh.permute(1, 0, 2), kh.permute(1, 0, 2), vh.permute(1, 0, 2),
+                  oh.permute(1, 0, 2), marks)
+            return head_to_seq(oh)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    # kept pairs (algorithmic FLOPs = 4 m^2 d per kept (head, q-block, kv-block))
+    pairs_local = int(kv_cnt.sum().item()) + Hl * layout.M_c * Mt
+    pairs = pairs_local
+    if world > 1:
+        t = torch.tensor([pairs_local], device=dev, dtype=torch.int64)
+        dist.all_reduce(t)
+        pairs = int(t.item())
+
+    marks = [[ev() for _ in range(5)] for _ in range(args.steps)]
+    t0, t1 = ev(), ev()
+    barrier()
+    with Clocks(local) as clk:
+        t0.record()
+        for i in range(args.steps):
+            step(marks[i])
+        t1.record()
+        barrier()
+    total_ms = t0.elapsed_time(t1)
+    per = np.array([[marks[i][j].elapsed_time(marks[i][j + 1]) for j in range(4)]
+                    for i in range(args.steps)])
+    ms_step = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    k_pool, k_rel, k_sel, k_carve = per.mean(axis=0)
+    flops = 4.0 * M * M * D * pairs
+    flops_local = 4.0 * M * M * D * pairs_local
+    hbm, tf_burst, tf_sust, peak_src = peaks()
+    carve_tflops = flops_local / (k_carve * 1e-3) / 1e12
+
+    # e2e through the public API with host buffers (pinned H2D in, O D2H out)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+        ho = torch.empty_like(hq).pin_memory()
+        inp_bytes = 3 * hq.numel() * hq.element_size()
+        out_bytes = ho.numel() * ho.element_size()
+
+        def e2e_step():
+            dq, dk, dv = (t.to(dev, non_blocking=True) for t in (hq, hk, hv))
+            mask, _ = tcb.build_block_mask(dq, dk, layout, statics, params)
+            out = tcb.carve_attention(tcb.AttentionInputs(q=dq, k=dk, v=dv, layout=layout), mask)
+            ho.copy_(out, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        n_e2e = max(2, min(args.steps, 5))
+        a, b = ev(), ev()
+        a.record()
+        for _ in range(n_e2e):
+            e2e_step()
+        b.record()
+        torch.cuda.synchronize()
+        e2e = {"value": round(a.elapsed_time(b) / n_e2e, 3), "unit": "ms",
+               "h2d_bytes_per_step": inp_bytes, "d2h_bytes_per_step": out_bytes,
+               "path": "tcb.build_block_mask + tcb.carve_attention on pinned host Q/K/V"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.cpu_seconds)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "carve_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC,
+        "value": round(ms_step, 4),
+        "unit": "ms",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (torch.randn Q/K/V, bf16), random-init; no checkpoint",
+        "config": {"workload": WORKLOAD, "tokens": Np, "heads": H, "d": D, "block": M,
+                   "k": K_RATE, "p": P_CUT, "kept_pairs": pairs,
+                   "kept_fraction": round(pairs / (H * Mt * Mt), 4),
+                   "parallelism": f"ulysses-heads{world}" if world > 1 else "single",
+                   "l2": "no flush: Q/K/V/O = 2.9 GB per layer > 126 MB L2"},
+        "kept_block_tflops": round(carve_tflops, 1),
+        "kernels_ms": {"block_pool": round(float(k_pool), 4), "block_relevance": round(float(k_rel), 4),
+                       "block_select": round(float(k_sel), 4), "carve_fwd": round(float(k_carve), 4)},
+        "roofline": {"bound": "tensor", "kernel": "k_carve_tc<128>",
+                     "achieved": round(carve_tflops, 1), "peak": tf_sust, "unit": "TFLOP/s",
+                     "frac": round(carve_tflops / tf_sust, 4),
+                     "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
+                     "frac_of_burst": round(carve_tflops / tf_burst, 4),
+                     "traffic": traffic,
+                     "algorithmic_flops_per_launch": flops_local,
+                     "pool_hbm_gbs": round(2 * Hl * Np * D * 2 / (k_pool * 1e-3) / 1e9, 1),
+                     "hbm_peak_gbs": hbm},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": 4 * args.steps,
+        "clocks": clk.result,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------ CPU arm
+def cpu_sample(budget_s: float):
+    """Time the oracle port of the reference on a bounded C2 sample and extrapolate to
+    one full layer (ms).  Sample: build_block_mask on 1 head + carve of as many head-0
+    q-blocks as fit the budget (cond rows excluded), per-pair cost scaled to all pairs."""
+    import oracle
+
+    from threadpoolctl import threadpool_limits
+
+    threads = len(os.sched_getaffinity(0))
+    with threadpool_limits(limits=1, user_api="blas"):  # workers x 1 BLAS thread
+        return _cpu_sample(budget_s, threads)
+
+
+def _cpu_sample(budget_s, threads):
+    import oracle
+
+    L = oracle.layout_scalars(DIMS, M, N_COND)
+    rng = np.random.default_rng(0)
+    shape = (1, L["padded_total"], D)
+    q, k, v = (rng.standard_normal(shape, dtype=np.float32) for _ in range(3))
+    inv = oracle.curve_inverse(oracle.curve_forward(DIMS))
+    adja = oracle.adjacency(DIMS, inv, M, L["M_v"])
+    t0 = time.perf_counter()
+    bits, _ = oracle.block_mask(q, k, L, adja, K_RATE, P_CUT)
+    t_mask = time.perf_counter() - t0
+    order = np.random.default_rng(1).permutation(L["M_v"])
+    # pick the faster of serial / threaded workers on a calibration chunk (the reference's
+    # ThreadPoolExecutor path, attention.py:233-242, only helps on some hosts)
+    best_w, best_rate = 1, None
+    pos = 0
+    for w in sorted({1, threads}):
+        sel = [(0, int(b)) for b in order[pos:pos + max(24, 3 * w)]]
+        pos += len(sel)
+        t0 = time.perf_counter()
+        oracle.carve(q, k, v, bits, L, 0.0, workers=w, items=sel)
+        rate = (time.perf_counter() - t0) / sum(int(bits[0, b].sum()) for _, b in sel)
+        if best_rate is None or rate < best_rate:
+            best_w, best_rate = w, rate
+    items, pairs, t_carve = 0, 0, 0.0
+    chunk = max(best_w * 4, 16)
+    while t_carve < budget_s and pos + items < L["M_v"]:
+        sel = [(0, int(b)) for b in order[pos + items:pos + items + chunk]]
+        t0 = time.perf_counter()
+        oracle.carve(q, k, v, bits, L, 0.0, workers=best_w, items=sel)
+        t_carve += time.perf_counter() - t0
+        pairs += int(sum(bits[0, b].sum() for _, b in sel))
+        items += len(sel)
+    kept_per_head = int(bits[0].sum()) + L["M_c"] * L["M_total"]
+    total_pairs = kept_per_head * H  # head 0's kept count stands in for every head
+    ms = (t_carve / pairs * total_pairs + t_mask * H) * 1e3
+    sample = (f"oracle port (numpy, {best_w} worker threads x 1 BLAS thread, {threads} cores): "
+              f"build_block_mask on 1 of "
+              f"{H} heads ({t_mask:.2f} s) + carve of {items} head-0 q-blocks / {pairs} kv pairs "
+              f"({t_carve:.2f} s), extrapolated to {total_pairs} pairs and {H} heads")
+    return ms, best_w, sample
+
+
+def cpu_baseline(budget_s):
+    ms, cores, sample = cpu_sample(budget_s)
+    return {"value": round(ms, 1), "unit": "ms", "cores": cores, "kind": "port", "sample": sample}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    budget = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
+    if args.cpu_seconds == 20.0:  # default: keep the whole reference run within minutes
+        budget = max(1.0, 120.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        cpu_sample(budget)
+    vals, samples = [], None
+    for _ in range(args.steps):
+        ms, cores, samples = cpu_sample(budget)
+        vals.append(ms)
+    v = float(np.mean(vals))
+    line = {"metric": METRIC, "value": round(v, 1), "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 1),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (numpy default_rng(0) Q/K/V, fp32)", "impl": "reference",
+            "config": {"workload": WORKLOAD, "k": K_RATE, "p": P_CUT},
+            "cpu_baseline": {"value": round(v, 1), "unit": "ms", "cores": cores, "kind": "port",
+                             "sample": samples},
+            "e2e": {"value": round(v, 1), "unit": "ms", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,68 @@
+"""Summarise ncu output into the tracked profiles/ directory.
+
+    python profiles/summarize.py launches gpurun_out/launches.csv > profiles/rXX_launches.md
+    python profiles/summarize.py full gpurun_out/prof.ncu-rep > profiles/rXX_ncu.md
+"""
+
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "dram read"),
+    ("dram__bytes_write.sum", "dram write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram % peak"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
+    ("sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe % active"),
+    ("sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active", "tmem pipe %"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64 pipe %"),
+    ("sm__pipe_xu_cycles_active.avg.pct_of_peak_sustained_active", "XU (MUFU) pipe %"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU inst %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("launch__registers_per_thread", "regs/thread"),
+    ("launch__shared_mem_per_block_dynamic", "dyn smem/block"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
+    ("lts__t_bytes.sum", "L2 bytes"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+]
+
+
+def launches(path):
+    text = open(path).read()
+    rows = list(csv.reader(io.StringIO(text[text.index('"ID"'):])))
+    h = rows[0]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = collections.OrderedDict()
+    for r in rows[1:]:
+        name = r[ki].split("(")[0]
+        agg.setdefault(name, []).append(float(r[vi]) / 1e3)
+    total = sum(sum(v) for v in agg.values())
+    print("| kernel | launches | mean us | total us | share |")
+    print("|---|---|---|---|---|")
+    for name, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        print(f"| `{name}` | {len(v)} | {sum(v)/len(v):.1f} | {sum(v):.1f} | {sum(v)/total:.1%} |")
+
+
+def full(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")]
+        print(f"### `{name[:120]}`\n")
+        print("| metric | value | unit |\n|---|---|---|")
+        for m, label in METRICS:
+            if m in h:
+                i = h.index(m)
+                print(f"| {label} (`{m}`) | {r[i]} | {units[i]} |")
+        print()
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
