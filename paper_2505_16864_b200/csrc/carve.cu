@@ -163,28 +163,39 @@ __global__ void __launch_bounds__(128) k_carve_simt(const T* __restrict__ q,
 // =====================================================================================
 namespace tc {
 
-constexpr int BM = 128;          // query rows per tile (== m)
-constexpr int BN = 128;          // key rows per kv block (== m)
+// Work unit of the pipeline: a "half-step" = one 64-key half of a 128-key kv block.
+// S is double-buffered in TMEM per half-step (2 x 64 columns) so the tensor core
+// computes S(t+1) = Q K(t+1)^T while the softmax warps work on S(t); P(t) is written
+// as bf16 over the first 32 columns of its S buffer and consumed by O += P(t) V(t).
+constexpr int BM = 128;           // query rows per tile (== m)
+constexpr int BK = 128;           // keys per kv block (== m)
+constexpr int HN = 64;            // keys per half-step
 constexpr int NUM_THREADS = 192;  // w0 TMA+scheduler, w1 MMA+TMEM owner, w2..w5 softmax
-constexpr int TMEM_COLS = 256;   // S/P [0,128) + O [128, 128+D)
-constexpr int S_COL = 0;
-constexpr int P_COL = 0;         // bf16 P packed 2/col over the first 64 S columns
+constexpr int TMEM_COLS = 256;    // S0 [0,64) S1 [64,128) O [128, 128+D)
 constexpr int O_COL = 128;
-constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: P <= 2^8 before a forced rescale
+constexpr int K_SLOTS = 3;        // K half-tiles in flight
+constexpr int V_SLOTS = 2;        // V half-tiles in flight
+constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: P <= 2^8 between rescales
 
 template <int D>
 struct Smem {
-  static constexpr int TILE_BYTES = BM * D * 2;  // one 128 x D bf16 tile
-  static constexpr int CHUNKS = D / 64;          // 64-element (128 B) swizzle columns
+  static constexpr int Q_BYTES = BM * D * 2;      // 128 x D bf16
+  static constexpr int HALF_BYTES = HN * D * 2;   // 64 x D bf16
+  static constexpr int CHUNKS = D / 64;           // 64-element (128 B) swizzle columns
+  static constexpr int Q_CHUNK = BM * 128;        // bytes per 64-col chunk of Q
+  static constexpr int H_CHUNK = HN * 128;        // bytes per 64-col chunk of a half tile
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + TILE_BYTES;
-  static constexpr int OFF_V = OFF_K + TILE_BYTES;
-  static constexpr int OFF_BAR = OFF_V + TILE_BYTES;
-  static constexpr int BYTES = OFF_BAR + 256 + 1024;  // + barriers + alignment slack
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + K_SLOTS * HALF_BYTES;
+  static constexpr int OFF_BAR = OFF_V + V_SLOTS * HALF_BYTES;
+  static constexpr int BYTES = OFF_BAR + 256;
 };
 
 struct Bars {
-  uint64_t q_full, q_empty, k_full, k_empty, v_full, v_empty, s_full, p_full, o_full;
+  uint64_t q_full, q_empty, o_full, o_done, p_full;
+  uint64_t s_full[2];
+  uint64_t k_full[K_SLOTS], k_empty[K_SLOTS];
+  uint64_t v_full[V_SLOTS], v_empty[V_SLOTS];
   uint64_t sched_full[2], sched_empty[2];
   int sched_item[2];
   uint32_t tmem_base;
@@ -202,6 +213,23 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
 }
 
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float f2_lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2_hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+// packed fp32x2 FMA / ADD (FFMA2 / FADD2 on sm_100a)
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 template <int D>
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     k_carve_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -210,9 +238,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
                const int32_t* __restrict__ kv_cnt, int* __restrict__ counter, int total_items,
                float scale_log2, float beta_log2) {
   using L = Smem<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + L::OFF_Q;
   uint8_t* sK = smem + L::OFF_K;
   uint8_t* sV = smem + L::OFF_V;
@@ -221,15 +247,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
+    if (ptx::smem_u32(smem) & 1023u) __trap();  // 128B-swizzle tiles need 1 KB alignment
     ptx::mbar_init(&bars->q_full, 1);
     ptx::mbar_init(&bars->q_empty, 1);
-    ptx::mbar_init(&bars->k_full, 1);
-    ptx::mbar_init(&bars->k_empty, 1);
-    ptx::mbar_init(&bars->v_full, 1);
-    ptx::mbar_init(&bars->v_empty, 1);
-    ptx::mbar_init(&bars->s_full, 1);
-    ptx::mbar_init(&bars->p_full, 128);
     ptx::mbar_init(&bars->o_full, 1);
+    ptx::mbar_init(&bars->o_done, 1);
+    ptx::mbar_init(&bars->p_full, 128);
+    for (int i = 0; i < 2; ++i) ptx::mbar_init(&bars->s_full[i], 1);
+    for (int i = 0; i < K_SLOTS; ++i) {
+      ptx::mbar_init(&bars->k_full[i], 1);
+      ptx::mbar_init(&bars->k_empty[i], 1);
+    }
+    for (int i = 0; i < V_SLOTS; ++i) {
+      ptx::mbar_init(&bars->v_full[i], 1);
+      ptx::mbar_init(&bars->v_empty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&bars->sched_full[i], 1);
       ptx::mbar_init(&bars->sched_empty[i], 1 + 4);
@@ -264,25 +296,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         const bool vis = qb < s.M_v;
         const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
         const int32_t* list = vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr;
+        const int T = 2 * n;
         ptx::mbar_wait(&bars->q_empty, (it & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&bars->q_full, L::TILE_BYTES);
+        ptx::mbar_arrive_expect_tx(&bars->q_full, L::Q_BYTES);
 #pragma unroll
         for (int c = 0; c < L::CHUNKS; ++c)
-          ptx::tma_load_3d(sQ + c * BM * 128, &tm_q, &bars->q_full, c * 64, qb * BM, h, pol_q);
-        for (int j = 0; j < n; ++j) {
-          const int b = vis ? __ldg(list + j) : j;
-          ptx::mbar_wait(&bars->k_empty, (gk & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(&bars->k_full, L::TILE_BYTES);
+          ptx::tma_load_3d(sQ + c * L::Q_CHUNK, &tm_q, &bars->q_full, c * 64, qb * BM, h, pol_q);
+        auto load_k = [&](int t) {
+          const int b = vis ? __ldg(list + (t >> 1)) : (t >> 1);
+          const int sl = gk % K_SLOTS;
+          ptx::mbar_wait(&bars->k_empty[sl], ((gk / K_SLOTS) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&bars->k_full[sl], L::HALF_BYTES);
 #pragma unroll
           for (int c = 0; c < L::CHUNKS; ++c)
-            ptx::tma_load_3d(sK + c * BN * 128, &tm_k, &bars->k_full, c * 64, b * BN, h, pol_kv);
+            ptx::tma_load_3d(sK + sl * L::HALF_BYTES + c * L::H_CHUNK, &tm_k, &bars->k_full[sl],
+                             c * 64, b * BK + (t & 1) * HN, h, pol_kv);
           ++gk;
-          ptx::mbar_wait(&bars->v_empty, (gv & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(&bars->v_full, L::TILE_BYTES);
+        };
+        auto load_v = [&](int t) {
+          const int b = vis ? __ldg(list + (t >> 1)) : (t >> 1);
+          const int sl = gv % V_SLOTS;
+          ptx::mbar_wait(&bars->v_empty[sl], ((gv / V_SLOTS) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&bars->v_full[sl], L::HALF_BYTES);
 #pragma unroll
           for (int c = 0; c < L::CHUNKS; ++c)
-            ptx::tma_load_3d(sV + c * BN * 128, &tm_v, &bars->v_full, c * 64, b * BN, h, pol_kv);
+            ptx::tma_load_3d(sV + sl * L::HALF_BYTES + c * L::H_CHUNK, &tm_v, &bars->v_full[sl],
+                             c * 64, b * BK + (t & 1) * HN, h, pol_kv);
           ++gv;
+        };
+        // same order the MMA warp consumes: K0, K1, V0, K2, V1, ..., V(T-1)
+        load_k(0);
+        for (int t = 0; t < T; ++t) {
+          if (t + 1 < T) load_k(t + 1);
+          load_v(t);
         }
       }
     }
@@ -290,10 +336,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
     if (lane == 0) {
-      constexpr uint32_t IDESC_S = make_idesc(BM, BN, 0);  // Q (K-major) x K (K-major)
+      constexpr uint32_t IDESC_S = make_idesc(BM, HN, 0);  // Q (K-major) x K (K-major)
       constexpr uint32_t IDESC_O = make_idesc(BM, D, 1);   // P (TMEM)   x V (MN-major)
       const uint32_t aQ = ptx::smem_u32(sQ), aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
-      uint32_t it = 0, g = 0;
+      uint32_t it = 0, gk = 0, gv = 0, gs = 0, gp = 0;
+      auto issue_s = [&]() {  // S(gs) = Q K(gs)^T into buffer gs & 1
+        const int sl = gk % K_SLOTS;
+        ptx::mbar_wait(&bars->k_full[sl], (gk / K_SLOTS) & 1);
+        ptx::tc_fence_after();
+        const uint32_t kbase = aK + sl * L::HALF_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t qoff = (kk >> 2) * L::Q_CHUNK + (kk & 3) * 32;
+          const uint32_t koff = (kk >> 2) * L::H_CHUNK + (kk & 3) * 32;
+          ptx::mma_ss(tmem + (gs & 1) * HN, make_sdesc(aQ + qoff, 16, 1024),
+                      make_sdesc(kbase + koff, 16, 1024), IDESC_S, kk > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(&bars->k_empty[sl]);
+        ptx::mma_commit(&bars->s_full[gs & 1]);
+        ++gk;
+        ++gs;
+      };
       for (;; ++it) {
         const int slot = it & 1;
         ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
@@ -304,34 +367,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         decode_item(item, s, h, qb);
         const bool vis = qb < s.M_v;
         const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
+        const int T = 2 * n;
         ptx::mbar_wait(&bars->q_full, it & 1);
-        for (int j = 0; j < n; ++j, ++g) {
-          // ---- S = Q K^T  (K = D in steps of 16; 128B swizzle rows hold 64 elements)
-          ptx::mbar_wait(&bars->k_full, g & 1);
-          ptx::tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * (BM * 128) + (kk & 3) * 32;
-            const uint64_t da = make_sdesc(aQ + off, 16, 1024);
-            const uint64_t db = make_sdesc(aK + off, 16, 1024);
-            ptx::mma_ss(tmem + S_COL, da, db, IDESC_S, kk > 0 ? 1u : 0u);
-          }
-          ptx::mma_commit(&bars->k_empty);
-          ptx::mma_commit(&bars->s_full);
-          if (j == n - 1) ptx::mma_commit(&bars->q_empty);
-          // ---- O += P V   (K = kv rows in steps of 16 -> 2 KB of V per step)
-          ptx::mbar_wait(&bars->p_full, g & 1);
-          ptx::mbar_wait(&bars->v_full, g & 1);
-          ptx::tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk) {
-            const uint64_t dv = make_sdesc(aV + kk * 16 * 128, BN * 128, 1024);
-            ptx::mma_ts(tmem + O_COL, tmem + P_COL + kk * 8, dv, IDESC_O,
-                        (j > 0 || kk > 0) ? 1u : 0u);
-          }
-          ptx::mma_commit(&bars->v_empty);
+        if (T == 0) {  // cannot come from build_block_mask (diagonal); keep the pipes consistent
+          ptx::mma_commit(&bars->q_empty);
+          ptx::mma_commit(&bars->o_full);
+          continue;
         }
-        if (n == 0) ptx::mma_commit(&bars->q_empty);
+        issue_s();
+        for (int t = 0; t < T; ++t) {
+          if (t + 1 < T) {
+            issue_s();
+            if (t + 2 == T) ptx::mma_commit(&bars->q_empty);
+          }
+          // ---- O += P(t) V(t): A = P from TMEM (32 packed columns), K = 64 keys
+          ptx::mbar_wait(&bars->p_full, gp & 1);
+          const int vs = gv % V_SLOTS;
+          ptx::mbar_wait(&bars->v_full[vs], (gv / V_SLOTS) & 1);
+          ptx::tc_fence_after();
+          const uint32_t vbase = aV + vs * L::HALF_BYTES;
+          const uint32_t pcol = tmem + (gp & 1) * HN;
+#pragma unroll
+          for (int kk = 0; kk < HN / 16; ++kk) {
+            ptx::mma_ts(tmem + O_COL, pcol + kk * 8,
+                        make_sdesc(vbase + kk * 16 * 128, L::H_CHUNK, 1024), IDESC_O,
+                        (t > 0 || kk > 0) ? 1u : 0u);
+          }
+          ptx::mma_commit(&bars->v_empty[vs]);
+          ptx::mma_commit(&bars->o_done);
+          ++gv;
+          ++gp;
+        }
         ptx::mma_commit(&bars->o_full);
       }
     }
@@ -354,63 +420,63 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       const bool vis = qb < s.M_v;
       const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
       const int32_t* list = vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr;
+      const int T = 2 * n;
       float m_run = -INFINITY, l_run = 0.f;
-      for (int j = 0; j < n; ++j, ++g) {
-        const int b = vis ? __ldg(list + j) : j;
-        const int kvalid = block_valid(b, BN, s.M_v, s.n_valid, s.n_cond);
-        const float bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
-        ptx::mbar_wait(&bars->s_full, g & 1);
+      int b = 0, kvalid = BK;
+      float bias = 0.f;
+      for (int t = 0; t < T; ++t, ++g) {
+        if ((t & 1) == 0) {
+          b = vis ? __ldg(list + (t >> 1)) : (t >> 1);
+          kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond);
+          bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
+        }
+        const int hvalid = kvalid - (t & 1) * HN;  // valid keys in this half (may be <= 0)
+        ptx::mbar_wait(&bars->s_full[g & 1], (g >> 1) & 1);
         ptx::tc_fence_after();
-        uint32_t sr[4][32];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(t_row + S_COL + c * 32, sr[c]);
+        uint32_t sr[64];
+        ptx::tmem_ld32(t_row + (g & 1) * HN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+        ptx::tmem_ld32(t_row + (g & 1) * HN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
         ptx::tmem_wait_ld();
-        float mx = -INFINITY;
+        if (hvalid < HN) {  // padding keys of a partial block -> -inf (attention.py:193)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            float t = fmaf(__uint_as_float(sr[c][e]), scale_log2, bias);
-            if (c * 32 + e >= kvalid) t = -INFINITY;
-            sr[c][e] = __float_as_uint(t);
-            mx = fmaxf(mx, t);
-          }
-        const float m_new = fmaxf(m_run, mx);
-        float m_use = m_run, alpha = 1.f;
-        const bool need = (j == 0) ? false : (m_new > m_run + RESCALE_THRESHOLD);
-        if (j == 0 || need) m_use = m_new;
-        if (need) alpha = ptx::ex2(m_run - m_new);
-        float psum = 0.f;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float p0 = ptx::ex2(__uint_as_float(sr[c][2 * e]) - m_use);
-            const float p1 = ptx::ex2(__uint_as_float(sr[c][2 * e + 1]) - m_use);
-            psum += p0 + p1;
-            pk[e] = ptx::pack_bf16(p0, p1);
-          }
-          // 16 packed columns per 32 scores; store as half of a x32 store pair
-#pragma unroll
-          for (int e = 0; e < 16; ++e) sr[c][e] = pk[e];
+          for (int e = 0; e < 64; ++e)
+            if (e >= hvalid) sr[e] = __float_as_uint(-INFINITY);
         }
-        {
-          uint32_t a0[32], a1[32];
+        float mx8[8];
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            a0[e] = sr[0][e];
-            a0[16 + e] = sr[1][e];
-            a1[e] = sr[2][e];
-            a1[16 + e] = sr[3][e];
-          }
-          ptx::tmem_st32(t_row + P_COL, a0);
-          ptx::tmem_st32(t_row + P_COL + 32, a1);
+        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
+#pragma unroll
+        for (int e = 8; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(sr[e]));
+        const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                 fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        // block max in the scaled log2 domain (scale > 0 keeps the argmax)
+        const float m_blk = (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
+        const float m_new = fmaxf(m_run, m_blk);
+        const bool first = (t == 0);
+        const bool need = !first && (m_new > m_run + RESCALE_THRESHOLD);
+        const float m_use = (first || need) ? m_new : m_run;
+        const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
+        // p = 2^(s * scale_log2 + bias - m_use): one FFMA2 per two keys
+        const float c0 = bias - m_use;
+        const uint64_t sc2 = f2_pack(scale_log2, scale_log2), c02 = f2_pack(c0, c0);
+        uint64_t acc2[4] = {0, 0, 0, 0};
+        uint32_t pk[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const uint64_t x = ffma2(f2_pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])),
+                                   sc2, c02);
+          const float p0 = ptx::ex2(f2_lo(x)), p1 = ptx::ex2(f2_hi(x));
+          acc2[e & 3] = fadd2(acc2[e & 3], f2_pack(p0, p1));
+          pk[e] = ptx::pack_bf16(p0, p1);
         }
-        l_run = l_run * alpha + psum;
+        ptx::tmem_st32(t_row + (g & 1) * HN, pk);
+        const uint64_t sum2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
+        l_run = l_run * alpha + (f2_lo(sum2) + f2_hi(sum2));
         m_run = m_use;
-        // lazy O correction: S_j complete => PV_{j-1} complete (in-order tensor pipe)
         if (__any_sync(0xffffffffu, need)) {
+          // O is final only once PV(t-1) retired: o_done completes once per PV
+          ptx::mbar_wait(&bars->o_done, (g - 1) & 1);
+          ptx::tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
             uint32_t ov[32];
@@ -481,12 +547,12 @@ static PFN_encodeTiled get_encode() {
 
 // (d, N_pad, H) bf16 view with box (64, 128, 1), 128-byte swizzle
 static int make_tmap(CUtensorMap* tm, const void* base, int d, int64_t n_pad, int H, int64_t sh,
-                     int64_t sn) {
+                     int64_t sn, int box_rows) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return set_error(TCB_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)n_pad, (cuuint64_t)H};
   cuuint64_t strides[2] = {(cuuint64_t)sn * 2, (cuuint64_t)sh * 2};
-  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -545,9 +611,9 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
   CUtensorMap tq, tk, tv;
   const int64_t n_pad = (int64_t)s.M_total * s.m;
   int rc;
-  if ((rc = make_tmap(&tq, q, D, n_pad, s.H, s.sh, s.sn))) return rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn))) return rc;
+  if ((rc = make_tmap(&tq, q, D, n_pad, s.H, s.sh, s.sn, tc::BM))) return rc;
+  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::HN))) return rc;
+  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::HN))) return rc;
   const int smem = tc::Smem<D>::BYTES;
   static bool attr_set = false;
   if (!attr_set) {

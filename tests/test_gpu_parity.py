@@ -262,3 +262,17 @@ def test_toy_pipeline_matches_reference():
     np.testing.assert_allclose([s["effective_sparsity"] for s in res.report["steps"]],
                                g["sparsity"])
     np.testing.assert_allclose(res.latent, g["latent"], rtol=1e-4, atol=1e-4)
+
+
+def test_select_general_rows_vs_oracle():
+    # user-supplied R: negatives (non-monotone prefix), zeros, exact ties, tiny values
+    rng = np.random.default_rng(9)
+    for n_cols in (3, 64, 200, 931):
+        R = rng.standard_normal((2, 5, n_cols))
+        R[0, 0] = 0.0
+        R[0, 1] = 1.0 / n_cols
+        R[1, 2] = np.abs(R[1, 2]) * 1e-300
+        R[1, 3, : n_cols // 2] = 0.25
+        for k, p in ((0.05, 0.0), (0.2, 0.3), (0.5, 0.7), (1.0, 0.1)):
+            got = tcb.importance_mask(R, tcb.SelectionParams(k=k, p=p), n_cols)
+            assert np.array_equal(got, oracle.select_topk(R, k, p, n_cols)), (n_cols, k, p)
