@@ -155,11 +155,12 @@ def run_gpu(args):
         _native.call("tcb_block_pool", qh.data_ptr(), kh.data_ptr(), 1, sh, sn, Hl, D, M, Mv, Mt,
                      layout.n_valid, layout.n_cond, pq.data_ptr(), pk.data_ptr(), sptr)
         if marks: marks[1].record()
-        _native.call("tcb_block_relevance", pq.data_ptr(), Mt, pk.data_ptr(), Hl, Mv, Mt, D,
+        _native.call("tcb_block_scores", pq.data_ptr(), Mt, pk.data_ptr(), Hl, Mv, Mt, D,
                      R.data_ptr(), sptr)
         if marks: marks[2].record()
-        _native.call("tcb_block_select", R.data_ptr(), Hl, Mv, Mt, adja.data_ptr(), words, n_floor,
-                     float(P_CUT), 1, bits.data_ptr(), kv_idx.data_ptr(), kv_cnt.data_ptr(), sptr)
+        _native.call("tcb_block_select_scores", R.data_ptr(), Hl, Mv, Mt, adja.data_ptr(), words,
+                     n_floor, float(P_CUT), 1, bits.data_ptr(), kv_idx.data_ptr(),
+                     kv_cnt.data_ptr(), sptr)
         if marks: marks[3].record()
         _native.call("tcb_carve_fwd", qh.data_ptr(), kh.data_ptr(), vh.data_ptr(), out.data_ptr(), 1,
                      sh, sn, kv_idx.data_ptr(), kv_cnt.data_ptr(), Hl, D, M, Mv, Mt, layout.n_valid,
@@ -282,8 +283,9 @@ def run_gpu(args):
                    "parallelism": f"ulysses-heads{world}" if world > 1 else "single",
                    "l2": "no flush: Q/K/V/O = 2.9 GB per layer > 126 MB L2"},
         "kept_block_tflops": round(carve_tflops, 1),
-        "kernels_ms": {"block_pool": round(float(k_pool), 4), "block_relevance": round(float(k_rel), 4),
-                       "block_select": round(float(k_sel), 4), "carve_fwd": round(float(k_carve), 4)},
+        "kernels_ms": {"block_pool": round(float(k_pool), 4), "block_scores": round(float(k_rel), 4),
+                       "block_softmax_select": round(float(k_sel), 4),
+                       "carve_fwd": round(float(k_carve), 4)},
         "roofline": {"bound": "tensor", "kernel": "k_carve_tc<128>",
                      "achieved": round(carve_tflops, 1), "peak": tf_sust, "unit": "TFLOP/s",
                      "frac": round(carve_tflops / tf_sust, 4),

@@ -82,6 +82,18 @@ int tcb_block_select(const double* R, int H, int M_v, int M_total, const uint32_
                      int n_floor, double p, int with_union, uint32_t* bits, int32_t* kv_idx,
                      int32_t* kv_cnt, void* stream);
 
+/* K4a -- scaled pooled scores S[h,i,j] = pq[h,i].pk[h,j] / sqrt(d) (masks.py:130-131),
+ * float64, i < rows, j < M_total.  First half of tcb_block_relevance. */
+int tcb_block_scores(const double* pq, int pq_blocks, const double* pk, int H, int rows,
+                     int M_total, int d, double* S, void* stream);
+
+/* K4b+K5 fused -- S (from tcb_block_scores) is turned into R in place (row softmax,
+ * masks.py:132-134, numpy pairwise row sums) and selected like tcb_block_select:
+ * the build_block_mask fast path (masks.py:178-199) in two launches. */
+int tcb_block_select_scores(double* S, int H, int M_v, int M_total, const uint32_t* adja,
+                            int words, int n_floor, double p, int with_union, uint32_t* bits,
+                            int32_t* kv_idx, int32_t* kv_cnt, void* stream);
+
 /* Mask conversions for user-built BlockMask(bits=bool array) (masks.py:78-95). */
 int tcb_mask_pack(const uint8_t* dense, int64_t rows, int M_total, int words, uint32_t* bits,
                   int32_t* kv_idx, int32_t* kv_cnt, void* stream);

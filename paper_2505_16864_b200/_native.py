@@ -34,6 +34,8 @@ SIGNATURES = {
     "tcb_block_pool": [_P, _P, _I, _I64, _I64, _I, _I, _I, _I, _I, _I64, _I64, _P, _P, _P],
     "tcb_block_relevance": [_P, _I, _P, _I, _I, _I, _I, _P, _P],
     "tcb_block_select": [_P, _I, _I, _I, _P, _I, _I, _D, _I, _P, _P, _P, _P],
+    "tcb_block_scores": [_P, _I, _P, _I, _I, _I, _I, _P, _P],
+    "tcb_block_select_scores": [_P, _I, _I, _I, _P, _I, _I, _D, _I, _P, _P, _P, _P],
     "tcb_mask_pack": [_P, _I64, _I, _I, _P, _P, _P, _P],
     "tcb_mask_unpack": [_P, _I64, _I, _I, _P, _P],
     "tcb_carve_fwd": [_P, _P, _P, _P, _I, _I64, _I64, _P, _P, _I, _I, _I, _I, _I, _I64, _I64,

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <math.h>
+#include <stdlib.h>
 
 namespace tcb {
 
@@ -230,7 +231,32 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   return d;
 }
 
-template <int D>
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));  // FMNMX3
+  return d;
+}
+
+// 2^x for a packed pair on the FMA pipe (offloads MUFU): x = j + f, j = rint(x) via the
+// 1.5*2^23 magic add, 2^f by a degree-3 minimax polynomial on [-0.5, 0.5] (max rel err
+// 7.5e-5, far below the bf16 rounding of P), 2^j added straight into the exponent bits.
+// x is clamped at -126 so the exponent never underflows into the sign bit.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+  const float x0 = fmaxf(f2_lo(x), -126.f), x1 = fmaxf(f2_hi(x), -126.f);
+  const uint64_t xc = f2_pack(x0, x1);
+  const uint64_t magic = f2_pack(12582912.f, 12582912.f);
+  const uint64_t t = fadd2(xc, magic);
+  const uint64_t jf = fadd2(t, f2_pack(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(jf, f2_pack(-1.f, -1.f), xc);
+  uint64_t p = ffma2(f, f2_pack(0.05517132f, 0.05517132f), f2_pack(0.24261054f, 0.24261054f));
+  p = ffma2(p, f, f2_pack(0.69326097f, 0.69326097f));
+  p = ffma2(p, f, f2_pack(0.99992812f, 0.99992812f));
+  const uint32_t lo = (uint32_t)p + ((uint32_t)t << 23);
+  const uint32_t hi = (uint32_t)(p >> 32) + ((uint32_t)(t >> 32) << 23);
+  return (uint64_t)lo | ((uint64_t)hi << 32);
+}
+
+template <int D, int EMU>
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     k_carve_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
@@ -446,9 +472,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
 #pragma unroll
         for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
 #pragma unroll
-        for (int e = 8; e < 64; ++e) mx8[e & 7] = fmaxf(mx8[e & 7], __uint_as_float(sr[e]));
-        const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                                 fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        for (int e = 8; e < 64; e += 16)
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            mx8[q] = fmax3(mx8[q], __uint_as_float(sr[e + q]), __uint_as_float(sr[e + 8 + q]));
+        const float mraw = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]),
+                                 fmaxf(mx8[6], mx8[7]));
         // block max in the scaled log2 domain (scale > 0 keeps the argmax)
         const float m_blk = (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
         const float m_new = fmaxf(m_run, m_blk);
@@ -465,7 +494,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         for (int e = 0; e < 32; ++e) {
           const uint64_t x = ffma2(f2_pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])),
                                    sc2, c02);
-          const float p0 = ptx::ex2(f2_lo(x)), p1 = ptx::ex2(f2_hi(x));
+          float p0, p1;
+          if ((e & 7) >= 8 - EMU) {  // FMA-pipe exp2 for EMU of every 8 pairs
+            const uint64_t pp = exp2_poly2(x);
+            p0 = f2_lo(pp);
+            p1 = f2_hi(pp);
+          } else {
+            p0 = ptx::ex2(f2_lo(x));
+            p1 = ptx::ex2(f2_hi(x));
+          }
           acc2[e & 3] = fadd2(acc2[e & 3], f2_pack(p0, p1));
           pk[e] = ptx::pack_bf16(p0, p1);
         }
@@ -604,7 +641,7 @@ static int launch_simt(const void* q, const void* k, const void* v, void* o, int
   return check_launch("k_carve_simt");
 }
 
-template <int D>
+template <int D, int EMU>
 static int launch_tc(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
                      const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
                      cudaStream_t st) {
@@ -617,7 +654,7 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
   const int smem = tc::Smem<D>::BYTES;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc::k_carve_tc<D>,
+    cudaError_t e = cudaFuncSetAttribute(tc::k_carve_tc<D, EMU>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
     attr_set = true;
@@ -632,7 +669,7 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
   if (grid > total) grid = total;
   const float LOG2E = 1.4426950408889634f;
   const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  tc::k_carve_tc<D><<<grid, tc::NUM_THREADS, smem, st>>>(tq, tk, tv, (__nv_bfloat16*)o, s, kv_idx,
+  tc::k_carve_tc<D, EMU><<<grid, tc::NUM_THREADS, smem, st>>>(tq, tk, tv, (__nv_bfloat16*)o, s, kv_idx,
                                                          kv_cnt, work, total, scale_log2,
                                                          beta * LOG2E);
   return check_launch("k_carve_tc");
@@ -662,6 +699,21 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
   const bool tc_ok = dtype == TCB_BF16 && m == 128 && (d == 128 || d == 64) && aligned && work &&
                      M_v > 0;
   if (!tc_ok) return launch_simt(q, k, v, o, dtype, s, kv_idx, kv_cnt, beta, as_stream(stream));
-  if (d == 128) return launch_tc<128>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, as_stream(stream));
-  return launch_tc<64>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, as_stream(stream));
+  // pairs (of 8) whose exp2 runs on the FMA pipe instead of MUFU; TCB_CARVE_EMU overrides
+  static int emu = -1;
+  if (emu < 0) {
+    const char* env = getenv("TCB_CARVE_EMU");
+    emu = env ? atoi(env) : 2;
+    if (emu != 0 && emu != 2 && emu != 3 && emu != 4) emu = 2;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (d == 128) {
+    switch (emu) {
+      case 0: return launch_tc<128, 0>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
+      case 3: return launch_tc<128, 3>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
+      case 4: return launch_tc<128, 4>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
+      default: return launch_tc<128, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
+    }
+  }
+  return launch_tc<64, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
 }

@@ -104,14 +104,15 @@ __global__ void __launch_bounds__(128) k_pool(const T* __restrict__ x0, const T*
 }
 
 // ---------------------------------------------------------------------------
-// K4 relevance: R[h,i,:] = softmax(pq_i . pk_j / sqrt(d)).  CTA = (head, 32 rows);
-// float64 register-tiled product (2 rows x 4 cols per thread) over 64-column
-// chunks of pk staged in smem; raw scaled scores go to R, then one thread per row
-// does max / exp / numpy-pairwise sum / divide in place (masks.py:130-134).
+// K4 relevance: R[h,i,:] = softmax(pq_i . pk_j / sqrt(d)) in float64, two launches:
+//  * k_scores: 64x64 output tiles per CTA, 4x4 register tile per thread, 32-wide d
+//    chunks of pq/pk staged transposed in smem; writes pq.pk / sqrt(d) (the
+//    reference divides after the product, masks.py:130-131);
+//  * k_row_softmax: one warp per row -- max, exp, numpy-pairwise sum, divide
+//    (masks.py:132-134), coalesced over the row.
 // ---------------------------------------------------------------------------
-constexpr int RT_ROWS = 32;
-constexpr int RT_COLS = 64;
-constexpr int RT_KC = 32;  // d-chunk staged per step
+constexpr int ST_TILE = 64;
+constexpr int ST_KC = 32;
 
 // numpy's pairwise summation (PW_BLOCKSIZE 128, 8-way unrolled leaves): the
 // recursion splits n > 128 at n2 = n/2 - (n/2)%8 and sums left + right.  The leaves
@@ -210,82 +211,74 @@ __device__ double warp_pairwise_sum(const double* row, int n, double* scratch) {
   return total;
 }
 
-__global__ void __launch_bounds__(256) k_relevance(const double* __restrict__ pq, int pq_blocks,
-                                                   const double* __restrict__ pk, int rows,
-                                                   int M_total, int d, double inv_sqrt_unused,
-                                                   double sqrt_d, double* __restrict__ R) {
-  // phase 1 tiles and phase 2 per-warp scratch share one buffer
-  __shared__ double sbuf[8 * 2 * PW_MAX_LEAVES];
-  static_assert(RT_ROWS * (RT_KC + 1) + RT_KC * (RT_COLS + 1) <= 8 * 2 * PW_MAX_LEAVES, "smem");
-  double(*sA)[RT_KC + 1] = reinterpret_cast<double(*)[RT_KC + 1]>(sbuf);
-  double(*sB)[RT_COLS + 1] = reinterpret_cast<double(*)[RT_COLS + 1]>(sbuf + RT_ROWS * (RT_KC + 1));
-  const int h = blockIdx.y;
-  const int r0 = blockIdx.x * RT_ROWS;
-  const int tid = threadIdx.x;
-  const int rg = tid >> 4;  // 16 row groups x 2 rows
-  const int cg = tid & 15;  // 16 col groups x 4 cols (cg, cg+16, cg+32, cg+48)
+__global__ void __launch_bounds__(256) k_scores(const double* __restrict__ pq, int pq_blocks,
+                                                const double* __restrict__ pk, int rows,
+                                                int M_total, int d, double sqrt_d,
+                                                double* __restrict__ R) {
+  __shared__ double sA[ST_KC][ST_TILE + 1];
+  __shared__ double sB[ST_KC][ST_TILE + 1];
+  const int h = blockIdx.z;
+  const int r0 = blockIdx.y * ST_TILE, c0 = blockIdx.x * ST_TILE;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   const double* A = pq + (int64_t)h * pq_blocks * d;
   const double* B = pk + (int64_t)h * M_total * d;
-  double* Rh = R + (int64_t)h * rows * M_total;
-  for (int c0 = 0; c0 < M_total; c0 += RT_COLS) {
-    double acc[2][4];
+  double acc[4][4];
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    for (int k0 = 0; k0 < d; k0 += RT_KC) {
-      __syncthreads();
-      for (int e = tid; e < RT_ROWS * RT_KC; e += 256) {
-        int rr = e / RT_KC, kk = e % RT_KC;
-        int gr = r0 + rr, gk = k0 + kk;
-        sA[rr][kk] = (gr < rows && gk < d) ? A[(int64_t)gr * d + gk] : 0.0;
-      }
-      for (int e = tid; e < RT_COLS * RT_KC; e += 256) {
-        int cc = e / RT_KC, kk = e % RT_KC;
-        int gc = c0 + cc, gk = k0 + kk;
-        sB[kk][cc] = (gc < M_total && gk < d) ? B[(int64_t)gc * d + gk] : 0.0;
-      }
-      __syncthreads();
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int k0 = 0; k0 < d; k0 += ST_KC) {
+    // coalesced along d, stored transposed (k-major) for the inner product loop
+    for (int e = tid; e < ST_TILE * ST_KC; e += 256) {
+      const int rr = e / ST_KC, kk = e - rr * ST_KC;
+      const int gk = k0 + kk;
+      const int gr = r0 + rr, gc = c0 + rr;
+      sA[kk][rr] = (gr < rows && gk < d) ? A[(int64_t)gr * d + gk] : 0.0;
+      sB[kk][rr] = (gc < M_total && gk < d) ? B[(int64_t)gc * d + gk] : 0.0;
+    }
+    __syncthreads();
 #pragma unroll 8
-      for (int kk = 0; kk < RT_KC; ++kk) {
-        double a0 = sA[2 * rg][kk], a1 = sA[2 * rg + 1][kk];
+    for (int kk = 0; kk < ST_KC; ++kk) {
+      double a[4], bv[4];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          double bv = sB[kk][cg + 16 * b];
-          acc[0][b] = fma(a0, bv, acc[0][b]);
-          acc[1][b] = fma(a1, bv, acc[1][b]);
-        }
-      }
+      for (int i = 0; i < 4; ++i) a[i] = sA[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = sB[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bv[j], acc[i][j]);
     }
+    __syncthreads();
+  }
+  double* Rh = R + (int64_t)h * rows * M_total;
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      int gr = r0 + 2 * rg + a;
-      if (gr >= rows) continue;
+  for (int i = 0; i < 4; ++i) {
+    const int gr = r0 + ty + 16 * i;
+    if (gr >= rows) continue;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        int gc = c0 + cg + 16 * b;
-        if (gc < M_total) Rh[(int64_t)gr * M_total + gc] = acc[a][b] / sqrt_d;  // masks.py:131
-      }
+    for (int j = 0; j < 4; ++j) {
+      const int gc = c0 + tx + 16 * j;
+      if (gc < M_total) Rh[(int64_t)gr * M_total + gc] = acc[i][j] / sqrt_d;
     }
   }
-  __syncthreads();
-  // per-row softmax (masks.py:132-134): one warp per row, lanes stride the row
-  // (coalesced); the row sum is numpy's pairwise order (bit-faithful).
-  const int warp = tid >> 5, lane = tid & 31;
-  double* scratch = sbuf + warp * 2 * PW_MAX_LEAVES;
-  for (int rr = warp; rr < RT_ROWS; rr += 8) {
-    if (r0 + rr >= rows) break;
-    double* row = Rh + (int64_t)(r0 + rr) * M_total;
-    double mx = -INFINITY;
-    for (int j = lane; j < M_total; j += 32) mx = fmax(mx, row[j]);
+}
+
+__global__ void __launch_bounds__(256) k_row_softmax(double* __restrict__ R, int64_t n_rows,
+                                                     int M_total) {
+  __shared__ double sbuf[8 * 2 * PW_MAX_LEAVES];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * 8 + warp;
+  if (r >= n_rows) return;
+  double* row = R + r * M_total;
+  double mx = -INFINITY;
+  for (int j = lane; j < M_total; j += 32) mx = fmax(mx, row[j]);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    for (int j = lane; j < M_total; j += 32) row[j] = exp(row[j] - mx);
-    __syncwarp();
-    const double ssum = warp_pairwise_sum(row, M_total, scratch);
-    for (int j = lane; j < M_total; j += 32) row[j] = row[j] / ssum;
-    __syncwarp();
-  }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  for (int j = lane; j < M_total; j += 32) row[j] = exp(row[j] - mx);
+  __syncwarp();
+  const double ssum = warp_pairwise_sum(row, M_total, sbuf + warp * 2 * PW_MAX_LEAVES);
+  for (int j = lane; j < M_total; j += 32) row[j] = row[j] / ssum;
 }
 
 // ---------------------------------------------------------------------------
@@ -352,155 +345,135 @@ __device__ void emit_row(uint32_t* sbits, int words, int M_total, uint32_t* __re
   }
 }
 
-constexpr int SEL_THREADS = 256;
+// ---- warp-per-row selection ------------------------------------------------------
+constexpr int SW_WARPS = 4;  // rows (one warp each) per CTA
+constexpr unsigned FULL = 0xffffffffu;
 
-struct SelSmem {
-  uint32_t hist[256];
-  double hsum[256];
-  int warp_tot[SEL_THREADS / 32];
+struct RadixState {
   uint64_t prefix, mask;
-  int remaining, n_cut, n_keep, k_ub, flag;
-  double cum;
+  int remaining;  // count mode: rank still needed inside the bin; weighted: count ranked before
+  int binc;       // elements in the chosen bin
+  double cum;     // weighted: value sum ranked before the candidate bin
+  int flag;       // weighted: the row total never exceeds p
 };
 
-// Block-wide inclusive-exclusive scan helper: returns the exclusive prefix of v over
-// threads in tid order; *total gets the block sum.
-__device__ int block_excl_scan(int v, SelSmem& S, int* total) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  int incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) S.warp_tot[w] = incl;
-  __syncthreads();
-  int base = 0, tot = 0;
-  for (int i = 0; i < SEL_THREADS / 32; ++i) {
-    if (i < w) base += S.warp_tot[i];
-    tot += S.warp_tot[i];
-  }
-  __syncthreads();
-  *total = tot;
-  return base + incl - v;
-}
-
-// MSB-first radix select of the K-th element (1-based) of the (key, column) order over
-// keys[0, n).  On return S.prefix/S.mask/S.remaining describe the top-K set:
-// {(key & mask) < prefix}  U  {first `remaining` columns (ascending) with (key & mask) == prefix}.
-// weighted: digit choice by cumulative value sum crossing `p` (K ignored) -> bound on n_cut.
-__device__ void radix_select(const uint64_t* keys, int n, int K, bool weighted, double p,
-                             SelSmem& S) {
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    S.prefix = 0; S.mask = 0; S.remaining = K; S.cum = 0.0; S.flag = 0;
-  }
-  __syncthreads();
+// MSB-first radix select over the (key, column) order of keys[0, n) by one warp.
+// Count mode: the top-K set is {(key & mask) < prefix} U {first `remaining` columns with
+// (key & mask) == prefix}.  Weighted mode: locates where the cumulative value sum first
+// exceeds p; remaining + binc then bounds the rank of that crossing element.
+__device__ RadixState warp_radix(const uint64_t* keys, int n, int K, bool weighted, double p,
+                                 uint32_t* hist, double* hsum) {
+  const int lane = threadIdx.x & 31;
+  RadixState r{0ull, 0ull, weighted ? 0 : K, 0, 0.0, 0};
   for (int byte = 7; byte >= 0; --byte) {
-    for (int i = tid; i < 256; i += SEL_THREADS) {
-      S.hist[i] = 0u;
-      S.hsum[i] = 0.0;
+    for (int i = lane; i < 256; i += 32) {
+      hist[i] = 0u;
+      if (weighted) hsum[i] = 0.0;
     }
-    __syncthreads();
-    const uint64_t pre = S.prefix, msk = S.mask;
+    __syncwarp();
     const int sh = byte * 8;
-    for (int j = tid; j < n; j += SEL_THREADS) {
-      const uint64_t k = keys[j];
-      if ((k & msk) != pre) continue;
-      const int dg = (int)((k >> sh) & 0xFF);
-      atomicAdd(&S.hist[dg], 1u);
-      if (weighted) atomicAdd(&S.hsum[dg], key_value(k));
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      bool cand = false;
+      int dg = 0;
+      uint64_t k = 0;
+      if (j < n) {
+        k = keys[j];
+        cand = (k & r.mask) == r.prefix;
+        dg = (int)((k >> sh) & 0xFF);
+      }
+      const unsigned act = __ballot_sync(FULL, cand);
+      if (cand) {
+        const unsigned peers = __match_any_sync(act, dg);
+        if (lane == __ffs(peers) - 1) atomicAdd(&hist[dg], (uint32_t)__popc(peers));
+        if (weighted) atomicAdd(&hsum[dg], key_value(k));
+      }
     }
-    __syncthreads();
-    if (tid < 32) {
-      // lane owns bins [8*lane, 8*lane+8): local totals, then warp scan over lanes
-      uint32_t c[8];
-      double sm[8];
-      uint32_t ct = 0;
-      double st = 0.0;
+    __syncwarp();
+    uint32_t c[8];
+    double sm[8];
+    uint32_t ct = 0;
+    double st = 0.0;
 #pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      c[i] = hist[lane * 8 + i];
+      sm[i] = weighted ? hsum[lane * 8 + i] : 0.0;
+      ct += c[i];
+      st += sm[i];
+    }
+    uint32_t cin = ct;
+    double sin_ = st;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, cin, o);
+      const double z = __shfl_up_sync(FULL, sin_, o);
+      if (lane >= o) { cin += y; sin_ += z; }
+    }
+    uint32_t cex = cin - ct;
+    double sex = sin_ - st;
+    bool hit;
+    if (weighted) hit = (r.cum + sin_ > p) && !(r.cum + sex > p);
+    else hit = (cex < (uint32_t)r.remaining) && ((uint32_t)r.remaining <= cin);
+    const unsigned bal = __ballot_sync(FULL, hit);
+    if (bal == 0u) {  // weighted: candidates never push the sum past p
+      r.flag = 1;
+      return r;
+    }
+    const int src = __ffs(bal) - 1;
+    int bin = 7;
+    if (lane == src) {
       for (int i = 0; i < 8; ++i) {
-        c[i] = S.hist[tid * 8 + i];
-        sm[i] = S.hsum[tid * 8 + i];
-        ct += c[i];
-        st += sm[i];
-      }
-      uint32_t cin = ct;
-      double sin_ = st;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, cin, o);
-        const double z = __shfl_up_sync(0xffffffffu, sin_, o);
-        if (tid >= o) { cin += y; sin_ += z; }
-      }
-      uint32_t cex = cin - ct;
-      double sex = sin_ - st;
-      const int rem = S.remaining;
-      const double base = S.cum;
-      // find the lane whose bins contain the target, then the bin
-      bool hit;
-      if (weighted) hit = (base + sin_ > p) && !(base + sex > p);
-      else hit = (cex < (uint32_t)rem) && ((uint32_t)rem <= cin);
-      const unsigned bal = __ballot_sync(0xffffffffu, hit);
-      if (bal == 0u) {
-        // weighted: the total never exceeds p -> no cutoff inside this candidate set
-        if (tid == 0) S.flag = 1;
-      } else if (tid == __ffs(bal) - 1) {
-        int bin = 7;
-        for (int i = 0; i < 8; ++i) {
-          const bool in = weighted ? (base + sex + sm[i] > p) : ((uint32_t)rem <= cex + c[i]);
-          if (in) { bin = i; break; }
-          cex += c[i];
-          sex += sm[i];
-        }
-        const int dg = tid * 8 + bin;
-        S.prefix = pre | ((uint64_t)dg << sh);
-        S.mask = msk | (0xFFull << sh);
-        if (weighted) {
-          S.cum = base + sex;
-          S.remaining = rem + (int)cex;  // elements ranked before the candidate bin
-          S.hist[0] = c[bin];      // stash candidates-in-bin for the early-exit test
-        } else {
-          S.remaining = rem - (int)cex;
-          S.hist[0] = c[bin];
-        }
+        const bool in = weighted ? (r.cum + sex + sm[i] > p) : ((uint32_t)r.remaining <= cex + c[i]);
+        if (in) { bin = i; break; }
+        cex += c[i];
+        sex += sm[i];
       }
     }
-    __syncthreads();
-    if (S.flag) return;
-    if (!weighted && (int)S.hist[0] == S.remaining) return;  // whole bin selected
-    if (weighted && S.hist[0] == 1u) return;                 // unique crossing element
-    __syncthreads();
+    const int dg = __shfl_sync(FULL, src * 8 + bin, src);
+    const uint32_t before = __shfl_sync(FULL, cex, src);
+    const double before_sum = __shfl_sync(FULL, sex, src);
+    const uint32_t binc = __shfl_sync(FULL, c[bin], src);
+    r.prefix |= (uint64_t)dg << sh;
+    r.mask |= 0xFFull << sh;
+    r.binc = (int)binc;
+    if (weighted) {
+      r.cum += before_sum;
+      r.remaining += (int)before;
+      if (binc == 1u) return r;  // the crossing element is identified
+    } else {
+      r.remaining -= (int)before;
+      if ((int)binc == r.remaining) return r;  // whole bin selected
+    }
+    __syncwarp();
+  }
+  return r;
+}
+
+// Visit the top-K set of `r` in ascending column order: fn(j, slot).
+template <typename F>
+__device__ void warp_topk_visit(const uint64_t* keys, int n, const RadixState& r, F fn) {
+  const int lane = threadIdx.x & 31;
+  int eq_base = 0, slot_base = 0;
+  for (int j0 = 0; j0 < n; j0 += 32) {
+    const int j = j0 + lane;
+    uint64_t km = ~0ull;
+    if (j < n) km = keys[j] & r.mask;
+    const bool eq = (j < n) && km == r.prefix;
+    const unsigned eqb = __ballot_sync(FULL, eq);
+    const int eq_rank = eq_base + __popc(eqb & ((1u << lane) - 1u));
+    const bool sel = (j < n) && (km < r.prefix || (eq && eq_rank < r.remaining));
+    const unsigned selb = __ballot_sync(FULL, sel);
+    if (sel) fn(j, slot_base + __popc(selb & ((1u << lane) - 1u)));
+    eq_base += __popc(eqb);
+    slot_base += __popc(selb);
   }
 }
 
-// selected(j) for the top-K set described by S (see radix_select); also the rank of
-// equal-prefix columns in ascending column order via a block scan.
-__device__ void mark_selected(const uint64_t* keys, int n, SelSmem& S, uint32_t* sbits) {
-  const int tid = threadIdx.x;
-  const uint64_t pre = S.prefix, msk = S.mask;
-  const int rem = S.remaining;
-  // contiguous chunk per thread keeps ascending column order across the scan
-  const int per = (n + SEL_THREADS - 1) / SEL_THREADS;
-  const int j0 = tid * per, j1 = min(n, j0 + per);
-  int eq = 0;
-  for (int j = j0; j < j1; ++j) eq += ((keys[j] & msk) == pre);
-  int total;
-  int rank = block_excl_scan(eq, S, &total);
-  for (int j = j0; j < j1; ++j) {
-    const uint64_t km = keys[j] & msk;
-    bool sel = km < pre;
-    if (km == pre) sel = (rank++ < rem);
-    if (sel) atomicOr(sbits + (j >> 5), 1u << (j & 31));
-  }
-}
-
-// Bitonic sort (ascending (key, col)) of cnt <= n_pow2 entries in smem.
-__device__ void bitonic_sort(uint64_t* key, int* col, int n_pow2) {
-  const int tid = threadIdx.x;
-  for (int kk = 2; kk <= n_pow2; kk <<= 1) {
+__device__ void warp_bitonic(uint64_t* key, int* col, int np2) {
+  const int lane = threadIdx.x & 31;
+  for (int kk = 2; kk <= np2; kk <<= 1) {
     for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-      for (int t = tid; t < (n_pow2 >> 1); t += SEL_THREADS) {
+      for (int t = lane; t < (np2 >> 1); t += 32) {
         const int a = ((t & ~(jj - 1)) << 1) | (t & (jj - 1));
         const int b = a + jj;
         const bool up = (a & kk) == 0;
@@ -512,165 +485,187 @@ __device__ void bitonic_sort(uint64_t* key, int* col, int n_pow2) {
           col[a] = cb; col[b] = ca;
         }
       }
-      __syncthreads();
+      __syncwarp();
     }
   }
 }
 
-// smem layout: keys[M_total] | skey[n_pow2] | scol[n_pow2] | sbits[words] | scan[words+1]
-__global__ void __launch_bounds__(SEL_THREADS) k_select(const double* __restrict__ R, int M_v,
-                                                        int M_total, int n_pow2,
-                                                        const uint32_t* __restrict__ adja,
-                                                        int words, int n_floor, double p,
-                                                        int with_union,
-                                                        uint32_t* __restrict__ bits,
-                                                        int32_t* __restrict__ kv_idx,
-                                                        int32_t* __restrict__ kv_cnt) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* skey = keys + M_total;
-  int* scol = reinterpret_cast<int*>(skey + n_pow2);
-  uint32_t* sbits = reinterpret_cast<uint32_t*>(scol + n_pow2);
-  int* s_scan = reinterpret_cast<int*>(sbits + words);
-  __shared__ SelSmem S;
-  __shared__ int s_neg;
-  const int64_t row = blockIdx.x;  // h * M_v + i
-  const int i = (int)(row % M_v);
-  const double* Rr = R + row * M_total;
-  const int tid = threadIdx.x;
-  if (tid == 0) s_neg = 0;
-  for (int w = tid; w < words; w += SEL_THREADS) sbits[w] = 0u;
-  __syncthreads();
-  int neg = 0;
-  for (int j = tid; j < M_total; j += SEL_THREADS) {
-    const double v = Rr[j];
-    keys[j] = desc_key(v);
-    neg |= (v < 0.0);
+// Sort (key, col) pairs [0, cnt) of skey/scol (padded to np2) and return
+// 1 + #(sequential prefix <= p) over the sorted values; *crossed reports whether the
+// monotone prefix exceeded p inside the sorted window.
+__device__ int warp_sorted_cut(uint64_t* skey, int* scol, int cnt, int np2, double p, bool monotone,
+                               bool* crossed) {
+  const int lane = threadIdx.x & 31;
+  for (int j = cnt + lane; j < np2; j += 32) { skey[j] = ~0ull; scol[j] = 0x7fffffff; }
+  __syncwarp();
+  warp_bitonic(skey, scol, np2);
+  int cut = 0;
+  bool cr = false;
+  if (lane == 0) {
+    double pre = 0.0;
+    int c = 0;
+    for (int s2 = 0; s2 < cnt; ++s2) {
+      pre = __dadd_rn(pre, key_value(skey[s2]));  // np.cumsum order (masks.py:152)
+      if (pre <= p) ++c;
+      else if (monotone) { cr = true; break; }
+    }
+    cut = c + 1;
   }
-  if (__syncthreads_or(neg) && tid == 0) s_neg = 1;
-  __syncthreads();
+  *crossed = __shfl_sync(FULL, (int)cr, 0) != 0;
+  return __shfl_sync(FULL, cut, 0);
+}
 
-  // ---- n_cut: 1 + #(sequential sorted prefix <= p)
-  if (tid == 0) { S.n_cut = -1; S.k_ub = M_total; }
+// One warp per (head, vision row).  RAW: the row holds scaled pooled scores and is first
+// turned into R in place (max, exp, numpy-pairwise sum, divide; masks.py:132-134).
+// Per-warp smem: keys[M_pad] | hist[256] | sbits[words_pad] | leaf[PW_MAX_LEAVES] |
+//                (SORT) hsum[256] | skey[np2] | scol[np2]
+template <bool RAW, bool SORT>
+__global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R, int64_t n_rows,
+                                                          int M_v, int M_total, int np2,
+                                                          const uint32_t* __restrict__ adja,
+                                                          int words, int n_floor, double p,
+                                                          int with_union,
+                                                          uint32_t* __restrict__ bits,
+                                                          int32_t* __restrict__ kv_idx,
+                                                          int32_t* __restrict__ kv_cnt,
+                                                          int per_warp_bytes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int leaf_off[PW_MAX_LEAVES], leaf_len[PW_MAX_LEAVES];
+  __shared__ int s_nl;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (RAW && threadIdx.x == 0) s_nl = pw_leaves(M_total, leaf_off, leaf_len);
   __syncthreads();
-  if (!s_neg) {
-    if (p == 0.0) {
-      // prefix_0 = row max > 0 ends the count at once; an all-zero row never exceeds 0
-      double mx = 0.0;
-      for (int j = tid; j < M_total; j += SEL_THREADS) mx = fmax(mx, key_value(keys[j]));
-      const int pos = __syncthreads_or(mx > 0.0);
-      if (tid == 0) S.n_cut = pos ? 1 : M_total + 1;
+  const int64_t row = (int64_t)blockIdx.x * SW_WARPS + warp;
+  if (row >= n_rows) return;
+  unsigned char* base = smem + (size_t)warp * per_warp_bytes;
+  const int M_pad = (M_total + 1) & ~1;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(base);
+  double* vals = reinterpret_cast<double*>(base);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(keys + M_pad);
+  uint32_t* sbits = hist + 256;
+  const int words_pad = (words + 1) & ~1;
+  double* leaf = reinterpret_cast<double*>(sbits + words_pad);
+  double* hsum = leaf + PW_MAX_LEAVES;
+  uint64_t* skey = reinterpret_cast<uint64_t*>(hsum + 256);
+  int* scol = reinterpret_cast<int*>(skey + np2);
+  const int i = (int)(row % M_v);
+  double* Rr = R + row * M_total;
+
+  // ---- load (+ softmax) ----
+  double mx = -INFINITY;
+  for (int j = lane; j < M_total; j += 32) {
+    const double v = Rr[j];
+    vals[j] = v;
+    mx = fmax(mx, v);
+  }
+  if (RAW) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+    for (int j = lane; j < M_total; j += 32) vals[j] = exp(vals[j] - mx);
+    __syncwarp();
+    const int nl = s_nl;
+    for (int l = lane; l < nl; l += 32) leaf[l] = pw_leaf(vals + leaf_off[l], leaf_len[l]);
+    __syncwarp();
+    double tot = 0.0;
+    if (lane == 0) tot = pw_fold(M_total, leaf);
+    tot = __shfl_sync(FULL, tot, 0);
+    for (int j = lane; j < M_total; j += 32) {
+      const double v = vals[j] / tot;
+      Rr[j] = v;
+      vals[j] = v;
+    }
+  }
+  __syncwarp();
+  bool neg = false, pos = false;
+  for (int j = lane; j < M_total; j += 32) {
+    const double v = vals[j];
+    neg |= v < 0.0;
+    pos |= v > 0.0;
+    keys[j] = desc_key(v);
+  }
+  neg = __any_sync(FULL, neg);
+  pos = __any_sync(FULL, pos);
+  for (int w = lane; w < words; w += 32) sbits[w] = 0u;
+  __syncwarp();
+
+  // ---- n_cut = 1 + #(sorted sequential prefix <= p)  (masks.py:150-153) ----
+  int n_cut;
+  if (!neg && p == 0.0) {
+    n_cut = pos ? 1 : M_total + 1;  // prefix_0 = row max
+  } else if (SORT) {
+    int k_ub = M_total;
+    if (!neg) {
+      const RadixState w = warp_radix(keys, M_total, 0, true, p, hist, hsum);
+      if (!w.flag) {
+        const int est = w.remaining + w.binc;
+        k_ub = min(M_total, est + 16 + est / 64);  // margin for summation-order rounding
+      }
+    }
+    int cnt = M_total;
+    if (k_ub < M_total) {
+      const RadixState t = warp_radix(keys, M_total, k_ub, false, 0.0, hist, nullptr);
+      warp_topk_visit(keys, M_total, t, [&](int j, int slot) { skey[slot] = keys[j]; scol[slot] = j; });
+      cnt = k_ub;
     } else {
-      radix_select(keys, M_total, 0, true, p, S);
-      if (tid == 0) {
-        if (S.flag) {
-          S.k_ub = M_total;  // approximate total <= p: scan the whole row exactly
-        } else {
-          // rank of the crossing element <= (#elements with smaller key) + bin size
-          const int est = S.remaining + (int)S.hist[0];
-          int ub = est + 16 + est / 64;
-          S.k_ub = ub < M_total ? ub : M_total;
+      for (int j = lane; j < M_total; j += 32) { skey[j] = keys[j]; scol[j] = j; }
+    }
+    int np = 2;
+    while (np < cnt) np <<= 1;
+    bool crossed;
+    n_cut = warp_sorted_cut(skey, scol, cnt, np, p, !neg, &crossed);
+    if (!neg && !crossed && cnt < M_total) {  // rounding pushed the cut past the window
+      for (int j = lane; j < M_total; j += 32) { skey[j] = keys[j]; scol[j] = j; }
+      int npf = 2;
+      while (npf < M_total) npf <<= 1;
+      n_cut = warp_sorted_cut(skey, scol, M_total, npf, p, true, &crossed);
+    }
+  } else {
+    n_cut = M_total + 1;  // unreachable: the host enables SORT whenever p > 0 or R is external
+  }
+  int keep = max(n_cut, n_floor);
+  keep = min(keep, M_total);
+
+  // ---- top-n_keep set -> bits, union, CSR ----
+  {
+    const RadixState t = warp_radix(keys, M_total, keep, false, 0.0, hist, nullptr);
+    warp_topk_visit(keys, M_total, t,
+                    [&](int j, int) { atomicOr(sbits + (j >> 5), 1u << (j & 31)); });
+  }
+  __syncwarp();
+  uint32_t* brow = bits + row * words;
+  int32_t* krow = kv_idx + row * M_total;
+  int run = 0;
+  for (int w0 = 0; w0 < words; w0 += 32) {
+    const int w = w0 + lane;
+    uint32_t x = 0;
+    if (w < words) {
+      x = sbits[w];
+      if (with_union) {
+        if (adja) x |= adja[(int64_t)i * words + w];
+        const int lo = w * 32;  // condition columns j >= M_v (masks.py:173)
+        for (int bb = 0; bb < 32; ++bb) {
+          const int j = lo + bb;
+          if (j >= M_v && j < M_total) x |= 1u << bb;
         }
       }
-      __syncthreads();
+      brow[w] = x;
     }
+    const int c = __popc(x);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int pos_ = run + incl - c;
+    while (x) {
+      const int b = __ffs(x) - 1;
+      x &= x - 1;
+      krow[pos_++] = w * 32 + b;
+    }
+    run += __shfl_sync(FULL, incl, 31);
   }
-  __syncthreads();
-  if (S.n_cut < 0) {
-    // sort the top-k_ub (all columns for rows with negative entries) and scan exactly
-    const int K = S.k_ub;
-    int np2 = 2;
-    while (np2 < K) np2 <<= 1;
-    if (K < M_total) {
-      radix_select(keys, M_total, K, false, 0.0, S);
-      // gather the top-K set (any order) into skey/scol
-      const uint64_t pre = S.prefix, msk = S.mask;
-      const int rem = S.remaining;
-      const int per = (M_total + SEL_THREADS - 1) / SEL_THREADS;
-      const int j0 = tid * per, j1 = min(M_total, j0 + per);
-      int eq = 0, cnt = 0;
-      for (int j = j0; j < j1; ++j) eq += ((keys[j] & msk) == pre);
-      int tot;
-      int rank = block_excl_scan(eq, S, &tot);
-      for (int j = j0; j < j1; ++j) {
-        const uint64_t km = keys[j] & msk;
-        cnt += (km < pre) || (km == pre && rank++ < rem);
-      }
-      int slot = block_excl_scan(cnt, S, &tot);
-      rank -= eq;  // restart the equal-rank walk
-      for (int j = j0; j < j1; ++j) {
-        const uint64_t km = keys[j] & msk;
-        bool sel = km < pre;
-        if (km == pre) sel = (rank++ < rem);
-        if (sel) { skey[slot] = keys[j]; scol[slot] = j; ++slot; }
-      }
-    } else {
-      for (int j = tid; j < M_total; j += SEL_THREADS) { skey[j] = keys[j]; scol[j] = j; }
-    }
-    for (int j = K + tid; j < np2; j += SEL_THREADS) { skey[j] = ~0ull; scol[j] = 0x7fffffff; }
-    __syncthreads();
-    bitonic_sort(skey, scol, np2);
-    if (tid == 0) {
-      double pre = 0.0;
-      int cnt = 0;
-      bool crossed = false;
-      for (int s2 = 0; s2 < K; ++s2) {
-        pre = __dadd_rn(pre, key_value(skey[s2]));
-        if (pre <= p) ++cnt;
-        else if (!s_neg) { crossed = true; break; }
-      }
-      // non-monotone rows: every prefix counted (full row sorted); monotone rows that did
-      // not cross within the bound (should not happen) -> mark for the full scan fallback
-      S.n_cut = (crossed || s_neg || K == M_total) ? cnt + 1 : -2;
-    }
-    __syncthreads();
-    if (S.n_cut == -2) {
-      // exact fallback: sort everything
-      int np = 2;
-      while (np < M_total) np <<= 1;
-      for (int j = tid; j < np; j += SEL_THREADS) {
-        skey[j] = j < M_total ? keys[j] : ~0ull;
-        scol[j] = j < M_total ? j : 0x7fffffff;
-      }
-      __syncthreads();
-      bitonic_sort(skey, scol, np);
-      if (tid == 0) {
-        double pre = 0.0;
-        int cnt = 0;
-        for (int s2 = 0; s2 < M_total; ++s2) {
-          pre = __dadd_rn(pre, key_value(skey[s2]));
-          if (pre <= p) ++cnt; else break;
-        }
-        S.n_cut = cnt + 1;
-      }
-      __syncthreads();
-    }
-  }
-  // ---- n_keep and the top-n_keep set
-  if (tid == 0) {
-    int keep = S.n_cut;
-    if (keep < n_floor) keep = n_floor;
-    if (keep > M_total) keep = M_total;
-    S.n_keep = keep;
-  }
-  __syncthreads();
-  radix_select(keys, M_total, S.n_keep, false, 0.0, S);
-  mark_selected(keys, M_total, S, sbits);
-  __syncthreads();
-  if (with_union) {
-    for (int w = tid; w < words; w += SEL_THREADS) {
-      uint32_t x = sbits[w];
-      if (adja) x |= adja[(int64_t)i * words + w];
-      const int lo = w * 32;  // condition columns j >= M_v (masks.py:173)
-      for (int bb = 0; bb < 32; ++bb) {
-        const int j = lo + bb;
-        if (j >= M_v && j < M_total) x |= 1u << bb;
-      }
-      sbits[w] = x;
-    }
-    __syncthreads();
-  }
-  emit_row(sbits, words, M_total, bits + row * words, kv_idx + row * M_total, kv_cnt + row, s_scan);
+  if (lane == 0) kv_cnt[row] = run;
 }
 
 __global__ void __launch_bounds__(128) k_mask_pack(const uint8_t* __restrict__ dense, int M_total,
@@ -758,35 +753,73 @@ extern "C" int tcb_block_relevance(const double* pq, int pq_blocks, const double
                 "bad relevance shape");
   TCB_CHECK_ARG(M_total <= 16384, TCB_ESIZE, "M_total %d > 16384 unsupported", M_total);
   if (rows == 0) return TCB_OK;
-  dim3 grid((unsigned)ceil_div(rows, RT_ROWS), H);
-  k_relevance<<<grid, 256, 0, as_stream(stream)>>>(pq, pq_blocks, pk, rows, M_total, d, 0.0,
-                                                   sqrt((double)d), R);
-  return check_launch("k_relevance");
+  cudaStream_t st = as_stream(stream);
+  dim3 grid((unsigned)ceil_div(M_total, ST_TILE), (unsigned)ceil_div(rows, ST_TILE), H);
+  k_scores<<<grid, 256, 0, st>>>(pq, pq_blocks, pk, rows, M_total, d, sqrt((double)d), R);
+  int rc = check_launch("k_scores");
+  if (rc) return rc;
+  const int64_t n_rows = (int64_t)H * rows;
+  k_row_softmax<<<(unsigned)ceil_div(n_rows, 8), 256, 0, st>>>(R, n_rows, M_total);
+  return check_launch("k_row_softmax");
+}
+
+static int launch_select(double* R, bool raw, int H, int M_v, int M_total, const uint32_t* adja,
+                         int words, int n_floor, double p, int with_union, uint32_t* bits,
+                         int32_t* kv_idx, int32_t* kv_cnt, cudaStream_t s) {
+  TCB_CHECK_ARG(R && bits && kv_idx && kv_cnt, TCB_ESHAPE, "null tensor");
+  TCB_CHECK_ARG(H >= 1 && M_v >= 0 && M_total >= 1, TCB_ESHAPE, "bad select shape");
+  TCB_CHECK_ARG(words >= ceil_div(M_total, 32), TCB_ESHAPE, "words too small");
+  TCB_CHECK_ARG(M_total <= 8192, TCB_ESIZE, "M_total %d > 8192 unsupported", M_total);
+  TCB_CHECK_ARG(n_floor >= 1, TCB_EDOMAIN, "n_floor must be >= 1");
+  const int64_t n_rows = (int64_t)H * M_v;
+  if (n_rows == 0) return TCB_OK;
+  const bool sort = !raw || p > 0.0;
+  int np2 = 2;
+  while (np2 < M_total) np2 <<= 1;
+  const int M_pad = (M_total + 1) & ~1, words_pad = (words + 1) & ~1;
+  size_t per_warp = (size_t)M_pad * 8 + 256 * 4 + (size_t)words_pad * 4 + PW_MAX_LEAVES * 8;
+  if (sort) per_warp += 256 * 8 + (size_t)np2 * 12;
+  per_warp = (per_warp + 15) & ~size_t(15);
+  const size_t smem = per_warp * SW_WARPS;
+  const unsigned grid = (unsigned)ceil_div(n_rows, SW_WARPS);
+  auto go = [&](auto kern) -> int {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_error(TCB_ECUDA, "k_select smem: %s", cudaGetErrorString(e));
+    kern<<<grid, SW_WARPS * 32, smem, s>>>(R, n_rows, M_v, M_total, np2, adja, words, n_floor, p,
+                                          with_union, bits, kv_idx, kv_cnt, (int)per_warp);
+    return check_launch("k_select");
+  };
+  if (raw) return sort ? go(k_select<true, true>) : go(k_select<true, false>);
+  return go(k_select<false, true>);
 }
 
 extern "C" int tcb_block_select(const double* R, int H, int M_v, int M_total,
                                 const uint32_t* adja, int words, int n_floor, double p,
                                 int with_union, uint32_t* bits, int32_t* kv_idx, int32_t* kv_cnt,
                                 void* stream) {
-  TCB_CHECK_ARG(R && bits && kv_idx && kv_cnt, TCB_ESHAPE, "null tensor");
-  TCB_CHECK_ARG(H >= 1 && M_v >= 0 && M_total >= 1, TCB_ESHAPE, "bad select shape");
-  TCB_CHECK_ARG(words >= ceil_div(M_total, 32), TCB_ESHAPE, "words too small");
-  TCB_CHECK_ARG(M_total <= 16384, TCB_ESIZE, "M_total %d > 16384 unsupported", M_total);
-  if ((int64_t)H * M_v == 0) return TCB_OK;
-  int n_pow2 = 1;
-  while (n_pow2 < M_total) n_pow2 <<= 1;
-  if (n_pow2 < 2) n_pow2 = 2;
-  const size_t smem = (size_t)M_total * 8 + (size_t)n_pow2 * (8 + 4) + (size_t)words * 4 +
-                      (size_t)(words + 1) * 4;
-  cudaStream_t s = as_stream(stream);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return set_error(TCB_ECUDA, "k_select smem: %s", cudaGetErrorString(e));
-  }
-  k_select<<<(unsigned)((int64_t)H * M_v), SEL_THREADS, smem, s>>>(
-      R, M_v, M_total, n_pow2, adja, words, n_floor, p, with_union, bits, kv_idx, kv_cnt);
-  return check_launch("k_select");
+  // R is only read on this path (RAW=false never writes it)
+  return launch_select(const_cast<double*>(R), false, H, M_v, M_total, adja, words, n_floor, p,
+                       with_union, bits, kv_idx, kv_cnt, as_stream(stream));
+}
+
+extern "C" int tcb_block_select_scores(double* S, int H, int M_v, int M_total,
+                                       const uint32_t* adja, int words, int n_floor, double p,
+                                       int with_union, uint32_t* bits, int32_t* kv_idx,
+                                       int32_t* kv_cnt, void* stream) {
+  return launch_select(S, true, H, M_v, M_total, adja, words, n_floor, p, with_union, bits, kv_idx,
+                       kv_cnt, as_stream(stream));
+}
+
+extern "C" int tcb_block_scores(const double* pq, int pq_blocks, const double* pk, int H, int rows,
+                                int M_total, int d, double* S, void* stream) {
+  TCB_CHECK_ARG(pq && pk && S, TCB_ESHAPE, "null tensor");
+  TCB_CHECK_ARG(H >= 1 && rows >= 0 && rows <= pq_blocks && M_total >= 1 && d >= 1, TCB_ESHAPE,
+                "bad scores shape");
+  if (rows == 0) return TCB_OK;
+  dim3 grid((unsigned)ceil_div(M_total, ST_TILE), (unsigned)ceil_div(rows, ST_TILE), H);
+  k_scores<<<grid, 256, 0, as_stream(stream)>>>(pq, pq_blocks, pk, rows, M_total, d,
+                                                sqrt((double)d), S);
+  return check_launch("k_scores");
 }
 
 extern "C" int tcb_mask_pack(const uint8_t* dense, int64_t rows, int M_total, int words,

@@ -2,10 +2,11 @@
 
 ``build_block_mask`` is three launches: K3 ``tcb_block_pool`` (Q and K in one
 pass, float64 accumulation -> pooled means bit-exact with masks.py:112-116),
-K4 ``tcb_block_relevance`` (float64 pooled scores + row softmax,
-masks.py:119-134) and K5 ``tcb_block_select`` (stable descending sort,
-sequential float64 prefix, cutoff/quota, union with condition columns and the
-packed adjacency, masks.py:137-175).  The mask is kept packed (H, M_v, words)
+K4a ``tcb_block_scores`` (float64 pooled scores / sqrt(d), masks.py:130-131) and
+the fused K4b+K5 ``tcb_block_select_scores`` (row softmax with numpy's pairwise
+sums, masks.py:132-134, then radix-select of the top n_keep under the stable
+descending order, the exact sequential prefix cutoff, and the union with the
+condition columns and the packed adjacency, masks.py:137-175).  The mask is kept packed (H, M_v, words)
 plus an ascending CSR (kv_idx, kv_cnt) that the attention kernel walks.
 """
 
@@ -210,15 +211,25 @@ def union_mask(b_top, cond, adja, layout: BlockLayout) -> BlockMask:
 
 
 def build_block_mask(q, k, layout: BlockLayout, statics: StaticMasks, params: SelectionParams):
-    """Pool -> score -> select -> union; returns (BlockMask, R) (masks.py:178-199)."""
+    """Pool -> score -> select -> union; returns (BlockMask, R) (masks.py:178-199).
+
+    Three launches: K3 pool (Q and K together), K4a float64 scores, and the fused
+    row-softmax + selection + union kernel, which leaves R in the score buffer."""
     qd, kd = _dev.as_cuda(q), _dev.as_cuda(k)
     d_k = qd.shape[-1]
+    H = qd.shape[0]
     pq, pk = _pool_one_or_two(qd, kd, layout)
-    R = torch.empty((qd.shape[0], layout.M_v, layout.M_total), dtype=torch.float64,
-                    device=qd.device)
-    _native.call("tcb_block_relevance", pq.values.data_ptr(), layout.M_total, pk.values.data_ptr(),
-                 qd.shape[0], layout.M_v, layout.M_total, d_k, R.data_ptr(), _dev.stream())
-    bits, kv_idx, kv_cnt = _select(R, params, layout.M_v, statics.packed(layout), with_union=True)
+    R = torch.empty((H, layout.M_v, layout.M_total), dtype=torch.float64, device=qd.device)
+    _native.call("tcb_block_scores", pq.values.data_ptr(), layout.M_total, pk.values.data_ptr(),
+                 H, layout.M_v, layout.M_total, d_k, R.data_ptr(), _dev.stream())
+    words = mask_words(layout.M_total)
+    bits = torch.empty((H, layout.M_v, words), dtype=torch.int32, device=qd.device)
+    kv_idx = torch.empty((H, layout.M_v, layout.M_total), dtype=torch.int32, device=qd.device)
+    kv_cnt = torch.empty((H, layout.M_v), dtype=torch.int32, device=qd.device)
+    adja = statics.packed(layout)
+    _native.call("tcb_block_select_scores", R.data_ptr(), H, layout.M_v, layout.M_total,
+                 _native.ptr(adja), words, params.n_floor(layout.M_v), float(params.p), 1,
+                 bits.data_ptr(), kv_idx.data_ptr(), kv_cnt.data_ptr(), _dev.stream())
     mask = BlockMask(words=bits, kv_idx=kv_idx, kv_cnt=kv_cnt, M_total=layout.M_total,
                      nonempty=True)
     return mask, _dev.to_like(R, q)
