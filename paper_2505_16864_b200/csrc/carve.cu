@@ -164,68 +164,45 @@ __global__ void __launch_bounds__(128) k_carve_simt(const T* __restrict__ q,
 // =====================================================================================
 namespace tc {
 
-// Debug timeline (TCB_CARVE_TRACE=1): CTA 0 records (event, step, clock) triples so the
-// pipeline's critical path can be read off without a profiler.  Off in production.
-constexpr int TRACE_CAP = 8192;
-__device__ unsigned long long g_trace[TRACE_CAP][2];
-__device__ unsigned int g_trace_n;
-__device__ __forceinline__ void trace(int on, int ev, int step) {
-  if (!on || blockIdx.x != 0) return;
-  const unsigned i = atomicAdd(&g_trace_n, 1u);
-  if (i < TRACE_CAP) {
-    g_trace[i][0] = ((unsigned long long)ev << 32) | (unsigned)step;
-    g_trace[i][1] = clock64();
-  }
-}
-
-// One persistent CTA per SM.  TMEM (512 columns):
-//   Q  [0, 64)      the item's 128 x 128 bf16 query tile as the MMA A operand (TS mode),
-//                   so S = Q K^T reads only K from shared memory
-//   S0 [64, 192)    S double buffer (fp32 128 x 128); P(t) is written as bf16 over the
-//   S1 [192, 320)   first 64 columns of its buffer and consumed by O += P V
-//   O  [320, 448)   fp32 accumulator (128 x D)
-// so the tensor core computes S(t+1) while the softmax warps work on S(t).  Eight softmax
-// warps: each row's 128 keys are split between two warps of the same lane quarter (each
-// computes the full row max itself; no per-block handshake), doubling the exp issue rate.
+// Work unit of the pipeline: a "half-step" = one 64-key half of a 128-key kv block.
+// S is double-buffered in TMEM per half-step (2 x 64 columns) so the tensor core
+// computes S(t+1) = Q K(t+1)^T while the softmax warps work on S(t); P(t) is written
+// as bf16 over the first 32 columns of its S buffer and consumed by O += P(t) V(t).
 constexpr int BM = 128;           // query rows per tile (== m)
 constexpr int BK = 128;           // keys per kv block (== m)
-constexpr int NUM_THREADS = 320;  // w0 TMA+scheduler, w1 MMA+TMEM owner, w2..w9 softmax
-constexpr int NUM_SOFTMAX = 256;  // two warps per TMEM lane quarter, one per key half
-constexpr int TMEM_COLS = 512;
-constexpr int Q_COL = 0;
-constexpr int S_COL = 64;
-constexpr int O_COL = 320;
-constexpr int K_SLOTS = 3;
-constexpr int V_SLOTS = 3;
+constexpr int HN = 64;            // keys per half-step
+constexpr int NUM_THREADS = 192;  // w0 TMA+scheduler, w1 MMA+TMEM owner, w2..w5 softmax
+constexpr int TMEM_COLS = 256;    // S0 [0,64) S1 [64,128) O [128, 128+D)
+constexpr int O_COL = 128;
+constexpr int K_SLOTS = 3;        // K half-tiles in flight
+constexpr int V_SLOTS = 2;        // V half-tiles in flight
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: P <= 2^8 between rescales
-constexpr int LIST_CAP = 4096;    // max kv blocks per row held in smem (M_total <= LIST_CAP)
-
-__device__ __forceinline__ uint16_t* bars_list(uint8_t* smem, int off, int slot) {
-  return reinterpret_cast<uint16_t*>(smem + off) + slot * LIST_CAP;
-}
 
 template <int D>
 struct Smem {
-  static constexpr int TILE_BYTES = BK * D * 2;  // 128 x D bf16
-  static constexpr int CHUNKS = D / 64;          // 64-element (128 B) swizzle columns
-  static constexpr int CHUNK_BYTES = BK * 128;   // bytes per 64-col chunk of a tile
-  static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = OFF_K + K_SLOTS * TILE_BYTES;
-  static constexpr int OFF_LIST = OFF_V + V_SLOTS * TILE_BYTES;  // 2 x LIST_CAP uint16 kv lists
-  static constexpr int OFF_BAR = OFF_LIST + 2 * LIST_CAP * 2;
-  static constexpr int BYTES = OFF_BAR + 4096;
+  static constexpr int Q_BYTES = BM * D * 2;      // 128 x D bf16
+  static constexpr int HALF_BYTES = HN * D * 2;   // 64 x D bf16
+  static constexpr int CHUNKS = D / 64;           // 64-element (128 B) swizzle columns
+  static constexpr int Q_CHUNK = BM * 128;        // bytes per 64-col chunk of Q
+  static constexpr int H_CHUNK = HN * 128;        // bytes per 64-col chunk of a half tile
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + K_SLOTS * HALF_BYTES;
+  static constexpr int OFF_BAR = OFF_V + V_SLOTS * HALF_BYTES;
+  static constexpr int BYTES = OFF_BAR + 256;
 };
 
 struct Bars {
-  uint64_t q_full, o_full, o_done, p_full;
+  uint64_t q_full, q_empty, o_full, o_done;
+  uint64_t p_full[2];  // by half-step parity: softmax(t+1) may finish before PV(t) is issued
   uint64_t s_full[2];
   uint64_t k_full[K_SLOTS], k_empty[K_SLOTS];
   uint64_t v_full[V_SLOTS], v_empty[V_SLOTS];
   uint64_t sched_full[2], sched_empty[2];
   int sched_item[2];
   uint32_t tmem_base;
-  float xsum[2][BM];     // [key half][row] partial row sums for the epilogue
 };
+static_assert(sizeof(Bars) <= 256, "barrier block must fit the reserved smem");
 
 // instruction descriptor, kind::f16: bf16 x bf16 -> f32, K-major A, B major per arg
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N, int b_mn_major) {
@@ -255,6 +232,7 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
+
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));  // FMNMX3
@@ -268,7 +246,8 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
   const float x0 = fmaxf(f2_lo(x), -126.f), x1 = fmaxf(f2_hi(x), -126.f);
   const uint64_t xc = f2_pack(x0, x1);
-  const uint64_t t = fadd2(xc, f2_pack(12582912.f, 12582912.f));
+  const uint64_t magic = f2_pack(12582912.f, 12582912.f);
+  const uint64_t t = fadd2(xc, magic);
   const uint64_t jf = fadd2(t, f2_pack(-12582912.f, -12582912.f));
   const uint64_t f = ffma2(jf, f2_pack(-1.f, -1.f), xc);
   uint64_t p = ffma2(f, f2_pack(0.05517132f, 0.05517132f), f2_pack(0.24261054f, 0.24261054f));
@@ -279,15 +258,34 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
   return (uint64_t)lo | ((uint64_t)hi << 32);
 }
 
+// Warp-cooperative view of a row's ascending kv list: lane l caches entry 32*c + l of the
+// current chunk c; block(j) broadcasts entry j (all 32 lanes must call it together).
+struct KvList {
+  const int32_t* list;
+  int n, lane, chunk, cache;
+  __device__ KvList(const int32_t* l, int n_, int lane_) : list(l), n(n_), lane(lane_), chunk(-1), cache(0) {}
+  __device__ __forceinline__ int block(int j) {
+    if (!list) return j;
+    const int c = j >> 5;
+    if (c != chunk) {
+      chunk = c;
+      const int idx = c * 32 + lane;
+      cache = idx < n ? __ldg(list + idx) : 0;
+    }
+    return __shfl_sync(0xffffffffu, cache, j & 31);
+  }
+};
+
 template <int D, int EMU>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    k_carve_tc(const __nv_bfloat16* __restrict__ q, const __grid_constant__ CUtensorMap tm_k,
+__global__ void __launch_bounds__(NUM_THREADS, 2)
+    k_carve_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
                CarveShape s, const int32_t* __restrict__ kv_idx,
                const int32_t* __restrict__ kv_cnt, int* __restrict__ counter, int total_items,
-               float scale_log2, float beta_log2, int dbg_noload, int dbg_trace) {
+               float scale_log2, float beta_log2, int dbg) {
   using L = Smem<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sQ = smem + L::OFF_Q;
   uint8_t* sK = smem + L::OFF_K;
   uint8_t* sV = smem + L::OFF_V;
   Bars* bars = reinterpret_cast<Bars*>(smem + L::OFF_BAR);
@@ -296,10 +294,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     if (ptx::smem_u32(smem) & 1023u) __trap();  // 128B-swizzle tiles need 1 KB alignment
-    ptx::mbar_init(&bars->q_full, NUM_SOFTMAX);
+    ptx::mbar_init(&bars->q_full, 1);
+    ptx::mbar_init(&bars->q_empty, 1);
     ptx::mbar_init(&bars->o_full, 1);
     ptx::mbar_init(&bars->o_done, 1);
-    ptx::mbar_init(&bars->p_full, NUM_SOFTMAX);
+    for (int i = 0; i < 2; ++i) ptx::mbar_init(&bars->p_full[i], 128);
     for (int i = 0; i < 2; ++i) ptx::mbar_init(&bars->s_full[i], 1);
     for (int i = 0; i < K_SLOTS; ++i) {
       ptx::mbar_init(&bars->k_full[i], 1);
@@ -311,9 +310,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&bars->sched_full[i], 1);
-      ptx::mbar_init(&bars->sched_empty[i], 1 + 8);
+      ptx::mbar_init(&bars->sched_empty[i], 1 + 4);
     }
     ptx::fence_mbar_init();
+    ptx::tma_prefetch_desc(&tm_q);
     ptx::tma_prefetch_desc(&tm_k);
     ptx::tma_prefetch_desc(&tm_v);
   }
@@ -325,85 +325,80 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 0) {
     // ============================ TMA producer + scheduler ============================
-    // The whole warp fetches the next item and stages its kv list in smem (coalesced,
-    // off the critical path); lane 0 then streams K/V tiles through the rings.
+    // Whole warp runs the loop: lane 0 waits on the rings and issues TMA; the item's kv
+    // list is read 32 entries at a time (one coalesced load per lane) and broadcast by
+    // shuffle, so the block index is never a dependent global load on the issue path.
     const uint64_t pol_kv = ptx::policy_evict_last();
+    const uint64_t pol_q = ptx::policy_evict_first();
     uint32_t it = 0, gk = 0, gv = 0;
     for (;; ++it) {
       const int slot = it & 1;
-      if (lane == 0) ptx::mbar_wait(&bars->sched_empty[slot], ((it >> 1) & 1) ^ 1);
-      __syncwarp();
       int item = 0;
       if (lane == 0) {
+        ptx::mbar_wait(&bars->sched_empty[slot], ((it >> 1) & 1) ^ 1);
         item = atomicAdd(counter, 1);
         if (item >= total_items) item = -1;
-      }
-      item = __shfl_sync(0xffffffffu, item, 0);
-      int h = 0, qb = 0, n = 0;
-      bool vis = false;
-      uint16_t* lst = bars_list(smem, L::OFF_LIST, slot);
-      if (item >= 0) {
-        decode_item(item, s, h, qb);
-        vis = qb < s.M_v;
-        n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-        if (vis) {
-          const int32_t* list = kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total;
-          for (int j = lane; j < n; j += 32) lst[j] = (uint16_t)__ldg(list + j);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
         bars->sched_item[slot] = item;
         ptx::mbar_arrive(&bars->sched_full[slot]);
       }
+      item = __shfl_sync(0xffffffffu, item, 0);
       if (item < 0) break;
+      int h, qb;
+      decode_item(item, s, h, qb);
+      const bool vis = qb < s.M_v;
+      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
+      KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
+      const int T = 2 * n;
       if (lane == 0) {
-        auto load = [&](const CUtensorMap* tm, uint8_t* base, uint64_t* full, uint64_t* empty,
-                        int slots, uint32_t& cnt, int t) {
-          const int b = vis ? (int)lst[t] : t;
+        ptx::mbar_wait(&bars->q_empty, (it & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&bars->q_full, L::Q_BYTES);
+#pragma unroll
+        for (int c = 0; c < L::CHUNKS; ++c)
+          ptx::tma_load_3d(sQ + c * L::Q_CHUNK, &tm_q, &bars->q_full, c * 64, qb * BM, h, pol_q);
+      }
+      auto load = [&](const CUtensorMap* tm, uint8_t* base, uint64_t* full, uint64_t* empty,
+                      int slots, uint32_t& cnt, int t) {
+        const int b = kl.block(t >> 1);
+        if (lane == 0) {
           const int sl = cnt % slots;
           ptx::mbar_wait(&empty[sl], ((cnt / slots) & 1) ^ 1);
-          if ((dbg_noload & 1) && cnt >= (uint32_t)slots) {  // timing experiment: reuse stale tiles
+          if ((dbg & 1) && cnt >= (uint32_t)slots) {  // timing experiment: no operand traffic
             ptx::mbar_arrive(&full[sl]);
-            ++cnt;
-            return;
-          }
-          ptx::mbar_arrive_expect_tx(&full[sl], L::TILE_BYTES);
+          } else {
+            ptx::mbar_arrive_expect_tx(&full[sl], L::HALF_BYTES);
 #pragma unroll
-          for (int c = 0; c < L::CHUNKS; ++c)
-            ptx::tma_load_3d(base + sl * L::TILE_BYTES + c * L::CHUNK_BYTES, tm, &full[sl], c * 64,
-                             b * BK, h, pol_kv);
-          ++cnt;
-        };
-        // MMA consumption order: K0, K1, V0, K2, V1, ..., V(n-1)
-        if (n > 0) load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, 0);
-        for (int t = 0; t < n; ++t) {
-          if (t + 1 < n) load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, t + 1);
-          load(&tm_v, sV, bars->v_full, bars->v_empty, V_SLOTS, gv, t);
+            for (int c = 0; c < L::CHUNKS; ++c)
+              ptx::tma_load_3d(base + sl * L::HALF_BYTES + c * L::H_CHUNK, tm, &full[sl], c * 64,
+                               b * BK + (t & 1) * HN, h, pol_kv);
+          }
         }
+        ++cnt;
+      };
+      // same order the MMA warp consumes: K0, K1, V0, K2, V1, ..., V(T-1)
+      load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, 0);
+      for (int t = 0; t < T; ++t) {
+        if (t + 1 < T) load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, t + 1);
+        load(&tm_v, sV, bars->v_full, bars->v_empty, V_SLOTS, gv, t);
       }
-      __syncwarp();
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
     if (lane == 0) {
-      constexpr uint32_t IDESC_S = make_idesc(BM, BK, 0);  // Q (TMEM) x K (K-major smem)
-      constexpr uint32_t IDESC_O = make_idesc(BM, D, 1);   // P (TMEM) x V (MN-major smem)
-      const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
+      constexpr uint32_t IDESC_S = make_idesc(BM, HN, 0);  // Q (K-major) x K (K-major)
+      constexpr uint32_t IDESC_O = make_idesc(BM, D, 1);   // P (TMEM)   x V (MN-major)
+      const uint32_t aQ = ptx::smem_u32(sQ), aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
       uint32_t it = 0, gk = 0, gv = 0, gs = 0, gp = 0;
-      auto issue_s = [&]() {  // S(gs) = Q K^T into buffer gs & 1
+      auto issue_s = [&]() {  // S(gs) = Q K(gs)^T into buffer gs & 1
         const int sl = gk % K_SLOTS;
-        trace(dbg_trace, 1, gs);
         ptx::mbar_wait(&bars->k_full[sl], (gk / K_SLOTS) & 1);
-        trace(dbg_trace, 2, gs);
         ptx::tc_fence_after();
-        const uint32_t kbase = aK + sl * L::TILE_BYTES;
-        const uint32_t dcol = tmem + S_COL + (gs & 1) * BK;
+        const uint32_t kbase = aK + sl * L::HALF_BYTES;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t koff = (kk >> 2) * L::CHUNK_BYTES + (kk & 3) * 32;
-          ptx::mma_ts(dcol, tmem + Q_COL + kk * 8, make_sdesc(kbase + koff, 16, 1024), IDESC_S,
-                      kk > 0 ? 1u : 0u);
+          const uint32_t qoff = (kk >> 2) * L::Q_CHUNK + (kk & 3) * 32;
+          const uint32_t koff = (kk >> 2) * L::H_CHUNK + (kk & 3) * 32;
+          ptx::mma_ss(tmem + (gs & 1) * HN, make_sdesc(aQ + qoff, 16, 1024),
+                      make_sdesc(kbase + koff, 16, 1024), IDESC_S, kk > 0 ? 1u : 0u);
         }
         ptx::mma_commit(&bars->k_empty[sl]);
         ptx::mma_commit(&bars->s_full[gs & 1]);
@@ -414,29 +409,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int slot = it & 1;
         ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
         const int item = bars->sched_item[slot];
+        ptx::mbar_arrive(&bars->sched_empty[slot]);
         if (item < 0) break;
         int h, qb;
         decode_item(item, s, h, qb);
         const bool vis = qb < s.M_v;
-        const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-        ptx::mbar_wait(&bars->q_full, it & 1);  // Q tile written to TMEM by the softmax warps
-        ptx::tc_fence_after();
-        if (n > 0) issue_s();
-        for (int t = 0; t < n; ++t) {
-          if (t + 1 < n) issue_s();
-          // ---- O += P(t) V(t): A = P from TMEM (64 packed columns), K = 128 keys
-          ptx::mbar_wait(&bars->p_full, gp & 1);
-          trace(dbg_trace, 3, gp);
+        const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
+        const int T = 2 * n;
+        ptx::mbar_wait(&bars->q_full, it & 1);
+        if (T == 0) {  // cannot come from build_block_mask (diagonal); keep the pipes consistent
+          ptx::mma_commit(&bars->q_empty);
+          ptx::mma_commit(&bars->o_full);
+          continue;
+        }
+        issue_s();
+        for (int t = 0; t < T; ++t) {
+          if (t + 1 < T) {
+            issue_s();
+            if (t + 2 == T) ptx::mma_commit(&bars->q_empty);
+          }
+          // ---- O += P(t) V(t): A = P from TMEM (32 packed columns), K = 64 keys
+          ptx::mbar_wait(&bars->p_full[gp & 1], (gp >> 1) & 1);
           const int vs = gv % V_SLOTS;
           ptx::mbar_wait(&bars->v_full[vs], (gv / V_SLOTS) & 1);
-          trace(dbg_trace, 4, gp);
           ptx::tc_fence_after();
-          const uint32_t vbase = aV + vs * L::TILE_BYTES;
-          const uint32_t pcol = tmem + S_COL + (gp & 1) * BK;
+          const uint32_t vbase = aV + vs * L::HALF_BYTES;
+          const uint32_t pcol = tmem + (gp & 1) * HN;
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
+          for (int kk = 0; kk < HN / 16; ++kk) {
             ptx::mma_ts(tmem + O_COL, pcol + kk * 8,
-                        make_sdesc(vbase + kk * 16 * 128, L::CHUNK_BYTES, 1024), IDESC_O,
+                        make_sdesc(vbase + kk * 16 * 128, L::H_CHUNK, 1024), IDESC_O,
                         (t > 0 || kk > 0) ? 1u : 0u);
           }
           ptx::mma_commit(&bars->v_empty[vs]);
@@ -445,98 +447,66 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ++gp;
         }
         ptx::mma_commit(&bars->o_full);
-        ptx::mbar_arrive(&bars->sched_empty[slot]);  // done with this item's slot
       }
     }
     __syncwarp();
   } else {
-    // ============================ Q load / softmax / correction / epilogue ============================
-    const int quarter = warp & 3;       // TMEM lane quarter this warp may access
-    const int half = (warp - 2) >> 2;   // key half of S (and column half of Q / O) it owns
+    // ============================ softmax / correction / epilogue ============================
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
     const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
-    const int bar_id = 1 + quarter;     // named barrier of the two warps sharing this quarter
-    constexpr int QH = D / 4;           // packed Q columns per half
-    constexpr int OH = D / 2;           // O columns per half
     uint32_t it = 0, g = 0;
     for (;; ++it) {
       const int slot = it & 1;
       ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
       const int item = bars->sched_item[slot];
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);
       if (item < 0) break;
       int h, qb;
       decode_item(item, s, h, qb);
       const bool vis = qb < s.M_v;
-      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-      const uint16_t* lst = bars_list(smem, L::OFF_LIST, slot);
-      // ---- Q row half -> TMEM A operand (packed bf16 pairs).  The previous item's last
-      // S MMA has completed (its softmax waited on it), so Q can be replaced.
-      {
-        const int4* qrow = reinterpret_cast<const int4*>(q + (int64_t)h * s.sh +
-                                                         ((int64_t)qb * BM + row) * s.sn) +
-                           half * (QH / 4);
-        uint32_t qa[32];
-#pragma unroll
-        for (int e = 0; e < QH / 4; ++e) {
-          const int4 v4 = __ldg(qrow + e);
-          qa[4 * e] = (uint32_t)v4.x;
-          qa[4 * e + 1] = (uint32_t)v4.y;
-          qa[4 * e + 2] = (uint32_t)v4.z;
-          qa[4 * e + 3] = (uint32_t)v4.w;
-        }
-        if constexpr (QH == 32) ptx::tmem_st32(t_row + Q_COL + half * QH, qa);
-        else ptx::tmem_st16(t_row + Q_COL + half * QH, *reinterpret_cast<uint32_t(*)[16]>(qa));
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars->q_full);
-      }
+      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
+      KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
+      const int T = 2 * n;
       float m_run = -INFINITY, l_run = 0.f;
-      for (int t = 0; t < n; ++t, ++g) {
-        const int b = vis ? (int)lst[t] : t;
-        const int kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond) - half * 64;
-        const float bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
-        const uint32_t sbuf = t_row + S_COL + (g & 1) * BK;
-        if (lane == 0 && (warp == 2 || warp == 9)) trace(dbg_trace, 10 + warp, g);
+      int b = 0, kvalid = BK;
+      float bias = 0.f;
+      for (int t = 0; t < T; ++t, ++g) {
+        if ((t & 1) == 0) {
+          b = kl.block(t >> 1);
+          kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond);
+          bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
+        }
+        const int hvalid = kvalid - (t & 1) * HN;  // valid keys in this half (may be <= 0)
         ptx::mbar_wait(&bars->s_full[g & 1], (g >> 1) & 1);
-        if (lane == 0 && (warp == 2 || warp == 9)) trace(dbg_trace, 20 + warp, g);
         ptx::tc_fence_after();
-        if (dbg_noload & 2) {  // timing experiment: no softmax work at all
+        if (dbg & 2) {  // timing experiment: no softmax work
           l_run = 1.f;
-          ptx::mbar_arrive(&bars->p_full);
+          ptx::mbar_arrive(&bars->p_full[g & 1]);
           continue;
         }
-        // Each warp reads all 128 scores of its rows (TMEM reads are cheap) and computes
-        // the full row max itself, so the two warps of a lane quarter never synchronise
-        // per block and drift apart, overlapping one's max/ld phase with the other's exps.
-        uint32_t sr[64], so[64];
-        ptx::tmem_ld32(sbuf + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-        ptx::tmem_ld32(sbuf + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-        ptx::tmem_ld32(sbuf + (half ^ 1) * 64, *reinterpret_cast<uint32_t(*)[32]>(&so[0]));
-        ptx::tmem_ld32(sbuf + (half ^ 1) * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&so[32]));
+        uint32_t sr[64];
+        ptx::tmem_ld32(t_row + (g & 1) * HN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+        ptx::tmem_ld32(t_row + (g & 1) * HN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
         ptx::tmem_wait_ld();
-        const int kvalid_o = kvalid + (half ? 64 : -64);  // valid keys of the other half
-        if (kvalid < 64) {  // padding keys of a partial block -> -inf (attention.py:193)
+        if (hvalid < HN) {  // padding keys of a partial block -> -inf (attention.py:193)
 #pragma unroll
           for (int e = 0; e < 64; ++e)
-            if (e >= kvalid) sr[e] = __float_as_uint(-INFINITY);
-        }
-        if (kvalid_o < 64) {
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (e >= kvalid_o) so[e] = __float_as_uint(-INFINITY);
+            if (e >= hvalid) sr[e] = __float_as_uint(-INFINITY);
         }
         float mx8[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) mx8[e] = fmaxf(__uint_as_float(sr[e]), __uint_as_float(so[e]));
+        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
 #pragma unroll
-        for (int e = 8; e < 64; e += 8)
+        for (int e = 8; e < 64; e += 16)
 #pragma unroll
-          for (int k2 = 0; k2 < 8; ++k2)
-            mx8[k2] = fmax3(mx8[k2], __uint_as_float(sr[e + k2]), __uint_as_float(so[e + k2]));
+          for (int q = 0; q < 8; ++q)
+            mx8[q] = fmax3(mx8[q], __uint_as_float(sr[e + q]), __uint_as_float(sr[e + 8 + q]));
         const float mraw = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]),
                                  fmaxf(mx8[6], mx8[7]));
         // block max in the scaled log2 domain (scale > 0 keeps the argmax)
-        const float m_blk = fmaf(mraw, scale_log2, bias);
+        const float m_blk = (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
         const float m_new = fmaxf(m_run, m_blk);
         const bool first = (t == 0);
         const bool need = !first && (m_new > m_run + RESCALE_THRESHOLD);
@@ -563,43 +533,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           acc2[e & 3] = fadd2(acc2[e & 3], f2_pack(p0, p1));
           pk[e] = ptx::pack_bf16(p0, p1);
         }
-        ptx::tmem_st32(sbuf + half * 32, pk);
+        ptx::tmem_st32(t_row + (g & 1) * HN, pk);
         const uint64_t sum2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
-        l_run = l_run * alpha + (f2_lo(sum2) + f2_hi(sum2));  // this half's share of l
+        l_run = l_run * alpha + (f2_lo(sum2) + f2_hi(sum2));
         m_run = m_use;
         if (__any_sync(0xffffffffu, need)) {
           // O is final only once PV(t-1) retired: o_done completes once per PV
           ptx::mbar_wait(&bars->o_done, (g - 1) & 1);
           ptx::tc_fence_after();
 #pragma unroll 1
-          for (int c = 0; c < OH / 32; ++c) {
+          for (int c = 0; c < D / 32; ++c) {
             uint32_t ov[32];
-            const uint32_t oc = t_row + O_COL + half * OH + c * 32;
-            ptx::tmem_ld32(oc, ov);
+            ptx::tmem_ld32(t_row + O_COL + c * 32, ov);
             ptx::tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            ptx::tmem_st32(oc, ov);
+            ptx::tmem_st32(t_row + O_COL + c * 32, ov);
           }
         }
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
-        if (lane == 0 && (warp == 2 || warp == 9)) trace(dbg_trace, 30 + warp, g);
-        ptx::mbar_arrive(&bars->p_full);
+        ptx::mbar_arrive(&bars->p_full[g & 1]);
       }
       // ---- epilogue: O / l -> bf16 row, padding rows zero (attention.py:203-206)
-      bars->xsum[half][row] = l_run;
-      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-      const float l_tot = l_run + bars->xsum[half ^ 1][row];
       ptx::mbar_wait(&bars->o_full, it & 1);
       ptx::tc_fence_after();
       const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
-      const float inv_l = (row < qvalid && l_tot > 0.f) ? 1.f / l_tot : 0.f;
-      __nv_bfloat16* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn + half * OH;
+      const float inv_l = (row < qvalid) ? 1.f / l_run : 0.f;
+      __nv_bfloat16* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
 #pragma unroll 1
-      for (int c = 0; c < OH / 32; ++c) {
+      for (int c = 0; c < D / 32; ++c) {
         uint32_t ov[32];
-        ptx::tmem_ld32(t_row + O_COL + half * OH + c * 32, ov);
+        ptx::tmem_ld32(t_row + O_COL + c * 32, ov);
         ptx::tmem_wait_ld();
         uint32_t pk[16];
 #pragma unroll
@@ -612,10 +577,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           dst[e] = make_int4((int)pk[4 * e], (int)pk[4 * e + 1], (int)pk[4 * e + 2],
                              (int)pk[4 * e + 3]);
       }
-      // xsum is reused by the next item only after both warps pass the next block barrier
       ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);  // list / item slot free
     }
   }
   ptx::tc_fence_before();
@@ -706,22 +668,13 @@ static int launch_simt(const void* q, const void* k, const void* v, void* o, int
   return check_launch("k_carve_simt");
 }
 
-// TCB_CARVE_DEBUG_NOLOAD bit 0: stream no K/V after the first ring fill; bit 1: skip the
-// softmax (wrong results; used only to measure the pipeline ceilings)
-static int dbg_noload() {
+// TCB_CARVE_DEBUG bit 0: stream no K/V after the first ring fill; bit 1: skip the softmax
+// (wrong results; only to measure the pipeline ceilings)
+static int dbg_flags() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("TCB_CARVE_DEBUG_NOLOAD");
+    const char* e = getenv("TCB_CARVE_DEBUG");
     v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
-static int dbg_trace() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TCB_CARVE_TRACE");
-    v = (e && atoi(e)) ? 1 : 0;
   }
   return v;
 }
@@ -730,11 +683,12 @@ template <int D, int EMU>
 static int launch_tc(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
                      const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
                      cudaStream_t st) {
-  CUtensorMap tk, tv;
+  CUtensorMap tq, tk, tv;
   const int64_t n_pad = (int64_t)s.M_total * s.m;
   int rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::BK))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::BK))) return rc;
+  if ((rc = make_tmap(&tq, q, D, n_pad, s.H, s.sh, s.sn, tc::BM))) return rc;
+  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::HN))) return rc;
+  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::HN))) return rc;
   const int smem = tc::Smem<D>::BYTES;
   static bool attr_set = false;
   if (!attr_set) {
@@ -749,14 +703,13 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int total = s.H * s.M_total;
-  int grid = sms;  // persistent: one CTA (one 512-column TMEM allocation) per SM
+  int grid = 2 * sms;
   if (grid > total) grid = total;
   const float LOG2E = 1.4426950408889634f;
   const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  tc::k_carve_tc<D, EMU><<<grid, tc::NUM_THREADS, smem, st>>>((const __nv_bfloat16*)q, tk, tv,
-                                                              (__nv_bfloat16*)o, s, kv_idx,
+  tc::k_carve_tc<D, EMU><<<grid, tc::NUM_THREADS, smem, st>>>(tq, tk, tv, (__nv_bfloat16*)o, s, kv_idx,
                                                          kv_cnt, work, total, scale_log2,
-                                                         beta * LOG2E, dbg_noload(), dbg_trace());
+                                                         beta * LOG2E, dbg_flags());
   return check_launch("k_carve_tc");
 }
 
@@ -782,35 +735,23 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
                        ((uintptr_t)v % 16 == 0) && ((uintptr_t)o % 16 == 0) &&
                        (stride_n * 2) % 16 == 0 && (stride_h * 2) % 16 == 0;
   const bool tc_ok = dtype == TCB_BF16 && m == 128 && (d == 128 || d == 64) && aligned && work &&
-                     M_v > 0 && M_total <= tc::LIST_CAP;
+                     M_v > 0;
   if (!tc_ok) return launch_simt(q, k, v, o, dtype, s, kv_idx, kv_cnt, beta, as_stream(stream));
   // pairs (of 8) whose exp2 runs on the FMA pipe instead of MUFU; TCB_CARVE_EMU overrides
   static int emu = -1;
   if (emu < 0) {
     const char* env = getenv("TCB_CARVE_EMU");
     emu = env ? atoi(env) : 0;
-    if (emu != 0 && emu != 1 && emu != 2 && emu != 3) emu = 0;
+    if (emu != 0 && emu != 2 && emu != 3 && emu != 4) emu = 0;
   }
   cudaStream_t st = as_stream(stream);
   if (d == 128) {
     switch (emu) {
-      case 1: return launch_tc<128, 1>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-      case 2: return launch_tc<128, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
       case 3: return launch_tc<128, 3>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
+      case 4: return launch_tc<128, 4>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
+      case 2: return launch_tc<128, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
       default: return launch_tc<128, 0>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
     }
   }
   return launch_tc<64, 0>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-}
-
-// Debug only (not part of include/tokencarve_b200.h): reset / read the CTA-0 timeline.
-extern "C" int tcb_debug_trace_read(unsigned long long* host, int cap) {
-  unsigned n = 0;
-  cudaMemcpyFromSymbol(&n, tcb::tc::g_trace_n, sizeof(n));
-  if (n > (unsigned)tcb::tc::TRACE_CAP) n = tcb::tc::TRACE_CAP;
-  if ((int)n > cap) n = cap;
-  cudaMemcpyFromSymbol(host, tcb::tc::g_trace, n * 16);
-  unsigned z = 0;
-  cudaMemcpyToSymbol(tcb::tc::g_trace_n, &z, sizeof(z));
-  return (int)n;
 }
