@@ -1,0 +1,218 @@
+"""Secondary measurements for SURVEY.md §8 configs beyond the bench.py headline (C2):
+
+  * hbm kernels at C2: permute (118,800 x 3,072 bf16 gather), block pool (Q+K), curve
+    build, adjacency build -- achieved GB/s vs the measured HBM peak;
+  * C3: Wan2.1-14B 480p layer (21x30x52, H=40, no text), k=0.08 -- ms/layer, TFLOP/s;
+  * C4: ProRes 2-stage switch at 720p: fused predict_clean+upsample+renoise
+    (33,34,60,16) -> (33,45,80,16), curve + adjacency rebuild at the new dims, and
+    one toy-width permute of the latent;
+  * C5: sparsity sweep on C2, k in {0.01, 0.02, 0.05, 0.08, 0.10, 0.20, 0.30}, p=0.
+
+All timings: CUDA events on the launching stream, median of repeats after warm-up.
+Writes one JSON document (stdout, and --out if given).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import paper_2505_16864_b200 as tcb  # noqa: E402
+from paper_2505_16864_b200 import _native  # noqa: E402
+from paper_2505_16864_b200.attention import _workspace  # noqa: E402
+from paper_2505_16864_b200.partition import mask_words  # noqa: E402
+
+
+def timed(fn, reps=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def peaks():
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return p["hbm_gbs"], p["bf16_tflops"]
+    except Exception:
+        return 6650.0, 1590.0
+
+
+class Layer:
+    """Device buffers + the four launches of one carved-attention layer."""
+
+    def __init__(self, dims, n_cond, H, k_rate, seed=0):
+        self.dims = tcb.GridDims(*dims)
+        self.lay = tcb.build_layout(self.dims, 128, n_cond)
+        self.st = tcb.StaticMasks.build(self.lay, self.dims, tcb.build_curve(self.dims))
+        self.adja = self.st.packed(self.lay)
+        self.H, self.k = H, k_rate
+        L = self.lay
+        g = torch.Generator(device="cuda")
+        g.manual_seed(seed)
+        self.q, self.kk, self.v = (torch.randn((H, L.padded_total, 128), generator=g, device="cuda")
+                                   .to(torch.bfloat16) for _ in range(3))
+        self.o = torch.empty_like(self.q)
+        self.pq = torch.empty((H, L.M_total, 128), dtype=torch.float64, device="cuda")
+        self.pk = torch.empty_like(self.pq)
+        self.R = torch.empty((H, L.M_v, L.M_total), dtype=torch.float64, device="cuda")
+        self.words = mask_words(L.M_total)
+        self.bits = torch.empty((H, L.M_v, self.words), dtype=torch.int32, device="cuda")
+        self.kv_idx = torch.empty((H, L.M_v, L.M_total), dtype=torch.int32, device="cuda")
+        self.kv_cnt = torch.empty((H, L.M_v), dtype=torch.int32, device="cuda")
+        self.work = _workspace(self.q.device)
+        self.s = torch.cuda.current_stream().cuda_stream
+
+    def mask(self):
+        L, H = self.lay, self.H
+        n_floor = tcb.SelectionParams(k=self.k, p=0.0).n_floor(L.M_v)
+        _native.call("tcb_block_pool", self.q.data_ptr(), self.kk.data_ptr(), 1, self.q.stride(0),
+                     self.q.stride(1), H, 128, 128, L.M_v, L.M_total, L.n_valid, L.n_cond,
+                     self.pq.data_ptr(), self.pk.data_ptr(), self.s)
+        _native.call("tcb_block_scores", self.pq.data_ptr(), L.M_total, self.pk.data_ptr(), H, L.M_v,
+                     L.M_total, 128, self.R.data_ptr(), self.s)
+        _native.call("tcb_block_select_scores", self.R.data_ptr(), H, L.M_v, L.M_total,
+                     self.adja.data_ptr(), self.words, n_floor, 0.0, 1, self.bits.data_ptr(),
+                     self.kv_idx.data_ptr(), self.kv_cnt.data_ptr(), self.s)
+
+    def carve(self):
+        L = self.lay
+        _native.call("tcb_carve_fwd", self.q.data_ptr(), self.kk.data_ptr(), self.v.data_ptr(),
+                     self.o.data_ptr(), 1, self.q.stride(0), self.q.stride(1),
+                     self.kv_idx.data_ptr(), self.kv_cnt.data_ptr(), self.H, 128, 128, L.M_v,
+                     L.M_total, L.n_valid, L.n_cond, 0.0, self.work.data_ptr(), self.s)
+
+    def pairs(self):
+        return int(self.kv_cnt.sum().item()) + self.H * self.lay.M_c * self.lay.M_total
+
+
+def layer_record(name, dims, n_cond, H, k):
+    lay = Layer(dims, n_cond, H, k)
+    t_mask = timed(lay.mask)
+    lay.mask()
+    t_carve = timed(lay.carve)
+    pairs = lay.pairs()
+    flops = 4.0 * 128 * 128 * 128 * pairs
+    _, tf = peaks()
+    rec = {"config": name, "dims": list(dims), "heads": H, "k": k, "p": 0.0,
+           "kept_pairs": pairs, "kept_fraction": round(pairs / (H * lay.lay.M_total ** 2), 4),
+           "mask_ms": round(t_mask, 4), "carve_ms": round(t_carve, 4),
+           "layer_ms": round(t_mask + t_carve, 4),
+           "kept_tflops": round(flops / (t_carve * 1e-3) / 1e12, 1),
+           "frac_of_measured_bf16": round(flops / (t_carve * 1e-3) / 1e12 / tf, 4)}
+    del lay
+    torch.cuda.empty_cache()
+    return rec
+
+
+def hbm_records():
+    hbm, _ = peaks()
+    out = []
+    dims = tcb.GridDims(33, 45, 80)
+    perm = tcb.build_curve(dims)
+    n = dims.n_cells
+    x = torch.randn((n, 3072), device="cuda").to(torch.bfloat16)
+    y = torch.empty_like(x)
+    t = timed(lambda: tcb.gather_rows(x, perm.forward, out=y), reps=20)
+    byts = 2 * x.numel() * 2 + 4 * n
+    out.append({"kernel": "permute_rows (K2)", "shape": "118800 x 3072 bf16", "ms": round(t, 4),
+                "gbs": round(byts / (t * 1e-3) / 1e9, 1), "frac_of_hbm": round(byts / (t * 1e-3) / 1e9 / hbm, 3)})
+    del x, y
+    lay = tcb.build_layout(dims, 128, 256)
+    q = torch.randn((24, lay.padded_total, 128), device="cuda").to(torch.bfloat16)
+    k = torch.randn_like(q)
+    pq = torch.empty((24, lay.M_total, 128), dtype=torch.float64, device="cuda")
+    pk = torch.empty_like(pq)
+    s = torch.cuda.current_stream().cuda_stream
+    t = timed(lambda: _native.call("tcb_block_pool", q.data_ptr(), k.data_ptr(), 1, q.stride(0), q.stride(1), 24,
+                                   128, 128, lay.M_v, lay.M_total, lay.n_valid, lay.n_cond, pq.data_ptr(),
+                                   pk.data_ptr(), s), reps=20)
+    byts = 2 * q.numel() * 2 + 2 * pq.numel() * 8
+    out.append({"kernel": "block_pool Q+K (K3)", "shape": "2 x 24 x 119168 x 128 bf16", "ms": round(t, 4),
+                "gbs": round(byts / (t * 1e-3) / 1e9, 1), "frac_of_hbm": round(byts / (t * 1e-3) / 1e9 / hbm, 3)})
+    del q, k
+    fwd = torch.empty(n, dtype=torch.int32, device="cuda")
+    inv = torch.empty_like(fwd)
+    t = timed(lambda: _native.call("tcb_curve_build", 33, 45, 80, fwd.data_ptr(), inv.data_ptr(), s), reps=20)
+    out.append({"kernel": "curve_build (K1)", "shape": "33x45x80", "ms": round(t, 4),
+                "gbs": round(8 * n / (t * 1e-3) / 1e9, 1), "note": "latency bound (0.95 MB written)"})
+    words = mask_words(lay.M_total)
+    adja = torch.empty((lay.M_v, words), dtype=torch.int32, device="cuda")
+    t = timed(lambda: _native.call("tcb_adjacency_build", inv.data_ptr(), 33, 45, 80, 128, lay.M_v, words,
+                                   adja.data_ptr(), s), reps=20)
+    out.append({"kernel": "adjacency_build (K6)", "shape": "33x45x80, m=128", "ms": round(t, 4),
+                "note": "13 neighbour offsets per cell, packed atomics"})
+    return out
+
+
+def c4_records():
+    hbm, _ = peaks()
+    src, dst, C = (33, 34, 60), tcb.GridDims(33, 45, 80), 16
+    x = torch.randn((*src, C), device="cuda")
+    vel = torch.randn_like(x)
+    eps = torch.randn((*dst.as_tuple(), C), device="cuda")
+    out = torch.empty_like(eps)
+    s = torch.cuda.current_stream().cuda_stream
+    t = timed(lambda: _native.call("tcb_upsample_renoise", x.data_ptr(), vel.data_ptr(), eps.data_ptr(),
+                                   out.data_ptr(), *src, *dst.as_tuple(), C, 0.899083, 1, 0, 0, s), reps=20)
+    byts = 2 * x.numel() * 4 + 2 * out.numel() * 4
+    recs = [{"kernel": "upsample_renoise (K9/K10, eps supplied)", "shape": "(33,34,60,16)->(33,45,80,16)",
+             "ms": round(t, 4), "gbs": round(byts / (t * 1e-3) / 1e9, 1)}]
+    t = timed(lambda: _native.call("tcb_upsample_renoise", x.data_ptr(), vel.data_ptr(), None, out.data_ptr(),
+                                   *src, *dst.as_tuple(), C, 0.899083, 2, 1234, 0, s), reps=20)
+    recs.append({"kernel": "upsample_renoise (K9/K10, in-kernel Philox)", "shape": "(33,34,60,16)->(33,45,80,16)",
+                 "ms": round(t, 4), "gbs": round((byts - out.numel() * 4) / (t * 1e-3) / 1e9, 1)})
+
+    def switch():
+        perm = tcb.build_curve(dst)
+        lay = tcb.build_layout(dst, 128, 256)
+        tcb.StaticMasks.build(lay, dst, perm)
+        z = tcb.switch_stage(x, vel, 0.899083, dst, 1234)
+        tcb.gather_rows(z.reshape(-1, C), perm.forward)
+
+    t = timed(switch, reps=10)
+    recs.append({"kernel": "full stage switch (switch + curve + statics + permute)", "ms": round(t, 4),
+                 "note": "includes host-side launches of 6 kernels"})
+    return recs
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--skip-sweep", action="store_true")
+    a = ap.parse_args()
+    res = {"device": torch.cuda.get_device_name(0), "hbm": hbm_records(), "c4_stage_switch": c4_records()}
+    res["c3"] = layer_record("C3 Wan2.1-14B 480p 21x30x52, H=40, no text", (21, 30, 52), 0, 40, 0.08)
+    res["c2"] = layer_record("C2 HunyuanVideo 720p 33x45x80 + 256 text, H=24", (33, 45, 80), 256, 24, 0.08)
+    if not a.skip_sweep:
+        res["c5_sweep"] = [layer_record("C5 sweep on C2", (33, 45, 80), 256, 24, k)
+                           for k in (0.01, 0.02, 0.05, 0.08, 0.10, 0.20, 0.30)]
+    # dense-FA roofline reference for C5: all 931^2 x 24 pairs at the measured bf16 peak
+    _, tf = peaks()
+    dense = 4.0 * 128 ** 3 * 931 ** 2 * 24
+    res["c5_dense_roofline_ms"] = round(dense / (tf * 1e12) * 1e3, 3)
+    text = json.dumps(res, indent=1)
+    print(text)
+    if a.out:
+        with open(a.out, "w") as fh:
+            fh.write(text + "\n")
+
+
+if __name__ == "__main__":
+    main()

@@ -17,6 +17,12 @@ METRICS = [
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram % peak"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM % peak"),
     ("sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe % active"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor pipe % elapsed"),
+    ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed", "tcgen05 (tc) pipe % elapsed"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor memory-path % elapsed"),
+    ("gpc__cycles_elapsed.avg.per_second", "SM clock during kernel"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
+    ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue active %"),
     ("sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active", "tmem pipe %"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64 pipe %"),
     ("sm__pipe_xu_cycles_active.avg.pct_of_peak_sustained_active", "XU (MUFU) pipe %"),
