@@ -590,373 +590,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
 
 }  // namespace tc
 
-// =====================================================================================
-// tcgen05 kernel, variant "q-in-TMEM": Q lives in TMEM as the A operand of QK^T (TS form),
-// so shared memory only streams K and V.  Steps are 32-key quarters of a kv block so that
-// Q (64 cols) + a double-buffered S (2 x 32 cols) + O (128 cols) fit 256 TMEM columns and
-// two CTAs still share each SM.  Everything else follows tc:: (same roles and barriers).
-// =====================================================================================
-namespace tq {
-
-using tc::BM;
-using tc::BK;
-using tc::make_idesc;
-using tc::make_sdesc;
-using tc::f2_pack;
-using tc::f2_lo;
-using tc::f2_hi;
-using tc::ffma2;
-using tc::fadd2;
-using tc::fmax3;
-using tc::exp2_poly2;
-using tc::KvList;
-using tc::RESCALE_THRESHOLD;
-
-constexpr int SN = 32;            // keys per step (a quarter of a kv block)
-constexpr int STEPS = BK / SN;    // steps per kv block
-constexpr int NUM_THREADS = 192;  // w0 TMA+scheduler, w1 MMA+TMEM owner, w2..w5 Q/softmax
-constexpr int TMEM_COLS = 256;
-constexpr int Q_COL = 0;          // Q as packed bf16 pairs: D/2 columns
-constexpr int S_COL = 64;         // S0 [64, 96), S1 [96, 128)
-constexpr int O_COL = 128;        // O [128, 128 + D)
-constexpr int K_SLOTS = 8;        // K quarter tiles in flight
-constexpr int V_SLOTS = 6;        // V quarter tiles in flight
-
-template <int D>
-struct Smem {
-  static constexpr int STEP_BYTES = SN * D * 2;  // 32 x D bf16
-  static constexpr int CHUNKS = D / 64;
-  static constexpr int S_CHUNK = SN * 128;       // bytes per 64-col chunk of a step tile
-  static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = OFF_K + K_SLOTS * STEP_BYTES;
-  static constexpr int OFF_BAR = OFF_V + V_SLOTS * STEP_BYTES;
-  static constexpr int BYTES = OFF_BAR + 512;
-};
-
-struct Bars {
-  uint64_t q_full, o_full, o_done;
-  uint64_t p_full[2];
-  uint64_t s_full[2];
-  uint64_t k_full[K_SLOTS], k_empty[K_SLOTS];
-  uint64_t v_full[V_SLOTS], v_empty[V_SLOTS];
-  uint64_t sched_full[2], sched_empty[2];
-  int sched_item[2];
-  uint32_t tmem_base;
-};
-static_assert(sizeof(Bars) <= 512, "barrier block must fit the reserved smem");
-
-template <int D, int EMU>
-__global__ void __launch_bounds__(NUM_THREADS, 2)
-    k_carve_tq(const __nv_bfloat16* __restrict__ q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
-               CarveShape s, const int32_t* __restrict__ kv_idx,
-               const int32_t* __restrict__ kv_cnt, int* __restrict__ counter, int total_items,
-               float scale_log2, float beta_log2, int dbg) {
-  using L = Smem<D>;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sK = smem + L::OFF_K;
-  uint8_t* sV = smem + L::OFF_V;
-  Bars* bars = reinterpret_cast<Bars*>(smem + L::OFF_BAR);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    if (ptx::smem_u32(smem) & 1023u) __trap();
-    ptx::mbar_init(&bars->q_full, 128);
-    ptx::mbar_init(&bars->o_full, 1);
-    ptx::mbar_init(&bars->o_done, 1);
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&bars->p_full[i], 128);
-      ptx::mbar_init(&bars->s_full[i], 1);
-      ptx::mbar_init(&bars->sched_full[i], 1);
-      ptx::mbar_init(&bars->sched_empty[i], 1 + 4);
-    }
-    for (int i = 0; i < K_SLOTS; ++i) {
-      ptx::mbar_init(&bars->k_full[i], 1);
-      ptx::mbar_init(&bars->k_empty[i], 1);
-    }
-    for (int i = 0; i < V_SLOTS; ++i) {
-      ptx::mbar_init(&bars->v_full[i], 1);
-      ptx::mbar_init(&bars->v_empty[i], 1);
-    }
-    ptx::fence_mbar_init();
-    ptx::tma_prefetch_desc(&tm_k);
-    ptx::tma_prefetch_desc(&tm_v);
-  }
-  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(&bars->tmem_base);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
-
-  if (warp == 0) {
-    // ============================ TMA producer + scheduler ============================
-    const uint64_t pol_kv = ptx::policy_evict_last();
-    uint32_t it = 0, gk = 0, gv = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      int item = 0;
-      if (lane == 0) {
-        ptx::mbar_wait(&bars->sched_empty[slot], ((it >> 1) & 1) ^ 1);
-        item = atomicAdd(counter, 1);
-        if (item >= total_items) item = -1;
-        bars->sched_item[slot] = item;
-        ptx::mbar_arrive(&bars->sched_full[slot]);
-      }
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-      KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      const int T = STEPS * n;
-      auto load = [&](const CUtensorMap* tm, uint8_t* base, uint64_t* full, uint64_t* empty,
-                      int slots, uint32_t& cnt, int t) {
-        const int b = kl.block(t / STEPS);
-        if (lane == 0) {
-          const int sl = cnt % slots;
-          ptx::mbar_wait(&empty[sl], ((cnt / slots) & 1) ^ 1);
-          if ((dbg & 1) && cnt >= (uint32_t)slots) {
-            ptx::mbar_arrive(&full[sl]);
-          } else {
-            ptx::mbar_arrive_expect_tx(&full[sl], L::STEP_BYTES);
-#pragma unroll
-            for (int c = 0; c < L::CHUNKS; ++c)
-              ptx::tma_load_3d(base + sl * L::STEP_BYTES + c * L::S_CHUNK, tm, &full[sl], c * 64,
-                               b * BK + (t % STEPS) * SN, h, pol_kv);
-          }
-        }
-        ++cnt;
-      };
-      // MMA consumption order: K0, K1, V0, K2, V1, ..., V(T-1)
-      if (T > 0) load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, 0);
-      for (int t = 0; t < T; ++t) {
-        if (t + 1 < T) load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, t + 1);
-        load(&tm_v, sV, bars->v_full, bars->v_empty, V_SLOTS, gv, t);
-      }
-    }
-  } else if (warp == 1) {
-    // ============================ MMA issuer ============================
-    if (lane == 0) {
-      constexpr uint32_t IDESC_S = make_idesc(BM, SN, 0);  // Q (TMEM) x K (K-major smem)
-      constexpr uint32_t IDESC_O = make_idesc(BM, D, 1);   // P (TMEM) x V (MN-major smem)
-      const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
-      uint32_t it = 0, gk = 0, gv = 0, gs = 0, gp = 0;
-      auto issue_s = [&]() {  // S(gs) = Q K(gs)^T into buffer gs & 1
-        const int sl = gk % K_SLOTS;
-        ptx::mbar_wait(&bars->k_full[sl], (gk / K_SLOTS) & 1);
-        ptx::tc_fence_after();
-        const uint32_t kbase = aK + sl * L::STEP_BYTES;
-        const uint32_t dcol = tmem + S_COL + (gs & 1) * SN;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t koff = (kk >> 2) * L::S_CHUNK + (kk & 3) * 32;
-          ptx::mma_ts(dcol, tmem + Q_COL + kk * 8, make_sdesc(kbase + koff, 16, 1024), IDESC_S,
-                      kk > 0 ? 1u : 0u);
-        }
-        ptx::mma_commit(&bars->k_empty[sl]);
-        ptx::mma_commit(&bars->s_full[gs & 1]);
-        ++gk;
-        ++gs;
-      };
-      for (;; ++it) {
-        const int slot = it & 1;
-        ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
-        const int item = bars->sched_item[slot];
-        ptx::mbar_arrive(&bars->sched_empty[slot]);
-        if (item < 0) break;
-        int h, qb;
-        decode_item(item, s, h, qb);
-        const bool vis = qb < s.M_v;
-        const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-        const int T = STEPS * n;
-        ptx::mbar_wait(&bars->q_full, it & 1);  // Q written to TMEM by the softmax warps
-        ptx::tc_fence_after();
-        if (T > 0) issue_s();
-        for (int t = 0; t < T; ++t) {
-          if (t + 1 < T) issue_s();
-          ptx::mbar_wait(&bars->p_full[gp & 1], (gp >> 1) & 1);
-          const int vs = gv % V_SLOTS;
-          ptx::mbar_wait(&bars->v_full[vs], (gv / V_SLOTS) & 1);
-          ptx::tc_fence_after();
-          const uint32_t vbase = aV + vs * L::STEP_BYTES;
-          const uint32_t pcol = tmem + S_COL + (gp & 1) * SN;
-#pragma unroll
-          for (int kk = 0; kk < SN / 16; ++kk) {
-            ptx::mma_ts(tmem + O_COL, pcol + kk * 8,
-                        make_sdesc(vbase + kk * 16 * 128, L::S_CHUNK, 1024), IDESC_O,
-                        (t > 0 || kk > 0) ? 1u : 0u);
-          }
-          ptx::mma_commit(&bars->v_empty[vs]);
-          ptx::mma_commit(&bars->o_done);
-          ++gv;
-          ++gp;
-        }
-        ptx::mma_commit(&bars->o_full);
-      }
-    }
-    __syncwarp();
-  } else {
-    // ============================ Q load / softmax / correction / epilogue ============================
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
-    uint32_t it = 0, g = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
-      const int item = bars->sched_item[slot];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-      KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      const int T = STEPS * n;
-      // ---- Q row -> TMEM (A operand, packed bf16 pairs); every S MMA of the previous item
-      // has been consumed by these warps, so the old Q is dead.
-      {
-        const int4* qrow = reinterpret_cast<const int4*>(q + (int64_t)h * s.sh +
-                                                         ((int64_t)qb * BM + row) * s.sn);
-#pragma unroll
-        for (int half = 0; half < D / 64; ++half) {
-          uint32_t qa[32];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int4 v4 = __ldg(qrow + half * 8 + e);
-            qa[4 * e] = (uint32_t)v4.x;
-            qa[4 * e + 1] = (uint32_t)v4.y;
-            qa[4 * e + 2] = (uint32_t)v4.z;
-            qa[4 * e + 3] = (uint32_t)v4.w;
-          }
-          ptx::tmem_st32(t_row + Q_COL + half * 32, qa);
-        }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars->q_full);
-      }
-      float m_run = -INFINITY, l_run = 0.f;
-      int b = 0, kvalid = BK;
-      float bias = 0.f;
-      for (int t = 0; t < T; ++t, ++g) {
-        if (t % STEPS == 0) {
-          b = kl.block(t / STEPS);
-          kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond);
-          bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
-        }
-        const int svalid = kvalid - (t % STEPS) * SN;  // valid keys in this step (may be <= 0)
-        const uint32_t sbuf = t_row + S_COL + (g & 1) * SN;
-        ptx::mbar_wait(&bars->s_full[g & 1], (g >> 1) & 1);
-        ptx::tc_fence_after();
-        if (dbg & 2) {
-          l_run = 1.f;
-          ptx::mbar_arrive(&bars->p_full[g & 1]);
-          continue;
-        }
-        uint32_t sr[32];
-        ptx::tmem_ld32(sbuf, sr);
-        ptx::tmem_wait_ld();
-        if (svalid < SN) {  // padding keys -> -inf (attention.py:193)
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (e >= svalid) sr[e] = __float_as_uint(-INFINITY);
-        }
-        float mx8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
-#pragma unroll
-        for (int e = 8; e < 24; e += 16)
-#pragma unroll
-          for (int k2 = 0; k2 < 8; ++k2)
-            mx8[k2] = fmax3(mx8[k2], __uint_as_float(sr[e + k2]), __uint_as_float(sr[e + 8 + k2]));
-#pragma unroll
-        for (int k2 = 0; k2 < 8; ++k2) mx8[k2] = fmaxf(mx8[k2], __uint_as_float(sr[24 + k2]));
-        const float mraw = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]),
-                                 fmaxf(mx8[6], mx8[7]));
-        const float m_blk = (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
-        const float m_new = fmaxf(m_run, m_blk);
-        const bool first = (t == 0);
-        const bool need = !first && (m_new > m_run + RESCALE_THRESHOLD);
-        const float m_use = (first || need) ? m_new : m_run;
-        const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
-        const float c0 = bias - m_use;
-        const uint64_t sc2 = f2_pack(scale_log2, scale_log2), c02 = f2_pack(c0, c0);
-        uint64_t acc2[4] = {0, 0, 0, 0};
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const uint64_t x = ffma2(f2_pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])),
-                                   sc2, c02);
-          float p0, p1;
-          if ((e & 7) >= 8 - EMU) {
-            const uint64_t pp = exp2_poly2(x);
-            p0 = f2_lo(pp);
-            p1 = f2_hi(pp);
-          } else {
-            p0 = ptx::ex2(f2_lo(x));
-            p1 = ptx::ex2(f2_hi(x));
-          }
-          acc2[e & 3] = fadd2(acc2[e & 3], f2_pack(p0, p1));
-          pk[e] = ptx::pack_bf16(p0, p1);
-        }
-        ptx::tmem_st16(sbuf, pk);
-        const uint64_t sum2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
-        l_run = l_run * alpha + (f2_lo(sum2) + f2_hi(sum2));
-        m_run = m_use;
-        if (__any_sync(0xffffffffu, need)) {
-          ptx::mbar_wait(&bars->o_done, (g - 1) & 1);  // PV(t-1) retired -> O is final
-          ptx::tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            ptx::tmem_ld32(t_row + O_COL + c * 32, ov);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            ptx::tmem_st32(t_row + O_COL + c * 32, ov);
-          }
-        }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars->p_full[g & 1]);
-      }
-      // ---- epilogue: O / l -> bf16 row, padding rows zero (attention.py:203-206)
-      ptx::mbar_wait(&bars->o_full, it & 1);
-      ptx::tc_fence_after();
-      const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
-      const float inv_l = (row < qvalid && l_run > 0.f) ? 1.f / l_run : 0.f;
-      __nv_bfloat16* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t ov[32];
-        ptx::tmem_ld32(t_row + O_COL + c * 32, ov);
-        ptx::tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pk[e] = ptx::pack_bf16(__uint_as_float(ov[2 * e]) * inv_l,
-                                 __uint_as_float(ov[2 * e + 1]) * inv_l);
-        int4* dst = reinterpret_cast<int4*>(orow + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          dst[e] = make_int4((int)pk[4 * e], (int)pk[4 * e + 1], (int)pk[4 * e + 2],
-                             (int)pk[4 * e + 3]);
-      }
-      ptx::tc_fence_before();
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<TMEM_COLS>(tmem);
-  }
-}
-
-}  // namespace tq
 
 // ---------------------------------------------------------------- host helpers
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1081,51 +714,6 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
   return check_launch("k_carve_tc");
 }
 
-template <int EMU>
-static int launch_tq(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                     const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
-                     cudaStream_t st) {
-  constexpr int D = 128;
-  CUtensorMap tk, tv;
-  const int64_t n_pad = (int64_t)s.M_total * s.m;
-  int rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tq::SN))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tq::SN))) return rc;
-  const int smem = tq::Smem<D>::BYTES;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tq::k_carve_tq<D, EMU>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
-    attr_set = true;
-  }
-  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
-  if (e != cudaSuccess) return set_error(TCB_ECUDA, "memset counter: %s", cudaGetErrorString(e));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int total = s.H * s.M_total;
-  int grid = 2 * sms;
-  if (grid > total) grid = total;
-  const float LOG2E = 1.4426950408889634f;
-  const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  tq::k_carve_tq<D, EMU><<<grid, tq::NUM_THREADS, smem, st>>>(
-      (const __nv_bfloat16*)q, tk, tv, (__nv_bfloat16*)o, s, kv_idx, kv_cnt, work, total,
-      scale_log2, beta * LOG2E, dbg_flags());
-  return check_launch("k_carve_tq");
-}
-
-// TCB_CARVE_VARIANT: 0 = half-step kernel with Q in smem (tc), 1 = quarter-step kernel with
-// Q in TMEM (tq)
-static int carve_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TCB_CARVE_VARIANT");
-    v = e ? atoi(e) : 1;
-  }
-  return v;
-}
-
 extern "C" int tcb_carve_fwd_simt(const void* q, const void* k, const void* v, void* o, int dtype,
                                   int64_t stride_h, int64_t stride_n, const int32_t* kv_idx,
                                   const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
@@ -1158,13 +746,6 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
     if (emu != 0 && emu != 2 && emu != 3 && emu != 4) emu = 0;
   }
   cudaStream_t st = as_stream(stream);
-  if (d == 128 && carve_variant() == 1) {
-    switch (emu) {
-      case 2: return launch_tq<2>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-      case 3: return launch_tq<3>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-      default: return launch_tq<0>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-    }
-  }
   if (d == 128) {
     switch (emu) {
       case 3: return launch_tc<128, 3>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
