@@ -232,10 +232,7 @@ def run_gpu(args):
         out_bytes = ho.numel() * ho.element_size()
 
         def e2e_step():
-            dq, dk, dv = (t.to(dev, non_blocking=True) for t in (hq, hk, hv))
-            mask, _ = tcb.build_block_mask(dq, dk, layout, statics, params)
-            out = tcb.carve_attention(tcb.AttentionInputs(q=dq, k=dk, v=dv, layout=layout), mask)
-            ho.copy_(out, non_blocking=True)
+            tcb.carve_layer(hq, hk, hv, layout, statics, params, out=ho)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -248,7 +245,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         e2e = {"value": round(a.elapsed_time(b) / n_e2e, 3), "unit": "ms",
                "h2d_bytes_per_step": inp_bytes, "d2h_bytes_per_step": out_bytes,
-               "path": "tcb.build_block_mask + tcb.carve_attention on pinned host Q/K/V"}
+               "path": "tcb.carve_layer on pinned host Q/K/V: head-chunked H2D / mask+carve / D2H on 3 streams"}
 
     if rank != 0:
         if world > 1:

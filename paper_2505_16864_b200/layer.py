@@ -1,0 +1,135 @@
+"""One carved-attention layer = ``build_block_mask`` + ``carve_attention``.
+
+This is the pair of calls the reference's attention layer makes
+(``toy_transformer_denoiser``, pipeline.py:432-433), exposed as one entry point so
+that host-resident Q/K/V can be streamed through the GPU.  Carved attention is
+independent per head (attention.py:236): pooling, scores, selection and
+the sparse flash-attention of head h read only head h.  With host inputs the layer
+therefore runs as a head-chunked pipeline on three CUDA streams --
+
+    copy stream   H2D  q/k/v[chunk c+1]
+    compute       pool -> scores -> select -> carve on chunk c      (4 launches)
+    copy stream   D2H  out[chunk c-1]
+
+-- so the PCIe transfers overlap the kernels and each other (PCIe is full duplex).
+Each chunk's launches are the same kernels on head-slice views, so the result is
+bitwise the unchunked one.  Device inputs take the plain two-call path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _dev, _native
+from .attention import AmplifierBias, _workspace
+from .errors import ShapeError
+from .masks import BlockMask, SelectionParams
+from .partition import BlockLayout, StaticMasks, mask_words
+
+__all__ = ["carve_layer"]
+
+_streams: dict = {}
+
+
+def _copy_streams(dev: torch.device):
+    s = _streams.get(dev)
+    if s is None:
+        s = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        _streams[dev] = s
+    return s
+
+
+def _launch_chunk(q, k, v, o, pq, pk, R, bits, kv_idx, kv_cnt, adja, layout, params, beta, work,
+                  sptr):
+    """pool -> scores -> softmax/select/union -> carve on head-slice views (H_c, N, d)."""
+    Hc, _, d = q.shape
+    sh, sn = q.stride(0), q.stride(1)
+    Mv, Mt = layout.M_v, layout.M_total
+    _native.call("tcb_block_pool", q.data_ptr(), k.data_ptr(), _dev.code_of(q.dtype), sh, sn, Hc, d,
+                 layout.m, Mv, Mt, layout.n_valid, layout.n_cond, pq.data_ptr(), pk.data_ptr(), sptr)
+    _native.call("tcb_block_scores", pq.data_ptr(), Mt, pk.data_ptr(), Hc, Mv, Mt, d, R.data_ptr(),
+                 sptr)
+    _native.call("tcb_block_select_scores", R.data_ptr(), Hc, Mv, Mt, _native.ptr(adja),
+                 mask_words(Mt), params.n_floor(Mv), float(params.p), 1, bits.data_ptr(),
+                 kv_idx.data_ptr(), kv_cnt.data_ptr(), sptr)
+    _native.call("tcb_carve_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                 _dev.code_of(q.dtype), sh, sn, kv_idx.data_ptr(), kv_cnt.data_ptr(), Hc, d, layout.m,
+                 Mv, Mt, layout.n_valid, layout.n_cond, float(beta), work.data_ptr(), sptr)
+
+
+def carve_layer(q, k, v, layout: BlockLayout, statics: StaticMasks, params: SelectionParams,
+                beta: AmplifierBias = AmplifierBias(0.0), *, out=None,
+                heads_per_chunk: int | None = None):
+    """Carved attention for all heads; returns ``(out, BlockMask)``.
+
+    q, k, v: (H, N_pad, d) bf16 or fp32, all three on the device or all three on the
+    host (torch CPU tensors -- pinned for asynchronous copies -- or numpy arrays).
+    Host inputs give a host output, complete on return (``out`` may supply a pinned
+    (H, N_pad, d) tensor; numpy inputs return numpy); the returned mask stays on the device.
+    """
+    on_host = not (isinstance(q, torch.Tensor) and q.is_cuda)
+    if not on_host:
+        from .attention import AttentionInputs, carve_attention
+        from .masks import build_block_mask
+
+        mask, _ = build_block_mask(q, k, layout, statics, params)
+        o = carve_attention(AttentionInputs(q=q, k=k, v=v, layout=layout), mask, beta)
+        if out is not None:
+            out.copy_(o)
+            o = out
+        return o, mask
+
+    numpy_in = _dev.is_numpy(q)
+    hq, hk, hv = (torch.from_numpy(np.ascontiguousarray(x)) if _dev.is_numpy(x) else x.contiguous()
+                  for x in (q, k, v))
+    if not (hq.shape == hk.shape == hv.shape) or hq.ndim != 3:
+        raise ShapeError(f"Q/K/V must share one (heads, N, d_k) shape, got {tuple(hq.shape)}/"
+                         f"{tuple(hk.shape)}/{tuple(hv.shape)}")
+    if hq.shape[1] != layout.padded_total:
+        raise ShapeError(f"token axis {hq.shape[1]} != padded token count {layout.padded_total}")
+    if hq.dtype not in (torch.float32, torch.bfloat16) or hk.dtype != hq.dtype or hv.dtype != hq.dtype:
+        raise ShapeError(f"Q/K/V must all be float32 or all bfloat16, got {hq.dtype}")
+    H, N, d = hq.shape
+    dev = _dev.device()
+    if out is None:
+        out = torch.empty((H, N, d), dtype=hq.dtype, pin_memory=True)
+    elif tuple(out.shape) != (H, N, d) or out.dtype != hq.dtype or out.is_cuda:
+        raise ShapeError("out must be a host tensor of the input shape and dtype")
+    Mv, Mt = layout.M_v, layout.M_total
+    words = mask_words(Mt)
+    dq, dk, dv = (torch.empty((H, N, d), dtype=hq.dtype, device=dev) for _ in range(3))
+    do = torch.empty((H, N, d), dtype=hq.dtype, device=dev)
+    pq = torch.empty((H, Mt, d), dtype=torch.float64, device=dev)
+    pk = torch.empty_like(pq)
+    R = torch.empty((H, Mv, Mt), dtype=torch.float64, device=dev)
+    bits = torch.empty((H, Mv, words), dtype=torch.int32, device=dev)
+    kv_idx = torch.empty((H, Mv, Mt), dtype=torch.int32, device=dev)
+    kv_cnt = torch.empty((H, Mv), dtype=torch.int32, device=dev)
+    adja = statics.packed(layout)
+    work = _workspace(dev)
+
+    comp = torch.cuda.current_stream(dev)
+    s_in, s_out = _copy_streams(dev)
+    hc = heads_per_chunk or max(1, H // 8)
+    chunks = [(h0, min(H, h0 + hc)) for h0 in range(0, H, hc)]
+    s_in.wait_stream(comp)  # device buffers may be recycled from work still queued on comp
+    s_out.wait_stream(comp)
+    for h0, h1 in chunks:
+        with torch.cuda.stream(s_in):
+            for src, dst in ((hq, dq), (hk, dk), (hv, dv)):
+                dst[h0:h1].copy_(src[h0:h1], non_blocking=True)
+        comp.wait_stream(s_in)
+        sl = slice(h0, h1)
+        _launch_chunk(dq[sl], dk[sl], dv[sl], do[sl], pq[sl], pk[sl], R[sl], bits[sl], kv_idx[sl],
+                      kv_cnt[sl], adja, layout, params, beta.beta, work, comp.cuda_stream)
+        s_out.wait_stream(comp)
+        with torch.cuda.stream(s_out):
+            out[h0:h1].copy_(do[h0:h1], non_blocking=True)
+    comp.wait_stream(s_out)
+    for t in (dq, dk, dv, do, pq, pk, R):  # keep the caching allocator from recycling early
+        t.record_stream(s_in)
+        t.record_stream(s_out)
+    mask = BlockMask(words=bits, kv_idx=kv_idx, kv_cnt=kv_cnt, M_total=Mt, nonempty=True)
+    comp.synchronize()  # a host result is complete on return, like the reference's arrays
+    return (out.numpy() if numpy_in else out), mask

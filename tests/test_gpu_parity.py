@@ -276,3 +276,31 @@ def test_select_general_rows_vs_oracle():
         for k, p in ((0.05, 0.0), (0.2, 0.3), (0.5, 0.7), (1.0, 0.1)):
             got = tcb.importance_mask(R, tcb.SelectionParams(k=k, p=p), n_cols)
             assert np.array_equal(got, oracle.select_topk(R, k, p, n_cols)), (n_cols, k, p)
+
+
+# ----------------------------------------------------------------- host-streamed layer
+@pytest.mark.parametrize("hpc", [1, 2, None])
+def test_carve_layer_host_pipeline_bitwise(hpc):
+    # head-chunked H2D / mask+carve / D2H pipeline == the device two-call path, bitwise
+    dims = tcb.GridDims(4, 16, 32)  # 2048 cells -> 16 vision blocks + 1 cond block
+    lay = tcb.build_layout(dims, 128, 100)
+    st = tcb.StaticMasks.build(lay, dims, tcb.build_curve(dims))
+    params = tcb.SelectionParams(k=0.25, p=0.0)
+    g = torch.Generator().manual_seed(5)
+    hq, hk, hv = (torch.randn((5, lay.padded_total, 128), generator=g).to(torch.bfloat16).pin_memory()
+                  for _ in range(3))
+    ref_mask, _ = tcb.build_block_mask(hq.cuda(), hk.cuda(), lay, st, params)
+    ref = tcb.carve_attention(tcb.AttentionInputs(q=hq.cuda(), k=hk.cuda(), v=hv.cuda(), layout=lay),
+                              ref_mask, tcb.AmplifierBias(0.3))
+    out, mask = tcb.carve_layer(hq, hk, hv, lay, st, params, tcb.AmplifierBias(0.3),
+                                heads_per_chunk=hpc)
+    assert not out.is_cuda
+    assert torch.equal(out, ref.cpu())
+    assert torch.equal(mask.words, ref_mask.words) and torch.equal(mask.kv_cnt, ref_mask.kv_cnt)
+    # numpy fp32 inputs run the fp32 path and come back as numpy
+    q32, k32, v32 = (t.float().numpy() for t in (hq, hk, hv))
+    o32, m32 = tcb.carve_layer(q32, k32, v32, lay, st, params, heads_per_chunk=2)
+    L = oracle.layout_scalars(dims.as_tuple(), 128, 100)
+    ref32 = oracle.carve(q32, k32, v32, m32.bits.cpu().numpy(), L, 0.0, workers=8)
+    assert isinstance(o32, np.ndarray)
+    np.testing.assert_allclose(o32, ref32, rtol=1e-5, atol=1e-5)
