@@ -602,368 +602,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
 
 }  // namespace tc
 
-// =====================================================================================
-// tcgen05 kernel, Q resident in TMEM ("tq")
-// =====================================================================================
-// Same work decomposition, warp roles and half-steps as k_carve_tc, but the 128 x D
-// query tile lives in TMEM and S = Q K^T runs in TS form (A from TMEM), so the tensor
-// core reads only K and V from shared memory (the SS form re-read the 32 KB Q tile for
-// every 64-key half-step; at two CTAs per SM that Q traffic was ~1/3 of the shared-memory
-// port).  The freed 32 KB per CTA deepen the K/V rings (4 + 3 half-tiles in flight).
-// TMEM per CTA (256 columns, two CTAs per SM): Q [0,64) packed bf16x2, S [64,128) fp32
-// (P written as bf16 over its first 32 columns), O [128, 128+D).  S is single-buffered,
-// so within a CTA the chain is S(t) -> softmax(t) -> PV(t), S(t+1) (issued back to back;
-// the tensor pipe runs them in order, so S(t+1) overwrites P(t) only after PV(t) read
-// it); the other CTA's MMAs fill the tensor pipe while this CTA's softmax runs.
-namespace tq {
-
-using tc::BM;
-using tc::BK;
-using tc::HN;
-using tc::NUM_THREADS;
-using tc::RESCALE_THRESHOLD;
-constexpr int TMEM_COLS = 256;
-constexpr int Q_COL = 0;
-constexpr int S_COL = 64;
-constexpr int O_COL = 128;
-constexpr int K_SLOTS = 4;
-constexpr int V_SLOTS = 3;
-
-template <int D>
-struct Smem {
-  static constexpr int HALF_BYTES = HN * D * 2;  // 64 x D bf16
-  static constexpr int CHUNKS = D / 64;
-  static constexpr int H_CHUNK = HN * 128;
-  static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = OFF_K + K_SLOTS * HALF_BYTES;
-  static constexpr int OFF_BAR = OFF_V + V_SLOTS * HALF_BYTES;
-  static constexpr int BYTES = OFF_BAR + 256;
-};
-
-struct Bars {
-  uint64_t q_full, o_full, p_full, s_full;
-  uint64_t k_full[K_SLOTS], k_empty[K_SLOTS];
-  uint64_t v_full[V_SLOTS], v_empty[V_SLOTS];
-  uint64_t sched_full[2], sched_empty[2];
-  int sched_item[2];
-  uint32_t tmem_base;
-};
-static_assert(sizeof(Bars) <= 256, "barrier block must fit the reserved smem");
-
-template <int D, int EMU>
-__global__ void __launch_bounds__(NUM_THREADS, 2)
-    k_carve_tq(const __nv_bfloat16* __restrict__ q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
-               CarveShape s, const int32_t* __restrict__ kv_idx,
-               const int32_t* __restrict__ kv_cnt, int* __restrict__ counter, int total_items,
-               float scale_log2, float beta_log2, int dbg) {
-  using L = Smem<D>;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sK = smem + L::OFF_K;
-  uint8_t* sV = smem + L::OFF_V;
-  Bars* bars = reinterpret_cast<Bars*>(smem + L::OFF_BAR);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    if (ptx::smem_u32(smem) & 1023u) __trap();  // 128B-swizzle tiles need 1 KB alignment
-    ptx::mbar_init(&bars->q_full, 128);
-    ptx::mbar_init(&bars->o_full, 1);
-    ptx::mbar_init(&bars->p_full, 128);
-    ptx::mbar_init(&bars->s_full, 1);
-    for (int i = 0; i < K_SLOTS; ++i) {
-      ptx::mbar_init(&bars->k_full[i], 1);
-      ptx::mbar_init(&bars->k_empty[i], 1);
-    }
-    for (int i = 0; i < V_SLOTS; ++i) {
-      ptx::mbar_init(&bars->v_full[i], 1);
-      ptx::mbar_init(&bars->v_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&bars->sched_full[i], 1);
-      ptx::mbar_init(&bars->sched_empty[i], 1 + 4);
-    }
-    ptx::fence_mbar_init();
-    ptx::tma_prefetch_desc(&tm_k);
-    ptx::tma_prefetch_desc(&tm_v);
-  }
-  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(&bars->tmem_base);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
-
-  if (warp == 0) {
-    // ============================ TMA producer + scheduler ============================
-    const uint64_t pol_kv = ptx::policy_evict_last();
-    uint32_t it = 0, gk = 0, gv = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      int item = 0;
-      if (lane == 0) {
-        ptx::mbar_wait(&bars->sched_empty[slot], ((it >> 1) & 1) ^ 1);
-        item = atomicAdd(counter, 1);
-        if (item >= total_items) item = -1;
-        bars->sched_item[slot] = item;
-        ptx::mbar_arrive(&bars->sched_full[slot]);
-      }
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      const int T = 2 * n;
-      auto load = [&](const CUtensorMap* tm, uint8_t* base, uint64_t* full, uint64_t* empty,
-                      int slots, uint32_t& cnt, int t) {
-        const int b = kl.block(t >> 1);
-        if (lane == 0) {
-          const int sl = cnt % slots;
-          ptx::mbar_wait(&empty[sl], ((cnt / slots) & 1) ^ 1);
-          if ((dbg & 1) && cnt >= (uint32_t)slots) {  // timing experiment: no operand traffic
-            ptx::mbar_arrive(&full[sl]);
-          } else {
-            ptx::mbar_arrive_expect_tx(&full[sl], L::HALF_BYTES);
-#pragma unroll
-            for (int c = 0; c < L::CHUNKS; ++c)
-              ptx::tma_load_3d(base + sl * L::HALF_BYTES + c * L::H_CHUNK, tm, &full[sl], c * 64,
-                               b * BK + (t & 1) * HN, h, pol_kv);
-          }
-        }
-        ++cnt;
-      };
-      // consumption order of the MMA warp: K0, V0, K1, V1, ...; K runs one ahead
-      load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, 0);
-      for (int t = 0; t < T; ++t) {
-        if (t + 1 < T) load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, t + 1);
-        load(&tm_v, sV, bars->v_full, bars->v_empty, V_SLOTS, gv, t);
-      }
-    }
-  } else if (warp == 1) {
-    // ============================ MMA issuer ============================
-    // The whole warp runs the loop (barrier waits are warp-uniform); one elected lane
-    // issues the MMAs and commits, so descriptors stay in uniform registers.
-    constexpr uint32_t IDESC_S = tc::make_idesc(BM, HN, 0);  // Q (TMEM) x K (K-major)
-    constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, 1);   // P (TMEM) x V (MN-major)
-    const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
-    uint32_t it = 0, gk = 0, gv = 0, gp = 0;
-    auto issue_s = [&]() {  // S = Q K(gk)^T
-      const int sl = gk % K_SLOTS;
-      ptx::mbar_wait(&bars->k_full[sl], (gk / K_SLOTS) & 1);
-      ptx::tc_fence_after();
-      const uint32_t kbase = aK + sl * L::HALF_BYTES;
-      if (ptx::elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t koff = (kk >> 2) * L::H_CHUNK + (kk & 3) * 32;
-          ptx::mma_ts(tmem + S_COL, tmem + Q_COL + kk * 8, tc::make_sdesc(kbase + koff, 16, 1024),
-                      IDESC_S, kk > 0 ? 1u : 0u);
-        }
-        ptx::mma_commit(&bars->k_empty[sl]);
-        ptx::mma_commit(&bars->s_full);
-      }
-      __syncwarp();
-      ++gk;
-    };
-    for (;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
-      const int item = bars->sched_item[slot];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      const int T = 2 * n;
-      ptx::mbar_wait(&bars->q_full, it & 1);  // Q in TMEM; previous item's O read out
-      ptx::tc_fence_after();
-      if (T == 0) {
-        if (ptx::elect_one()) ptx::mma_commit(&bars->o_full);
-        __syncwarp();
-        continue;
-      }
-      issue_s();
-      for (int t = 0; t < T; ++t) {
-        ptx::mbar_wait(&bars->p_full, gp & 1);
-        const int vs = gv % V_SLOTS;
-        ptx::mbar_wait(&bars->v_full[vs], (gv / V_SLOTS) & 1);
-        ptx::tc_fence_after();
-        const uint32_t vbase = aV + vs * L::HALF_BYTES;
-        if (ptx::elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < HN / 16; ++kk)
-            ptx::mma_ts(tmem + O_COL, tmem + S_COL + kk * 8,
-                        tc::make_sdesc(vbase + kk * 16 * 128, L::H_CHUNK, 1024), IDESC_O,
-                        (t > 0 || kk > 0) ? 1u : 0u);
-          ptx::mma_commit(&bars->v_empty[vs]);
-        }
-        __syncwarp();
-        ++gv;
-        ++gp;
-        if (t + 1 < T) issue_s();  // in-order behind PV(t): overwrites P(t) after it is read
-      }
-      if (ptx::elect_one()) ptx::mma_commit(&bars->o_full);
-      __syncwarp();
-    }
-  } else {
-    // ============================ Q load / softmax / epilogue ============================
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = quarter * 32 + lane;
-    const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
-    uint32_t it = 0, g = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
-      const int item = bars->sched_item[slot];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      const int T = 2 * n;
-      {  // this thread's query row -> TMEM lane `row`, columns Q_COL.. (bf16 pairs)
-        const int4* src = reinterpret_cast<const int4*>(q + (int64_t)h * s.sh +
-                                                        ((int64_t)qb * BM + row) * s.sn);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          uint32_t w[32];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int4 x = __ldg(src + c * 8 + e);
-            w[4 * e] = (uint32_t)x.x;
-            w[4 * e + 1] = (uint32_t)x.y;
-            w[4 * e + 2] = (uint32_t)x.z;
-            w[4 * e + 3] = (uint32_t)x.w;
-          }
-          ptx::tmem_st32(t_row + Q_COL + c * 32, w);
-        }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars->q_full);
-      }
-      float m_run = -INFINITY, l_run = 0.f;
-      int b = 0, kvalid = BK;
-      float bias = 0.f;
-      for (int t = 0; t < T; ++t, ++g) {
-        if ((t & 1) == 0) {
-          b = kl.block(t >> 1);
-          kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond);
-          bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
-        }
-        const int hvalid = kvalid - (t & 1) * HN;
-        ptx::mbar_wait(&bars->s_full, g & 1);
-        ptx::tc_fence_after();
-        if (dbg & 2) {  // timing experiment: no softmax work
-          l_run = 1.f;
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&bars->p_full);
-          continue;
-        }
-        uint32_t sr[64];
-        ptx::tmem_ld32(t_row + S_COL, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-        ptx::tmem_ld32(t_row + S_COL + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-        ptx::tmem_wait_ld();
-        if (hvalid < HN) {  // padding keys of a partial block -> -inf (attention.py:193)
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (e >= hvalid) sr[e] = __float_as_uint(-INFINITY);
-        }
-        float mx8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
-#pragma unroll
-        for (int e = 8; e < 64; e += 16)
-#pragma unroll
-          for (int qq = 0; qq < 8; ++qq)
-            mx8[qq] = tc::fmax3(mx8[qq], __uint_as_float(sr[e + qq]), __uint_as_float(sr[e + 8 + qq]));
-        const float mraw = tc::fmax3(tc::fmax3(mx8[0], mx8[1], mx8[2]), tc::fmax3(mx8[3], mx8[4], mx8[5]),
-                                     fmaxf(mx8[6], mx8[7]));
-        const float m_blk = (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
-        const float m_new = fmaxf(m_run, m_blk);
-        const bool first = (t == 0);
-        const bool need = !first && (m_new > m_run + RESCALE_THRESHOLD);
-        const float m_use = (first || need) ? m_new : m_run;
-        const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
-        const float c0 = bias - m_use;
-        const uint64_t sc2 = tc::f2_pack(scale_log2, scale_log2), c02 = tc::f2_pack(c0, c0);
-        uint64_t acc2[4] = {0, 0, 0, 0};
-        uint32_t pk[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const uint64_t x = tc::ffma2(tc::f2_pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])),
-                                       sc2, c02);
-          float p0, p1;
-          if ((e & 7) >= 8 - EMU) {
-            const uint64_t pp = tc::exp2_poly2(x);
-            p0 = tc::f2_lo(pp);
-            p1 = tc::f2_hi(pp);
-          } else {
-            p0 = ptx::ex2(tc::f2_lo(x));
-            p1 = ptx::ex2(tc::f2_hi(x));
-          }
-          acc2[e & 3] = tc::fadd2(acc2[e & 3], tc::f2_pack(p0, p1));
-          pk[e] = ptx::pack_bf16(p0, p1);
-        }
-        ptx::tmem_st32(t_row + S_COL, pk);
-        const uint64_t sum2 = tc::fadd2(tc::fadd2(acc2[0], acc2[1]), tc::fadd2(acc2[2], acc2[3]));
-        l_run = l_run * alpha + (tc::f2_lo(sum2) + tc::f2_hi(sum2));
-        m_run = m_use;
-        if (__any_sync(0xffffffffu, need)) {
-          // O holds PV(t-1): the s_full commit of S(t) covered every earlier MMA
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            ptx::tmem_ld32(t_row + O_COL + c * 32, ov);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            ptx::tmem_st32(t_row + O_COL + c * 32, ov);
-          }
-        }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars->p_full);
-      }
-      // ---- epilogue: O / l -> bf16 row, padding rows zero (attention.py:203-206)
-      ptx::mbar_wait(&bars->o_full, it & 1);
-      ptx::tc_fence_after();
-      const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
-      const float inv_l = (row < qvalid) ? 1.f / l_run : 0.f;
-      __nv_bfloat16* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t ov[32];
-        ptx::tmem_ld32(t_row + O_COL + c * 32, ov);
-        ptx::tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pk[e] = ptx::pack_bf16(__uint_as_float(ov[2 * e]) * inv_l,
-                                 __uint_as_float(ov[2 * e + 1]) * inv_l);
-        int4* dst = reinterpret_cast<int4*>(orow + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          dst[e] = make_int4((int)pk[4 * e], (int)pk[4 * e + 1], (int)pk[4 * e + 2],
-                             (int)pk[4 * e + 3]);
-      }
-      ptx::tc_fence_before();
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<TMEM_COLS>(tmem);
-  }
-}
-
-}  // namespace tq
 
 
 // ---------------------------------------------------------------- host helpers
@@ -1090,39 +728,6 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
 }
 
 
-template <int D, int EMU>
-static int launch_tq(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                     const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
-                     cudaStream_t st) {
-  CUtensorMap tk, tv;
-  const int64_t n_pad = (int64_t)s.M_total * s.m;
-  int rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::HN))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::HN))) return rc;
-  const int smem = tq::Smem<D>::BYTES;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tq::k_carve_tq<D, EMU>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
-    attr_set = true;
-  }
-  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
-  if (e != cudaSuccess) return set_error(TCB_ECUDA, "memset counter: %s", cudaGetErrorString(e));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int total = s.H * s.M_total;
-  int grid = 2 * sms;
-  if (grid > total) grid = total;
-  const float LOG2E = 1.4426950408889634f;
-  const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  tq::k_carve_tq<D, EMU><<<grid, tc::NUM_THREADS, smem, st>>>(
-      (const __nv_bfloat16*)q, tk, tv, (__nv_bfloat16*)o, s, kv_idx, kv_cnt, work, total,
-      scale_log2, beta * LOG2E, dbg_flags());
-  return check_launch("k_carve_tq");
-}
-
 extern "C" int tcb_carve_fwd_simt(const void* q, const void* k, const void* v, void* o, int dtype,
                                   int64_t stride_h, int64_t stride_n, const int32_t* kv_idx,
                                   const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
@@ -1155,22 +760,6 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
     if (emu != 0 && emu != 2 && emu != 3 && emu != 4) emu = 0;
   }
   cudaStream_t st = as_stream(stream);
-  // TCB_CARVE_IMPL=1 selects the Q-in-TMEM kernel (k_carve_tq)
-  static int impl = -1;
-  if (impl < 0) {
-    const char* env = getenv("TCB_CARVE_IMPL");
-    impl = env ? atoi(env) : 0;
-  }
-  if (impl == 1) {
-    if (d == 128) {
-      switch (emu) {
-        case 2: return launch_tq<128, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-        case 3: return launch_tq<128, 3>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-        default: return launch_tq<128, 0>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-      }
-    }
-    return launch_tq<64, 0>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-  }
   if (d == 128) {
     switch (emu) {
       case 3: return launch_tc<128, 3>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
