@@ -6,7 +6,9 @@
   * C4: ProRes 2-stage switch at 720p: fused predict_clean+upsample+renoise
     (33,34,60,16) -> (33,45,80,16), curve + adjacency rebuild at the new dims, and
     one toy-width permute of the latent;
-  * C5: sparsity sweep on C2, k in {0.01, 0.02, 0.05, 0.08, 0.10, 0.20, 0.30}, p=0.
+  * C5: sparsity sweep on C2, k in {0.01, 0.02, 0.05, 0.08, 0.10, 0.20, 0.30}, p=0;
+  * §8f-1 fused neighbours at C2: QKV -> curve-order head-major with 3D RoPE (vs the
+    unfused torch composition), unpermute+Euler, curve positions.
 
 All timings: CUDA events on the launching stream, median of repeats after warm-up.
 Writes one JSON document (stdout, and --out if given).
@@ -192,12 +194,68 @@ def c4_records():
     return recs
 
 
+def fused_records():
+    """§8f-1 fused neighbours at C2: QKV raster -> curve head-major with 3D RoPE (one pass)
+    vs the unfused torch composition (gather, rotate, transpose), plus the per-step
+    latent kernels."""
+    from paper_2505_16864_b200 import fused
+
+    hbm, _ = peaks()
+    dims = tcb.GridDims(33, 45, 80)
+    perm = tcb.build_curve(dims)
+    lay = tcb.build_layout(dims, 128, 256)
+    n, H, d = dims.n_cells, 24, 128
+    qkv = torch.randn((n, 3, H, d), device="cuda").to(torch.bfloat16)
+    outs = [torch.zeros((H, lay.padded_total, d), dtype=torch.bfloat16, device="cuda") for _ in range(3)]
+    srcs = [qkv[:, 0], qkv[:, 1], qkv[:, 2]]
+    fused.rope_tables(dims)
+    t = timed(lambda: fused.rope_permute(srcs, perm, outs, [True, True, False]), reps=20)
+    byts = 2 * 3 * n * H * d * 2 + 4 * n
+    recs = [{"kernel": "rope_permute Q/K/V (3D RoPE on Q,K; raster token-major -> curve head-major)",
+             "shape": "118800 x 3 x 24 x 128 bf16", "ms": round(t, 4),
+             "gbs": round(byts / (t * 1e-3) / 1e9, 1), "frac_of_hbm": round(byts / (t * 1e-3) / 1e9 / hbm, 3)}]
+    # unfused torch composition of the same result (for the traffic comparison)
+    tab = fused.rope_tables(dims).view(-1, 2)
+    pos = fused.curve_positions(perm)
+    sec = (16, 56, 56)
+    offs = [0, dims.t * 8, dims.t * 8 + dims.h * 28]
+    cs = torch.cat([tab[offs[a] + pos[:, a:a + 1] * (sec[a] // 2) +
+                        torch.arange(sec[a] // 2, device="cuda")] for a in range(3)], dim=1)  # (n, 64, 2)
+    fidx = perm.forward.long()
+
+    def unfused():
+        res = []
+        for j in range(3):
+            x = qkv[:, j][fidx].float()  # gather
+            if j < 2:
+                x0, x1 = x[..., 0::2], x[..., 1::2]
+                c, s_ = cs[:, None, :, 0], cs[:, None, :, 1]
+                x = torch.stack([x0 * c - x1 * s_, x0 * s_ + x1 * c], dim=-1).flatten(-2)
+            outs[j][:, :n] = x.to(torch.bfloat16).permute(1, 0, 2)
+        return res
+
+    t2 = timed(unfused, reps=5)
+    recs.append({"kernel": "same result, unfused torch (gather, rotate, cast, transpose)", "ms": round(t2, 4),
+                 "speedup_of_fused": round(t2 / t, 2)})
+    C = 16
+    lat = torch.randn((33, 45, 80, C), device="cuda")
+    vel = torch.randn((n, C), device="cuda")
+    t = timed(lambda: fused.unpermute_euler(lat, vel, perm, 0.7, 0.6), reps=20)
+    byts = 3 * lat.numel() * 4 + 4 * n
+    recs.append({"kernel": "unpermute_euler (invert_permutation + Euler, one pass)", "shape": "(33,45,80,16) f32",
+                 "ms": round(t, 4), "gbs": round(byts / (t * 1e-3) / 1e9, 1)})
+    t = timed(lambda: fused.curve_positions(perm), reps=20)
+    recs.append({"kernel": "curve_positions", "shape": "118800 x 3 int64", "ms": round(t, 4)})
+    return recs
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--skip-sweep", action="store_true")
     a = ap.parse_args()
-    res = {"device": torch.cuda.get_device_name(0), "hbm": hbm_records(), "c4_stage_switch": c4_records()}
+    res = {"device": torch.cuda.get_device_name(0), "hbm": hbm_records(), "c4_stage_switch": c4_records(),
+           "fused_f1": fused_records()}
     res["c3"] = layer_record("C3 Wan2.1-14B 480p 21x30x52, H=40, no text", (21, 30, 52), 0, 40, 0.08)
     res["c2"] = layer_record("C2 HunyuanVideo 720p 33x45x80 + 256 text, H=24", (33, 45, 80), 256, 24, 0.08)
     if not a.skip_sweep:

@@ -136,6 +136,43 @@ int tcb_upsample_renoise(const float* x, const float* vel, const float* eps, flo
 int tcb_euler_step(const float* x, const float* v, float* out, int64_t n, float dsigma,
                    void* stream);
 
+/* ---- fused neighbours of the path ---- */
+
+/* K9 variant reading a curve-order velocity through inv: vel(cell) = vel_curve[inv[cell]].
+ * Fuses invert_permutation (pipeline.py:363) into the stage switch. */
+int tcb_upsample_renoise_curve(const float* x, const float* vel_curve, const int32_t* inv,
+                               const float* eps, float* out, int st, int sh, int sw, int dt,
+                               int dh, int dw, int C, double sigma, int mode, uint64_t seed,
+                               uint64_t offset, void* stream);
+
+/* positions = apply_permutation(unravel_index(arange(n), (t,h,w)), perm)
+ * (pipeline.py:334-337) straight from fwd: pos (n, 3) int64. */
+int tcb_curve_positions(const int32_t* fwd, int64_t n, int t, int h, int w, int64_t* pos,
+                        void* stream);
+
+/* Patchify + permute: latent (t*pt, h*ph, w*pw, C) float32 -> tokens (n, pt*ph*pw*C) in
+ * curve order, tokens[i] = patch(fwd[i]).  With pt=ph=pw=1 this is
+ * apply_permutation(x.reshape(n, C), perm) (pipeline.py:345). */
+int tcb_patchify_permute(const float* x, const int32_t* fwd, int t, int h, int w, int pt, int ph,
+                         int pw, int C, float* tokens, void* stream);
+
+/* Unpatchify + invert_permutation + Euler (pipeline.py:363-371) in one pass:
+ * out = x + dsigma * unpatchify(vel_curve[inv]). */
+int tcb_unpermute_euler(const float* x, const float* vel_curve, const int32_t* inv, int t, int h,
+                        int w, int pt, int ph, int pw, int C, float dsigma, float* out,
+                        void* stream);
+
+/* Raster-order token-major bf16 (n, H, d) tensors (element strides src_sn, src_sh; d
+ * contiguous) -> curve-order head-major (dst_sh, dst_sn): dst[hh, i] = f(src[fwd[i], hh]),
+ * f = 3D rotary embedding where rotate[k] != 0 (Q, K), plain copy otherwise (V).
+ * cos_sin: float (cos, sin) pairs, [t x d_t/2][h x d_h/2][w x d_w/2]; head-dim sections
+ * [0,d_t) t, [d_t,d_t+d_h) h, rest w; pair j rotates elements (2j, 2j+1).  Rows >= n of
+ * dst are not touched (padding / condition tokens belong to the caller). */
+int tcb_rope_permute(const void* const* src, int64_t src_sn, int64_t src_sh, void* const* dst,
+                     int64_t dst_sh, int64_t dst_sn, const int* rotate, int n_tensors,
+                     const int32_t* fwd, int t, int h, int w, int H, int d,
+                     const float* cos_sin, int d_t, int d_h, int d_w, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -39,6 +39,11 @@ __all__ = [
     "upsample_area",
     "transition",
     "beta_of",
+    "curve_positions",
+    "patchify",
+    "unpatchify",
+    "rope_table",
+    "rope_apply",
 ]
 
 
@@ -388,3 +393,64 @@ def transition(x0: np.ndarray, sigma: float, target, noise: np.ndarray) -> np.nd
     up = upsample_area(x0, target).astype(np.float32)
     s = np.float32(sigma)
     return (np.float32(1.0) - s) * up + s * noise
+
+
+# --------------------------------------------------------------------------
+# §8f-1: neighbours of the path (positions, patchify, RoPE)
+# --------------------------------------------------------------------------
+
+def curve_positions(dims) -> np.ndarray:
+    """apply_permutation(unravel_index(arange(n), dims), perm) (pipeline.py:334-337)."""
+    t, h, w = (int(v) for v in dims)
+    coords = np.stack(np.unravel_index(np.arange(t * h * w), (t, h, w)), axis=1).astype(np.int64)
+    return coords[curve_forward(dims)]
+
+
+def patchify(x: np.ndarray, dims, patch) -> np.ndarray:
+    """(t*pt, h*ph, w*pw, C) -> (n, pt*ph*pw*C) tokens in row-major cell order, features
+    ordered (pt, ph, pw, C).  Patch (1,1,1) is x.reshape(n, C) (pipeline.py:345)."""
+    t, h, w = (int(v) for v in dims)
+    pt, ph, pw = (int(v) for v in patch)
+    C = x.shape[-1]
+    y = x.reshape(t, pt, h, ph, w, pw, C).transpose(0, 2, 4, 1, 3, 5, 6)
+    return np.ascontiguousarray(y.reshape(t * h * w, pt * ph * pw * C))
+
+
+def unpatchify(tok: np.ndarray, dims, patch, C: int) -> np.ndarray:
+    """Inverse of ``patchify``."""
+    t, h, w = (int(v) for v in dims)
+    pt, ph, pw = (int(v) for v in patch)
+    y = tok.reshape(t, h, w, pt, ph, pw, C).transpose(0, 3, 1, 4, 2, 5, 6)
+    return np.ascontiguousarray(y.reshape(t * pt, h * ph, w * pw, C))
+
+
+def rope_table(dims, sections, theta: float) -> list:
+    """Per axis (cos, sin) float32 tables (n_pos, d_a/2): angle pos * theta^(-2j/d_a) in
+    float64.  Not in the reference (it has no positional embedding in attention); this is
+    the 3D RoPE convention the fused kernel implements (HunyuanVideo sections 16/56/56)."""
+    out = []
+    for n_pos, da in zip((int(v) for v in dims), sections):
+        inv = theta ** (-(np.arange(0, da, 2, dtype=np.float64)) / da)
+        ang = np.arange(n_pos, dtype=np.float64)[:, None] * inv[None, :]
+        out.append((np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)))
+    return out
+
+
+def rope_apply(x: np.ndarray, pos: np.ndarray, sections, theta: float, dims) -> np.ndarray:
+    """x (n, H, d) float32, pos (n, 3) -> rotated float32; pair (2j, 2j+1) of section a:
+    (x0*c - x1*s, x0*s + x1*c), every product and sum rounded to float32."""
+    tabs = rope_table(dims, sections, theta)
+    out = x.copy()
+    off = 0
+    for a, da in enumerate(sections):
+        if da == 0:
+            continue
+        c, s = tabs[a]
+        cc = c[pos[:, a]][:, None, :]  # (n, 1, da/2)
+        ss = s[pos[:, a]][:, None, :]
+        x0 = x[:, :, off: off + da: 2]
+        x1 = x[:, :, off + 1: off + da: 2]
+        out[:, :, off: off + da: 2] = (x0 * cc).astype(np.float32) - (x1 * ss).astype(np.float32)
+        out[:, :, off + 1: off + da: 2] = (x0 * ss).astype(np.float32) + (x1 * cc).astype(np.float32)
+        off += da
+    return out

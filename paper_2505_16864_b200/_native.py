@@ -44,6 +44,13 @@ SIGNATURES = {
                            _I64, _F, _P],
     "tcb_upsample_renoise": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _I, _U64, _U64, _P],
     "tcb_euler_step": [_P, _P, _P, _I64, _F, _P],
+    "tcb_upsample_renoise_curve": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _I, _U64,
+                                   _U64, _P],
+    "tcb_curve_positions": [_P, _I64, _I, _I, _I, _P, _P],
+    "tcb_patchify_permute": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P],
+    "tcb_unpermute_euler": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P],
+    "tcb_rope_permute": [_P, _I64, _I64, _P, _I64, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _P, _I,
+                         _I, _I, _P],
 }
 
 

@@ -66,9 +66,9 @@ __device__ __forceinline__ float philox_normal(uint64_t seed, uint64_t idx) {
 }
 
 __global__ void __launch_bounds__(256) k_upsample_renoise(
-    const float* __restrict__ x, const float* __restrict__ vel, const float* __restrict__ eps,
-    float* __restrict__ out, int st, int sh, int sw, int dt, int dh, int dw, int C, float sigma_f,
-    int mode, uint64_t seed, uint64_t offset) {
+    const float* __restrict__ x, const float* __restrict__ vel, const int32_t* __restrict__ inv,
+    const float* __restrict__ eps, float* __restrict__ out, int st, int sh, int sw, int dt, int dh,
+    int dw, int C, float sigma_f, int mode, uint64_t seed, uint64_t offset) {
   const int64_t n = (int64_t)dt * dh * dw * C;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
@@ -86,9 +86,13 @@ __global__ void __launch_bounds__(256) k_upsample_renoise(
     for (int a = 0; a < th.n; ++a) {
       double acc_t = 0.0;
       for (int z = 0; z < tt.n; ++z) {
-        const int64_t src = (((int64_t)(tt.i0 + z) * sh + (th.i0 + a)) * sw + (tw.i0 + b)) * C + c;
+        const int64_t cell = ((int64_t)(tt.i0 + z) * sh + (th.i0 + a)) * sw + (tw.i0 + b);
+        const int64_t src = cell * C + c;
         float x0 = x[src];
-        if (vel) x0 = __fsub_rn(x0, __fmul_rn(sigma_f, vel[src]));  // predict_clean in fp32
+        if (vel) {  // predict_clean in fp32; a curve-order velocity is read through inv
+          const float v = vel[(inv ? (int64_t)inv[cell] : cell) * C + c];
+          x0 = __fsub_rn(x0, __fmul_rn(sigma_f, v));
+        }
         acc_t += (z == 0 ? tt.w0 : tt.w1) * (double)x0;
       }
       acc_h += (a == 0 ? th.w0 : th.w1) * acc_t;
@@ -127,7 +131,24 @@ extern "C" int tcb_upsample_renoise(const float* x, const float* vel, const floa
   TCB_CHECK_ARG(sigma >= 0.0 && sigma <= 1.0, TCB_EDOMAIN, "sigma %g outside [0, 1]", sigma);
   const int64_t n = (int64_t)dt * dh * dw * C;
   k_upsample_renoise<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(
-      x, vel, eps, out, st, sh, sw, dt, dh, dw, C, (float)sigma, mode, seed, offset);
+      x, vel, nullptr, eps, out, st, sh, sw, dt, dh, dw, C, (float)sigma, mode, seed, offset);
+  return check_launch("k_upsample_renoise");
+}
+
+extern "C" int tcb_upsample_renoise_curve(const float* x, const float* vel_curve,
+                                          const int32_t* inv, const float* eps, float* out, int st,
+                                          int sh, int sw, int dt, int dh, int dw, int C,
+                                          double sigma, int mode, uint64_t seed, uint64_t offset,
+                                          void* stream) {
+  TCB_CHECK_ARG(x && out && vel_curve && inv, TCB_ESHAPE, "null tensor");
+  TCB_CHECK_ARG(st >= 1 && sh >= 1 && sw >= 1 && C >= 1, TCB_ESHAPE, "bad source dims");
+  TCB_CHECK_ARG(dt >= st && dh >= sh && dw >= sw, TCB_EDOMAIN, "target shrinks source");
+  TCB_CHECK_ARG(mode >= 0 && mode <= 2, TCB_EDOMAIN, "bad mode %d", mode);
+  TCB_CHECK_ARG(mode != 1 || eps, TCB_ESHAPE, "mode 1 needs eps");
+  TCB_CHECK_ARG(sigma >= 0.0 && sigma <= 1.0, TCB_EDOMAIN, "sigma %g outside [0, 1]", sigma);
+  const int64_t n = (int64_t)dt * dh * dw * C;
+  k_upsample_renoise<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(
+      x, vel_curve, inv, eps, out, st, sh, sw, dt, dh, dw, C, (float)sigma, mode, seed, offset);
   return check_launch("k_upsample_renoise");
 }
 

@@ -294,6 +294,8 @@ def run_pipeline(plan: StagePlan, denoiser: Denoiser, rng=0, channels: int = 1) 
     so runs are comparable bitwise in their noise) -- tokens, velocities and the
     latent stay on the device; the terminal latent is returned as numpy.
     """
+    from .fused import curve_positions, switch_stage_curve, unpermute_euler
+
     if not isinstance(rng, np.random.Generator):
         rng = np.random.default_rng(rng)
     t0 = time.perf_counter()
@@ -307,10 +309,7 @@ def run_pipeline(plan: StagePlan, denoiser: Denoiser, rng=0, channels: int = 1) 
         perm = build_curve(dims)
         layout = build_layout(dims, plan.block_size, plan.n_cond_tokens)
         statics = StaticMasks.build(layout, dims, perm)
-        t_, h_, w_ = dims.as_tuple()
-        cells = torch.arange(n, device=x.device, dtype=torch.int64)
-        coords = torch.stack([cells // (h_ * w_), (cells // w_) % h_, cells % w_], dim=1)
-        positions = gather_rows(coords, perm.forward)
+        positions = curve_positions(perm)  # one pass from fwd (pipeline.py:334-337)
         beta = AmplifierBias(compute_beta(n, target_numel, stage.rho))
         params = SelectionParams(k=stage.k, p=plan.p)
         schedule = shifted_sigmas(stage.step_indices, plan.base_T, stage.alpha)
@@ -324,13 +323,13 @@ def run_pipeline(plan: StagePlan, denoiser: Denoiser, rng=0, channels: int = 1) 
             vel_curve = _dev.as_cuda(denoiser(z, ctx))
             if tuple(vel_curve.shape) != tuple(z.shape):
                 raise ShapeError(f"denoiser returned shape {tuple(vel_curve.shape)}, expected {tuple(z.shape)}")
-            vel = gather_rows(vel_curve.contiguous(), perm.inverse).reshape(x.shape)
             step_records.append({"stage": s_idx, "step_index": int(idx), "sigma": sigma,
                                  **ctx.metrics})
+            # invert_permutation fused into the update / switch (pipeline.py:363-371)
             if s_idx < len(plan.stages) - 1 and j == last:
-                x = switch_stage(x, vel, sigma, plan.stages[s_idx + 1].dims, rng)
+                x = switch_stage_curve(x, vel_curve, perm, sigma, plan.stages[s_idx + 1].dims, rng)
             else:
-                x = denoise_step(x, vel, sigma, float(schedule.sigmas[j + 1]))
+                x = unpermute_euler(x, vel_curve, perm, sigma, float(schedule.sigmas[j + 1]))
         stage_reports.append({"stage": s_idx, "dims": list(dims.as_tuple()), "n_tokens": n,
                               "token_ratio_to_target": n / target_numel,
                               "n_steps": len(stage.step_indices), "alpha": stage.alpha,
