@@ -209,6 +209,30 @@ def pipeline_run():
          betas=np.array([s["beta"] for s in res.report["stages"]]))
 
 
+def positions():
+    """Curve-order positional metadata exactly as run_pipeline builds it
+    (pipeline.py:333-337), captured from inside the reference loop for two stages, plus
+    the same construction at the C2 grid (fingerprint)."""
+    seen = {}
+    base = tpl.toy_transformer_denoiser(channels=1, n_heads=1, d_k=8, seed=3)
+
+    def spy(z, ctx):
+        seen.setdefault(ctx.dims.as_tuple(), np.array(ctx.positions))
+        return base(z, ctx)
+
+    plan = tpl.StagePlan(
+        stages=(tpl.StageConfig(dims=tc.GridDims(2, 4, 6), step_indices=(0, 5), alpha=3.0, k=0.3),
+                tpl.StageConfig(dims=tc.GridDims(3, 5, 7), step_indices=(5, 8), alpha=3.0, k=0.3)),
+        base_T=10, block_size=8, n_cond_tokens=0, p=0.3)
+    tpl.run_pipeline(plan, spy, rng=0, channels=1)
+    dims = (33, 45, 80)
+    n = dims[0] * dims[1] * dims[2]
+    coords = np.stack(np.unravel_index(np.arange(n), dims), axis=1).astype(np.int64)
+    big = tc.apply_permutation(coords, tc.build_curve(tc.GridDims(*dims)))
+    save("positions.npz", s0=seen[(2, 4, 6)], s1=seen[(3, 5, 7)], c2_sha=np.array(sha16(big.astype("<i8"))),
+         c2_head=big[:64])
+
+
 if __name__ == "__main__":
     curves()
     layouts_and_adjacency()
@@ -216,3 +240,4 @@ if __name__ == "__main__":
     attention()
     stage_switch()
     pipeline_run()
+    positions()

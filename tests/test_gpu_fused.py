@@ -104,3 +104,14 @@ def test_rope_permute_identity_and_norm():
     assert torch.allclose(n0, n1, rtol=2e-2)  # rotations preserve the norm (bf16 rounding)
     with pytest.raises(tcb.DomainError):
         fused.rope_permute([x], perm, [out], [True], (0, 30, 30))
+
+
+def test_curve_positions_match_reference_loop_fixture():
+    import golden_io as gio
+
+    g = gio.load("positions.npz")
+    for dims, key in (((2, 4, 6), "s0"), ((3, 5, 7), "s1")):
+        pos = fused.curve_positions(tcb.build_curve(tcb.GridDims(*dims))).cpu().numpy()
+        assert np.array_equal(pos, g[key])
+    big = fused.curve_positions(tcb.build_curve(tcb.GridDims(33, 45, 80))).cpu().numpy()
+    assert np.array_equal(big[:64], g["c2_head"])

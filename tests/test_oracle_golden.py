@@ -131,3 +131,32 @@ def test_stage_switch():
         noise = np.random.default_rng(99).standard_normal((*dst, C), dtype=np.float32)
         np.testing.assert_allclose(oracle.transition(x0, 0.899083, dst, noise), g[f"case{i}_tr"],
                                    rtol=0, atol=1e-6)
+
+
+# ----------------------------------------------------------------- §8f-1 neighbours
+def test_oracle_positions_match_reference_loop():
+    g = gio.load("positions.npz")
+    assert np.array_equal(oracle.curve_positions((2, 4, 6)), g["s0"])
+    assert np.array_equal(oracle.curve_positions((3, 5, 7)), g["s1"])
+    big = oracle.curve_positions((33, 45, 80))
+    import hashlib
+    assert hashlib.sha256(big.astype("<i8").tobytes()).hexdigest()[:16] == str(g["c2_sha"])
+
+
+def test_oracle_patchify_roundtrip_and_rope_properties():
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((4, 6, 10, 3)).astype(np.float32)
+    for patch in ((1, 1, 1), (2, 3, 5), (1, 2, 2)):
+        dims = (4 // patch[0], 6 // patch[1], 10 // patch[2])
+        tok = oracle.patchify(x, dims, patch)
+        assert np.array_equal(oracle.unpatchify(tok, dims, patch, 3), x)
+    assert np.array_equal(oracle.patchify(x, (4, 6, 10), (1, 1, 1)), x.reshape(-1, 3))
+    # position 0 -> angle 0 -> identity; rotations preserve pair norms
+    dims = (2, 3, 4)
+    q = rng.standard_normal((24, 2, 16)).astype(np.float32)
+    zero = np.zeros((24, 3), np.int64)
+    assert np.array_equal(oracle.rope_apply(q, zero, (4, 6, 6), 256.0, dims), q)
+    pos = oracle.curve_positions(dims)
+    r = oracle.rope_apply(q, pos, (4, 6, 6), 256.0, dims)
+    np.testing.assert_allclose((r[..., 0::2] ** 2 + r[..., 1::2] ** 2),
+                               (q[..., 0::2] ** 2 + q[..., 1::2] ** 2), rtol=1e-5)
