@@ -173,6 +173,15 @@ int tcb_rope_permute(const void* const* src, int64_t src_sn, int64_t src_sh, voi
                      const int32_t* fwd, int t, int h, int w, int H, int d,
                      const float* cos_sin, int d_t, int d_h, int d_w, void* stream);
 
+/* ---- mask file format (§8f-3): tensorio.py write_mask / read_mask (tensorio.py:80-100) ----
+ * words (rows, words_per_row) uint32, little-endian bit order -> packed (rows,
+ * ceil(M_total/8)) bytes in np.packbits order (column 8b = MSB of byte b). */
+int tcb_mask_words_to_packbits(const uint32_t* words, int64_t rows, int M_total,
+                               int words_per_row, uint8_t* packed, void* stream);
+/* packed bytes (np.packbits order) -> dense (rows, M_total) 0/1 bytes. */
+int tcb_packbits_to_dense(const uint8_t* packed, int64_t rows, int M_total, uint8_t* dense,
+                          void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,6 +49,8 @@ SIGNATURES = {
     "tcb_curve_positions": [_P, _I64, _I, _I, _I, _P, _P],
     "tcb_patchify_permute": [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P],
     "tcb_unpermute_euler": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _F, _P, _P],
+    "tcb_mask_words_to_packbits": [_P, _I64, _I, _I, _P, _P],
+    "tcb_packbits_to_dense": [_P, _I64, _I, _P, _P],
     "tcb_rope_permute": [_P, _I64, _I64, _P, _I64, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _P, _I,
                          _I, _I, _P],
 }

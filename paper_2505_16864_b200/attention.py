@@ -12,6 +12,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import _dev, _native
@@ -19,7 +20,8 @@ from .errors import DomainError, ShapeError
 from .masks import BlockMask
 from .partition import BlockLayout
 
-__all__ = ["AttentionInputs", "AmplifierBias", "compute_beta", "carve_attention"]
+__all__ = ["AttentionInputs", "AmplifierBias", "compute_beta", "carve_attention",
+           "dense_attention", "block_mask_logit_bias"]
 
 
 @dataclass(frozen=True)
@@ -123,3 +125,60 @@ def carve_attention(inputs: AttentionInputs, mask: BlockMask,
         q, k, v = q.float(), k.float(), v.float()
     out = carve_raw(q, k, v, mask, layout, beta.beta)
     return _dev.to_like(out, inputs.q)
+
+
+def _valid_keys(n: int, valid, device) -> torch.Tensor:
+    if valid is None:
+        return torch.ones(n, dtype=torch.bool, device=device)
+    if isinstance(valid, (int, np.integer)):
+        ok = torch.zeros(n, dtype=torch.bool, device=device)
+        ok[: int(valid)] = True
+        return ok
+    ok = _dev.as_cuda(np.asarray(valid, dtype=bool) if not isinstance(valid, torch.Tensor) else valid)
+    if tuple(ok.shape) != (n,):
+        raise ShapeError(f"valid mask shape {tuple(ok.shape)} != ({n},)")
+    return ok.to(torch.bool)
+
+
+def dense_attention(q, k, v, logit_bias=None, valid=None):
+    """Exact two-pass fp32 softmax attention (attention.py:112-142): the dense check the
+    reference CLI runs against carve output.  fp32 GEMMs (cuBLAS, TF32 off) on the device;
+    ``logit_bias`` broadcastable to (H, N, N) with -inf dropping pairs; padding keys get
+    -inf and padding query rows are zeroed.  Not a hot-path kernel."""
+    shp = [tuple(x.shape) for x in (q, k, v)]
+    if not (shp[0] == shp[1] == shp[2]) or len(shp[0]) != 3:
+        raise ShapeError(f"Q/K/V must share one (heads, N, d_k) shape, got {shp[0]}")
+    H, n, d_k = shp[0]
+    qd, kd, vd = (_dev.as_cuda(x).float() for x in (q, k, v))
+    ok = _valid_keys(n, valid, qd.device)
+    scale = np.float32(1.0 / math.sqrt(d_k))
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        scores = torch.matmul(qd * float(scale), kd.transpose(1, 2))
+        if logit_bias is not None:
+            scores = scores + _dev.as_cuda(logit_bias).float()
+        scores = torch.where(ok[None, None, :], scores, torch.tensor(float("-inf"), device=qd.device))
+        scores = scores - scores.amax(dim=-1, keepdim=True)
+        w = torch.exp(scores)
+        w = w / w.sum(dim=-1, keepdim=True)
+        out = torch.matmul(w, vd)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    out[:, ~ok, :] = 0.0
+    return _dev.to_like(out, q)
+
+
+def block_mask_logit_bias(mask: BlockMask, layout: BlockLayout, beta: float = 0.0):
+    """Token-level additive bias equivalent to a block mask + amplifier
+    (attention.py:145-159): -inf on deselected vision-row blocks, condition rows open,
+    +beta on vision-query x condition-key pairs.  Built on the device."""
+    m, n = layout.m, layout.padded_total
+    bits = mask.bits if isinstance(mask, BlockMask) else _dev.as_cuda(mask)
+    H = int(bits.shape[0])
+    bias = torch.zeros((H, layout.M_total, layout.M_total), dtype=torch.float32, device=bits.device)
+    bias[:, : layout.M_v, :] = torch.where(bits.to(torch.bool), 0.0, float("-inf"))
+    if beta:
+        bias[:, : layout.M_v, layout.M_v:] += np.float32(beta)
+    out = bias.repeat_interleave(m, dim=1).repeat_interleave(m, dim=2).reshape(H, n, n)
+    return out.cpu().numpy() if isinstance(mask, np.ndarray) else out

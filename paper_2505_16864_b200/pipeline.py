@@ -260,6 +260,37 @@ def switch_stage(x, vel, sigma_t: float, target: GridDims, rng):
     return _dev.to_like(_launch_switch(xt, vt, eps, sigma_t, dst, mode, seed), x)
 
 
+# ----------------------------------------------------------------------------- analytic denoiser
+def gaussian_posterior_mean(x_t, sigma: float, mu: float, s: float):
+    """E[x0 | x_t] for x0 ~ N(mu, s^2 I), x_t = (1-sigma) x0 + sigma eps
+    (pipeline.py:195-199); same scalar/array operation order as the reference."""
+    a = 1.0 - sigma
+    denom = a * a * s * s + sigma * sigma
+    return mu + a * s * s * (x_t - a * mu) / denom
+
+
+def gaussian_analytic_denoiser(mu: float, s: float) -> "Denoiser":
+    """Exact velocity E[eps - x0 | x_t] for Gaussian data (pipeline.py:202-221), as an
+    elementwise expression on the device tokens (float32 result like the input)."""
+    if s <= 0:
+        raise DomainError(f"data std must be positive, got {s}")
+    s2 = s * s
+
+    def velocity(tokens, ctx: "StepContext"):
+        tok = _dev.as_cuda(tokens)
+        sig = ctx.sigma
+        a = 1.0 - sig
+        denom = a * a * s2 + sig * sig
+        # numpy >= 2 keeps Python scalars weak: every op runs in float32 with the scalar
+        # rounded to float32, as torch does; the divisor is a 0-dim tensor so the division
+        # is a true per-element divide (a CPU-scalar divide would multiply by 1/denom)
+        t = tok.float()
+        num = sig * (t - mu) - a * s2 * t
+        return num / torch.tensor(denom, dtype=torch.float32, device=t.device)
+
+    return velocity
+
+
 # ----------------------------------------------------------------------------- loop
 @dataclass
 class StepContext:

@@ -233,6 +233,63 @@ def positions():
          c2_head=big[:64])
 
 
+def cli_outputs():
+    """Files and stdout of the reference CLI (cli.py) for small cases, to check the GPU
+    front end's outputs byte for byte (formats) or within tolerance (attention)."""
+    import contextlib
+    import io
+    import json
+
+    from tokencarve import cli as tcli
+    from tokencarve import tensorio as tio
+
+    d = os.path.join(HERE, "cli")
+    os.makedirs(d, exist_ok=True)
+
+    def run(argv):
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = tcli.main(argv)
+        assert rc == 0, argv
+        return buf.getvalue()
+
+    with open(os.path.join(d, "order_3_4_5.txt"), "w") as fh:
+        fh.write(run(["order", "--dims", "3,4,5"]))
+    run(["order", "--dims", "3,4,5", "--binary", "--out", os.path.join(d, "order_3_4_5.tct")])
+    run(["masks", "--dims", "4,8,8", "--block", "16", "--cond", "5", "--heads", "2", "--dk", "16",
+         "--seed", "0", "--rate", "0.3", "--cutoff", "0.3", "--out", os.path.join(d, "mask.tcm"),
+         "--stats", os.path.join(d, "mask_stats.json"), "--csv", os.path.join(d, "neighbors.csv")])
+    lay = tc.build_layout(tc.GridDims(4, 8, 8), 16, 5)
+    rng = np.random.default_rng(21)
+    for name in ("q", "k", "v"):
+        tio.write_tensor(os.path.join(d, f"{name}.tct"),
+                         rng.standard_normal((2, lay.padded_total, 16), dtype=np.float32))
+    run(["attend", "--q", os.path.join(d, "q.tct"), "--k", os.path.join(d, "k.tct"), "--v",
+         os.path.join(d, "v.tct"), "--dims", "4,8,8", "--block", "16", "--cond", "5", "--mask",
+         os.path.join(d, "mask.tcm"), "--beta", "0.3", "--out", os.path.join(d, "attend_out.tct"),
+         "--report", os.path.join(d, "attend_report.json")])
+    with open(os.path.join(d, "plan_33_45_80.json"), "w") as fh:
+        fh.write(run(["plan", "--target", "33,45,80", "--cond", "256", "--seed", "3"]))
+    with open(os.path.join(d, "plan_3stage.json"), "w") as fh:
+        fh.write(run(["plan", "--target", "16,40,64", "--stages", "3", "--base-steps", "30",
+                      "--keep", "12", "--rates", "0.3,0.25,0.2", "--denoiser", "toy-transformer"]))
+    rows = [run(["analyze", "--dims", "33,45,80", "--strategy", "sfc"]),
+            run(["analyze", "--dims", "33,45,80", "--strategy", "tiled", "--tile", "4,8,8"]),
+            run(["analyze", "--dims", "21,30,52", "--strategy", "tiled", "--tile", "3,6,6",
+                 "--block", "64"])]
+    with open(os.path.join(d, "analyze_rows.txt"), "w") as fh:
+        fh.write("".join(rows))
+    plan = {"stages": [{"dims": [2, 4, 6], "steps": [0, 3, 6], "alpha": 3.0, "k": 0.3, "rho": 0.5},
+                       {"dims": [2, 6, 8], "steps": [6, 8, 9], "alpha": 5.0, "k": 0.2}],
+            "base_steps": 10, "block_size": 8, "cond_tokens": 0, "p": 0.3, "seed": 4,
+            "denoiser": "gaussian", "denoiser_params": {"mu": 3.0, "s": 2.0}, "channels": 2}
+    with open(os.path.join(d, "pipeline_plan.json"), "w") as fh:
+        json.dump(plan, fh)
+    run(["pipeline", "--plan", os.path.join(d, "pipeline_plan.json"), "--out",
+         os.path.join(d, "pipeline_latent.tct"), "--report", os.path.join(d, "pipeline_report.json")])
+    print("wrote cli/")
+
+
 if __name__ == "__main__":
     curves()
     layouts_and_adjacency()
@@ -241,3 +298,4 @@ if __name__ == "__main__":
     stage_switch()
     pipeline_run()
     positions()
+    cli_outputs()
