@@ -329,6 +329,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     // list is read 32 entries at a time (one coalesced load per lane) and broadcast by
     // shuffle, so the block index is never a dependent global load on the issue path.
     const uint64_t pol_kv = ptx::policy_evict_last();
+    // Q is read once; condition rows sweep a whole head's K/V once (both condition rows of
+    // a head run concurrently), so neither should displace the vision rows' K/V in L2
     const uint64_t pol_q = ptx::policy_evict_first();
     uint32_t it = 0, gk = 0, gv = 0;
     for (;; ++it) {
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
 #pragma unroll
             for (int c = 0; c < L::CHUNKS; ++c)
               ptx::tma_load_3d(base + sl * L::HALF_BYTES + c * L::H_CHUNK, tm, &full[sl], c * 64,
-                               b * BK + (t & 1) * HN, h, pol_kv);
+                               b * BK + (t & 1) * HN, h, vis ? pol_kv : pol_q);
           }
         }
         ++cnt;
@@ -586,8 +588,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         int4* dst = reinterpret_cast<int4*>(orow + c * 32);
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          dst[e] = make_int4((int)pk[4 * e], (int)pk[4 * e + 1], (int)pk[4 * e + 2],
-                             (int)pk[4 * e + 3]);
+          __stcs(dst + e, make_int4((int)pk[4 * e], (int)pk[4 * e + 1], (int)pk[4 * e + 2],
+                                    (int)pk[4 * e + 3]));  // streaming: keep K/V resident in L2
       }
       ptx::tc_fence_before();
     }

@@ -8,6 +8,7 @@
 
 #include <cuda_bf16.h>
 #include <math.h>
+#include <stdlib.h>
 
 namespace tcb {
 
@@ -264,6 +265,67 @@ __global__ void __launch_bounds__(256) k_scores(const double* __restrict__ pq, i
   }
 }
 
+// Same product on the FP64 tensor core (DMMA.8x8x4, mma.sync m8n8k4 f64): warp tile
+// 32 x 32 (4 x 4 MMA tiles, 32 fp64 accumulators per thread), CTA = 2 x 2 warps, operand
+// fragments read straight from L1/L2 (pq/pk are 11 MB each, L2-resident).
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128) k_scores_dmma(const double* __restrict__ pq, int pq_blocks,
+                                                     const double* __restrict__ pk, int rows,
+                                                     int M_total, int d, double sqrt_d,
+                                                     double* __restrict__ R) {
+  const int h = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = blockIdx.y * 64 + (warp >> 1) * 32;
+  const int c0 = blockIdx.x * 64 + (warp & 1) * 32;
+  const double* A = pq + (int64_t)h * pq_blocks * d;
+  const double* B = pk + (int64_t)h * M_total * d;
+  const int fr = lane >> 2, fk = lane & 3;
+  const double* ap[4];
+  const double* bp[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    ap[i] = A + (int64_t)min(r0 + 8 * i + fr, pq_blocks - 1) * d + fk;
+    bp[i] = B + (int64_t)min(c0 + 8 * i + fr, M_total - 1) * d + fk;
+  }
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < d; k += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a[i] = __ldg(ap[i] + k);
+      b[i] = __ldg(bp[i] + k);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+  double* Rh = R + (int64_t)h * rows * M_total;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gr = r0 + 8 * i + fr;
+    if (gr >= rows) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gc = c0 + 8 * j + 2 * fk + e;
+        if (gc < M_total) Rh[(int64_t)gr * M_total + gc] = acc[i][j][e] / sqrt_d;
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_row_softmax(double* __restrict__ R, int64_t n_rows,
                                                      int M_total) {
   __shared__ double sbuf[8 * 2 * PW_MAX_LEAVES];
@@ -365,28 +427,42 @@ __device__ RadixState warp_radix(const uint64_t* keys, int n, int K, bool weight
                                  uint32_t* hist, double* hsum) {
   const int lane = threadIdx.x & 31;
   RadixState r{0ull, 0ull, weighted ? 0 : K, 0, 0.0, 0};
+  // Count mode: bytes on which every key agrees (the sign/exponent bytes of a row of
+  // probabilities) cannot split the candidates; they are folded into the prefix without a
+  // histogram pass.  AND/OR of all keys finds them.
+  uint64_t kand = ~0ull, kor = 0ull;
+  if (!weighted) {
+    for (int j = lane; j < n; j += 32) {
+      const uint64_t k = keys[j];
+      kand &= k;
+      kor |= k;
+    }
+    const uint32_t al = __reduce_and_sync(FULL, (uint32_t)kand), ah = __reduce_and_sync(FULL, (uint32_t)(kand >> 32));
+    const uint32_t ol = __reduce_or_sync(FULL, (uint32_t)kor), oh = __reduce_or_sync(FULL, (uint32_t)(kor >> 32));
+    kand = ((uint64_t)ah << 32) | al;
+    kor = ((uint64_t)oh << 32) | ol;
+  }
   for (int byte = 7; byte >= 0; --byte) {
+    const int sh = byte * 8;
+    if (!weighted && (((kand ^ kor) >> sh) & 0xFFull) == 0ull) {
+      r.prefix |= kand & (0xFFull << sh);
+      r.mask |= 0xFFull << sh;
+      continue;
+    }
     for (int i = lane; i < 256; i += 32) {
       hist[i] = 0u;
       if (weighted) hsum[i] = 0.0;
     }
     __syncwarp();
-    const int sh = byte * 8;
     for (int j0 = 0; j0 < n; j0 += 32) {
       const int j = j0 + lane;
-      bool cand = false;
-      int dg = 0;
-      uint64_t k = 0;
       if (j < n) {
-        k = keys[j];
-        cand = (k & r.mask) == r.prefix;
-        dg = (int)((k >> sh) & 0xFF);
-      }
-      const unsigned act = __ballot_sync(FULL, cand);
-      if (cand) {
-        const unsigned peers = __match_any_sync(act, dg);
-        if (lane == __ffs(peers) - 1) atomicAdd(&hist[dg], (uint32_t)__popc(peers));
-        if (weighted) atomicAdd(&hsum[dg], key_value(k));
+        const uint64_t k = keys[j];
+        if ((k & r.mask) == r.prefix) {
+          const int dg = (int)((k >> sh) & 0xFF);
+          atomicAdd(&hist[dg], 1u);  // digits are spread once constant bytes are skipped
+          if (weighted) atomicAdd(&hsum[dg], key_value(k));
+        }
       }
     }
     __syncwarp();
@@ -702,6 +778,25 @@ __global__ void k_mask_unpack(const uint32_t* __restrict__ bits, int64_t rows, i
 
 using namespace tcb;
 
+// K4a launcher: DMMA (FP64 tensor core) by default, the SIMT-DFMA tile kernel with
+// TCB_SCORES_SIMT=1 (kept for A/B).
+static int launch_scores(const double* pq, int pq_blocks, const double* pk, int H, int rows,
+                         int M_total, int d, double* R, cudaStream_t st) {
+  static int simt = -1;
+  if (simt < 0) {
+    const char* e = getenv("TCB_SCORES_SIMT");
+    simt = e ? atoi(e) : 0;
+  }
+  if (simt || d % 4 != 0) {
+    dim3 grid((unsigned)ceil_div(M_total, ST_TILE), (unsigned)ceil_div(rows, ST_TILE), H);
+    k_scores<<<grid, 256, 0, st>>>(pq, pq_blocks, pk, rows, M_total, d, sqrt((double)d), R);
+    return check_launch("k_scores");
+  }
+  dim3 grid((unsigned)ceil_div(M_total, 64), (unsigned)ceil_div(rows, 64), H);
+  k_scores_dmma<<<grid, 128, 0, st>>>(pq, pq_blocks, pk, rows, M_total, d, sqrt((double)d), R);
+  return check_launch("k_scores_dmma");
+}
+
 extern "C" int tcb_block_pool(const void* x0, const void* x1, int dtype, int64_t stride_h,
                               int64_t stride_n, int H, int d, int m, int M_v, int M_total,
                               int64_t n_valid, int64_t n_cond, double* out0, double* out1,
@@ -754,9 +849,7 @@ extern "C" int tcb_block_relevance(const double* pq, int pq_blocks, const double
   TCB_CHECK_ARG(M_total <= 16384, TCB_ESIZE, "M_total %d > 16384 unsupported", M_total);
   if (rows == 0) return TCB_OK;
   cudaStream_t st = as_stream(stream);
-  dim3 grid((unsigned)ceil_div(M_total, ST_TILE), (unsigned)ceil_div(rows, ST_TILE), H);
-  k_scores<<<grid, 256, 0, st>>>(pq, pq_blocks, pk, rows, M_total, d, sqrt((double)d), R);
-  int rc = check_launch("k_scores");
+  int rc = launch_scores(pq, pq_blocks, pk, H, rows, M_total, d, R, st);
   if (rc) return rc;
   const int64_t n_rows = (int64_t)H * rows;
   k_row_softmax<<<(unsigned)ceil_div(n_rows, 8), 256, 0, st>>>(R, n_rows, M_total);
@@ -816,10 +909,7 @@ extern "C" int tcb_block_scores(const double* pq, int pq_blocks, const double* p
   TCB_CHECK_ARG(H >= 1 && rows >= 0 && rows <= pq_blocks && M_total >= 1 && d >= 1, TCB_ESHAPE,
                 "bad scores shape");
   if (rows == 0) return TCB_OK;
-  dim3 grid((unsigned)ceil_div(M_total, ST_TILE), (unsigned)ceil_div(rows, ST_TILE), H);
-  k_scores<<<grid, 256, 0, as_stream(stream)>>>(pq, pq_blocks, pk, rows, M_total, d,
-                                                sqrt((double)d), S);
-  return check_launch("k_scores");
+  return launch_scores(pq, pq_blocks, pk, H, rows, M_total, d, S, as_stream(stream));
 }
 
 extern "C" int tcb_mask_pack(const uint8_t* dense, int64_t rows, int M_total, int words,
