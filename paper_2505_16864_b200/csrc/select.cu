@@ -120,6 +120,7 @@ constexpr int ST_KC = 32;
 // (contiguous runs of <= 128) are independent, so a warp sums them in parallel and
 // lane 0 folds the leaf sums in the recursion's order.
 constexpr int PW_MAX_LEAVES = 256;  // enough for n <= 16384
+constexpr int SEL_MAX_LEAVES = 128;  // k_select: M_total <= 8192 -> <= 128 leaves of >= 64
 
 __device__ __forceinline__ double pw_leaf(const double* p, int len) {
   if (len < 8) {
@@ -194,6 +195,37 @@ __device__ double pw_fold(int n, const double* leaf) {
 // Whole-row pairwise sum by one warp: lane 0 enumerates the leaves into the warp's
 // scratch, lanes sum leaves in parallel, lane 0 folds.  scratch: PW_MAX_LEAVES doubles
 // followed by 2*PW_MAX_LEAVES ints.
+// The fold as a straight-line program over value slots: leaves occupy slots [0, nl),
+// internal node i (post-order, the order pw_fold evaluates them) writes slot nl + i =
+// slot a_i + slot b_i.  Built once per CTA (the tree depends only on n), executed per
+// row by one lane with no stack -- bitwise the pw_fold result.
+__device__ int pw_program(int n, int nl, int2* ops) {
+  int st_len[32], st_state[32], st_left[32], sp = 1, ret = -1, leafc = 0, nops = 0;
+  st_len[0] = n;
+  st_state[0] = 0;
+  while (sp) {
+    const int top = sp - 1;
+    int n2 = st_len[top] / 2;
+    n2 -= n2 % 8;
+    if (st_state[top] == 0 && st_len[top] > 128) {
+      st_state[top] = 1;
+      st_len[sp] = n2; st_state[sp] = 0; ++sp;
+    } else if (st_state[top] == 0) {
+      ret = leafc++;
+      --sp;
+    } else if (st_state[top] == 1) {
+      st_left[top] = ret;
+      st_state[top] = 2;
+      st_len[sp] = st_len[top] - n2; st_state[sp] = 0; ++sp;
+    } else {
+      ops[nops] = make_int2(st_left[top], ret);
+      ret = nl + nops++;
+      --sp;
+    }
+  }
+  return nops;
+}
+
 __device__ double warp_pairwise_sum(const double* row, int n, double* scratch) {
   const int lane = threadIdx.x & 31;
   double* leaf = scratch;
@@ -593,7 +625,7 @@ __device__ int warp_sorted_cut(uint64_t* skey, int* scol, int cnt, int np2, doub
 
 // One warp per (head, vision row).  RAW: the row holds scaled pooled scores and is first
 // turned into R in place (max, exp, numpy-pairwise sum, divide; masks.py:132-134).
-// Per-warp smem: keys[M_pad] | hist[256] | sbits[words_pad] | leaf[PW_MAX_LEAVES] |
+// Per-warp smem: keys[M_pad] | hist[256] | sbits[words_pad] | leaf[nslots] |
 //                (SORT) hsum[256] | skey[np2] | scol[np2]
 template <bool RAW, bool SORT>
 __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R, int64_t n_rows,
@@ -604,12 +636,16 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
                                                           uint32_t* __restrict__ bits,
                                                           int32_t* __restrict__ kv_idx,
                                                           int32_t* __restrict__ kv_cnt,
-                                                          int per_warp_bytes) {
+                                                          int per_warp_bytes, int nslots) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int leaf_off[PW_MAX_LEAVES], leaf_len[PW_MAX_LEAVES];
-  __shared__ int s_nl;
+  __shared__ int leaf_off[SEL_MAX_LEAVES], leaf_len[SEL_MAX_LEAVES];
+  __shared__ int2 fold_ops[SEL_MAX_LEAVES];
+  __shared__ int s_nl, s_nops;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (RAW && threadIdx.x == 0) s_nl = pw_leaves(M_total, leaf_off, leaf_len);
+  if (RAW && threadIdx.x == 0) {
+    s_nl = pw_leaves(M_total, leaf_off, leaf_len);
+    s_nops = pw_program(M_total, s_nl, fold_ops);
+  }
   __syncthreads();
   const int64_t row = (int64_t)blockIdx.x * SW_WARPS + warp;
   if (row >= n_rows) return;
@@ -621,7 +657,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
   uint32_t* sbits = hist + 256;
   const int words_pad = (words + 1) & ~1;
   double* leaf = reinterpret_cast<double*>(sbits + words_pad);
-  double* hsum = leaf + PW_MAX_LEAVES;
+  double* hsum = leaf + nslots;
   uint64_t* skey = reinterpret_cast<uint64_t*>(hsum + 256);
   int* scol = reinterpret_cast<int*>(skey + np2);
   const int i = (int)(row % M_v);
@@ -643,7 +679,11 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
     for (int l = lane; l < nl; l += 32) leaf[l] = pw_leaf(vals + leaf_off[l], leaf_len[l]);
     __syncwarp();
     double tot = 0.0;
-    if (lane == 0) tot = pw_fold(M_total, leaf);
+    if (lane == 0) {
+      const int nops = s_nops;
+      for (int q = 0; q < nops; ++q) leaf[nl + q] = leaf[fold_ops[q].x] + leaf[fold_ops[q].y];
+      tot = leaf[nops ? nl + nops - 1 : 0];
+    }
     tot = __shfl_sync(FULL, tot, 0);
     for (int j = lane; j < M_total; j += 32) {
       const double v = vals[j] / tot;
@@ -863,6 +903,21 @@ static int launch_select(double* R, bool raw, int H, int M_v, int M_total, const
   TCB_CHECK_ARG(H >= 1 && M_v >= 0 && M_total >= 1, TCB_ESHAPE, "bad select shape");
   TCB_CHECK_ARG(words >= ceil_div(M_total, 32), TCB_ESHAPE, "words too small");
   TCB_CHECK_ARG(M_total <= 8192, TCB_ESIZE, "M_total %d > 8192 unsupported", M_total);
+  // per-warp leaf slots: nl leaves + (nl - 1) folds, nl <= 8192 / 64 = SEL_MAX_LEAVES
+  int nl = 0;
+  {
+    int st[64], sp = 0;
+    st[sp++] = M_total;
+    while (sp) {
+      const int l = st[--sp];
+      if (l <= 128) { ++nl; continue; }
+      int n2 = l / 2;
+      n2 -= n2 % 8;
+      st[sp++] = l - n2;
+      st[sp++] = n2;
+    }
+  }
+  const int nslots = (2 * nl + 1) & ~1;
   TCB_CHECK_ARG(n_floor >= 1, TCB_EDOMAIN, "n_floor must be >= 1");
   const int64_t n_rows = (int64_t)H * M_v;
   if (n_rows == 0) return TCB_OK;
@@ -870,7 +925,7 @@ static int launch_select(double* R, bool raw, int H, int M_v, int M_total, const
   int np2 = 2;
   while (np2 < M_total) np2 <<= 1;
   const int M_pad = (M_total + 1) & ~1, words_pad = (words + 1) & ~1;
-  size_t per_warp = (size_t)M_pad * 8 + 256 * 4 + (size_t)words_pad * 4 + PW_MAX_LEAVES * 8;
+  size_t per_warp = (size_t)M_pad * 8 + 256 * 4 + (size_t)words_pad * 4 + (size_t)nslots * 8;
   if (sort) per_warp += 256 * 8 + (size_t)np2 * 12;
   per_warp = (per_warp + 15) & ~size_t(15);
   const size_t smem = per_warp * SW_WARPS;
@@ -879,7 +934,7 @@ static int launch_select(double* R, bool raw, int H, int M_v, int M_total, const
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "k_select smem: %s", cudaGetErrorString(e));
     kern<<<grid, SW_WARPS * 32, smem, s>>>(R, n_rows, M_v, M_total, np2, adja, words, n_floor, p,
-                                          with_union, bits, kv_idx, kv_cnt, (int)per_warp);
+                                          with_union, bits, kv_idx, kv_cnt, (int)per_warp, nslots);
     return check_launch("k_select");
   };
   if (raw) return sort ? go(k_select<true, true>) : go(k_select<true, false>);
