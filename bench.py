@@ -109,10 +109,16 @@ def run_gpu(args):
     from paper_2505_16864_b200.partition import mask_words
 
     world, rank, local = dist_env()
+    # --dist-backend gloo: orchestration test with several ranks sharing the visible GPUs
+    # (the exchange is staged through the host); production runs use NCCL, one GPU per rank
+    local = local % torch.cuda.device_count() if args.dist_backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     _native.load()
 
     dims = tcb.GridDims(*DIMS)
@@ -184,7 +190,10 @@ def run_gpu(args):
                   oh.permute(1, 0, 2), marks)
             return head_to_seq(oh)
 
+    red_dev = "cpu" if args.dist_backend == "gloo" else dev  # device of the scalar reductions
+
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -196,7 +205,7 @@ def run_gpu(args):
     pairs_local = int(kv_cnt.sum().item()) + Hl * layout.M_c * Mt
     pairs = pairs_local
     if world > 1:
-        t = torch.tensor([pairs_local], device=dev, dtype=torch.int64)
+        t = torch.tensor([pairs_local], device=red_dev, dtype=torch.int64)
         dist.all_reduce(t)
         pairs = int(t.item())
 
@@ -214,7 +223,7 @@ def run_gpu(args):
                     for i in range(args.steps)])
     ms_step = total_ms / args.steps
     if world > 1:
-        t = torch.tensor([ms_step], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms_step], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
     k_pool, k_rel, k_sel, k_carve = per.mean(axis=0)
@@ -256,7 +265,7 @@ def run_gpu(args):
         cpu = cpu_baseline(args.cpu_seconds)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "carve_traffic.json")
-    if os.path.exists(tpath):
+    if world == 1 and os.path.exists(tpath):  # the capture is of the 1-GPU C2 launch
         try:
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
@@ -400,6 +409,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

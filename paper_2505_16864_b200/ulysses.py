@@ -24,6 +24,17 @@ from .partition import BlockLayout
 __all__ = ["seq_to_head", "head_to_seq", "carve_layer_sp"]
 
 
+def _all_to_all(recv: torch.Tensor, send: torch.Tensor, group=None) -> None:
+    """NCCL all_to_all_single over NVLink; a gloo group (CPU tests, or several ranks
+    sharing one GPU in the orchestration test) stages CUDA tensors through the host."""
+    if recv.is_cuda and dist.get_backend(group) == "gloo":
+        r = torch.empty(recv.shape, dtype=recv.dtype)
+        dist.all_to_all_single(r, send.cpu(), group=group)
+        recv.copy_(r)
+        return
+    dist.all_to_all_single(recv, send, group=group)
+
+
 def seq_to_head(xs: list, group=None) -> list:
     """[(N/G, H, d)] per tensor -> [(N, H/G, d)] head shards, one collective for all."""
     G = dist.get_world_size(group)
@@ -37,7 +48,7 @@ def seq_to_head(xs: list, group=None) -> list:
         # so recv viewed as (G*n_loc, hg, d) is already the token-ordered head shard
         send = x.view(n_loc, G, hg, d).permute(1, 0, 2, 3).contiguous()
         recv = torch.empty_like(send)
-        dist.all_to_all_single(recv, send, group=group)
+        _all_to_all(recv, send, group)
         outs.append(recv.view(G * n_loc, hg, d))
     return outs
 
@@ -49,7 +60,7 @@ def head_to_seq(o: torch.Tensor, group=None) -> torch.Tensor:
     n_loc = N // G
     send = o.contiguous().view(G, n_loc, hg, d)
     recv = torch.empty_like(send)
-    dist.all_to_all_single(recv, send, group=group)
+    _all_to_all(recv, send, group)
     return recv.permute(1, 0, 2, 3).reshape(n_loc, G * hg, d)
 
 

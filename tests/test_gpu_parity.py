@@ -304,3 +304,31 @@ def test_carve_layer_host_pipeline_bitwise(hpc):
     ref32 = oracle.carve(q32, k32, v32, m32.bits.cpu().numpy(), L, 0.0, workers=8)
     assert isinstance(o32, np.ndarray)
     np.testing.assert_allclose(o32, ref32, rtol=1e-5, atol=1e-5)
+
+
+# ----------------------------------------------------------------- Ulysses layout (§8e)
+def test_token_major_head_shard_layout_bitwise():
+    # after the all-to-all each rank holds a token-major (N, H/G, d) head shard; every
+    # kernel consumes it in place through (stride_h, stride_n) -- results must equal the
+    # head-major contiguous path bitwise (this is what bench.py --gpus N>1 runs)
+    dims = tcb.GridDims(4, 16, 24)
+    lay = tcb.build_layout(dims, 128, 60)
+    st = tcb.StaticMasks.build(lay, dims, tcb.build_curve(dims))
+    params = tcb.SelectionParams(k=0.3, p=0.0)
+    g = torch.Generator(device="cuda").manual_seed(8)
+    H, d = 3, 128
+    q, k, v = (torch.randn((H, lay.padded_total, d), generator=g, device="cuda").to(torch.bfloat16)
+               for _ in range(3))
+    tm = [torch.empty((lay.padded_total, H, d), dtype=torch.bfloat16, device="cuda") for _ in range(3)]
+    for dst, src in zip(tm, (q, k, v)):
+        dst.copy_(src.permute(1, 0, 2))
+    qv, kv, vv = (t.permute(1, 0, 2) for t in tm)  # (H, N, d) views, strides (d, H*d, 1)
+    assert qv.stride() == (d, H * d, 1)
+    m_ref, R_ref = tcb.build_block_mask(q, k, lay, st, params)
+    m_tm, R_tm = tcb.build_block_mask(qv, kv, lay, st, params)
+    assert torch.equal(R_tm, R_ref) and torch.equal(m_tm.words, m_ref.words)
+    beta = tcb.AmplifierBias(0.2)
+    o_ref = tcb.carve_attention(tcb.AttentionInputs(q=q, k=k, v=v, layout=lay), m_ref, beta)
+    o_tm = tcb.carve_attention(tcb.AttentionInputs(q=qv, k=kv, v=vv, layout=lay), m_tm, beta)
+    assert o_tm.stride() == qv.stride()
+    assert torch.equal(o_tm, o_ref)
