@@ -94,17 +94,6 @@ struct RopeGeom {
   int t, h, w, d_t, d_h, d_w;
 };
 
-__device__ __forceinline__ float2 rope_cs(const float2* __restrict__ tab, const RopeGeom& r,
-                                          int ct, int ch, int cw, int e) {
-  if (e < r.d_t) return __ldg(tab + ct * (r.d_t / 2) + e / 2);
-  const int off_h = r.t * (r.d_t / 2);
-  e -= r.d_t;
-  if (e < r.d_h) return __ldg(tab + off_h + ch * (r.d_h / 2) + e / 2);
-  const int off_w = off_h + r.h * (r.d_h / 2);
-  e -= r.d_h;
-  return __ldg(tab + off_w + cw * (r.d_w / 2) + e / 2);
-}
-
 __device__ __forceinline__ float2 bf2_unpack(uint32_t u) {  // (lo, hi) bf16 -> fp32
   return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
 }
@@ -139,38 +128,53 @@ __global__ void __launch_bounds__(1024) k_rope_permute(RopeIO io, int64_t src_sn
   __nv_bfloat16* dst = io.dst[which];
   const bool rot = io.rotate[which] != 0;
   const int hw = r.h * r.w;
+  // The launch gives every thread exactly one (head, chunk) slot of a token (blockDim ==
+  // H * d/8 <= 1024), so the chunk's 4 rotation pairs -- their axis, table base and
+  // per-position stride -- are resolved once, outside the token loop.
+  const int j = threadIdx.x;
+  if (j >= per_tok) return;
+  const int hh = j / chunks, c = j - hh * chunks;
+  const int64_t so = (int64_t)hh * src_sh + c * 8, dof = (int64_t)hh * dst_sh + c * 8;
+  int axis[4], tb[4], ts[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    int e = c * 8 + 2 * p;
+    if (e < r.d_t) {
+      axis[p] = 0; tb[p] = e / 2; ts[p] = r.d_t / 2;
+    } else if ((e -= r.d_t) < r.d_h) {
+      axis[p] = 1; tb[p] = r.t * (r.d_t / 2) + e / 2; ts[p] = r.d_h / 2;
+    } else {
+      e -= r.d_h;
+      axis[p] = 2; tb[p] = r.t * (r.d_t / 2) + r.h * (r.d_h / 2) + e / 2; ts[p] = r.d_w / 2;
+    }
+  }
   for (int i0 = blockIdx.x * ROPE_TOK; i0 < n; i0 += gridDim.x * ROPE_TOK) {
     int cell[ROPE_TOK];  // tail tokens re-read the last valid one (store skipped)
 #pragma unroll
     for (int u = 0; u < ROPE_TOK; ++u) cell[u] = __ldg(fwd + min(i0 + u, n - 1));
-    for (int j = threadIdx.x; j < per_tok; j += blockDim.x) {
-      const int hh = j / chunks, c = j - hh * chunks;
-      const int64_t so = (int64_t)hh * src_sh + c * 8;
-      int4 raw[ROPE_TOK];
+    int4 raw[ROPE_TOK];
 #pragma unroll
-      for (int u = 0; u < ROPE_TOK; ++u)
-        raw[u] = __ldcs(reinterpret_cast<const int4*>(src + (int64_t)cell[u] * src_sn + so));
+    for (int u = 0; u < ROPE_TOK; ++u)
+      raw[u] = __ldcs(reinterpret_cast<const int4*>(src + (int64_t)cell[u] * src_sn + so));
 #pragma unroll
-      for (int u = 0; u < ROPE_TOK; ++u) {
-        int4 res = raw[u];
-        if (rot) {
-          const int ct = cell[u] / hw, rem = cell[u] - ct * hw;
-          const int ch = rem / r.w, cw = rem - ch * r.w;
-          uint32_t w4[4] = {(uint32_t)res.x, (uint32_t)res.y, (uint32_t)res.z, (uint32_t)res.w};
+    for (int u = 0; u < ROPE_TOK; ++u) {
+      int4 res = raw[u];
+      if (rot) {
+        const int ct = cell[u] / hw, rem = cell[u] - ct * hw;
+        const int ch = rem / r.w, cw = rem - ch * r.w;
+        uint32_t w4[4] = {(uint32_t)res.x, (uint32_t)res.y, (uint32_t)res.z, (uint32_t)res.w};
 #pragma unroll
-          for (int p = 0; p < 4; ++p) {
-            const float2 x = bf2_unpack(w4[p]);
-            const float2 cs = rope_cs(tab, r, ct, ch, cw, c * 8 + 2 * p);
-            const float o0 = __fsub_rn(__fmul_rn(x.x, cs.x), __fmul_rn(x.y, cs.y));
-            const float o1 = __fadd_rn(__fmul_rn(x.x, cs.y), __fmul_rn(x.y, cs.x));
-            w4[p] = bf2_pack(o0, o1);
-          }
-          res = make_int4((int)w4[0], (int)w4[1], (int)w4[2], (int)w4[3]);
+        for (int p = 0; p < 4; ++p) {
+          const int pos = axis[p] == 0 ? ct : (axis[p] == 1 ? ch : cw);
+          const float2 cs = __ldg(tab + tb[p] + pos * ts[p]);
+          const float2 x = bf2_unpack(w4[p]);
+          const float o0 = __fsub_rn(__fmul_rn(x.x, cs.x), __fmul_rn(x.y, cs.y));
+          const float o1 = __fadd_rn(__fmul_rn(x.x, cs.y), __fmul_rn(x.y, cs.x));
+          w4[p] = bf2_pack(o0, o1);
         }
-        if (i0 + u < n)
-          __stcs(reinterpret_cast<int4*>(dst + (int64_t)(i0 + u) * dst_sn + (int64_t)hh * dst_sh + c * 8),
-                 res);
+        res = make_int4((int)w4[0], (int)w4[1], (int)w4[2], (int)w4[3]);
       }
+      if (i0 + u < n) __stcs(reinterpret_cast<int4*>(dst + (int64_t)(i0 + u) * dst_sn + dof), res);
     }
   }
 }
@@ -262,8 +266,9 @@ extern "C" int tcb_rope_permute(const void* const* src, int64_t src_sn, int64_t 
   int64_t blocks = groups < (int64_t)sms * 16 ? groups : (int64_t)sms * 16;  // grid-stride
   dim3 grid((unsigned)blocks, (unsigned)n_tensors);
   // one thread per 16-byte chunk of a token's H*d row block (384 at H=24, d=128)
-  int threads = (int)ceil_div((int64_t)H * (d / 8), 32) * 32;
-  if (threads > 1024) threads = 1024;
+  TCB_CHECK_ARG((int64_t)H * (d / 8) <= 1024, TCB_ESIZE, "H * d / 8 = %d > 1024 chunks per token",
+                H * (d / 8));
+  const int threads = (int)ceil_div((int64_t)H * (d / 8), 32) * 32;
   k_rope_permute<<<grid, threads, 0, as_stream(stream)>>>(io, src_sn, src_sh, dst_sh, dst_sn, fwd,
                                                       (int)n, H, d, (const float2*)cos_sin,
                                                       RopeGeom{t, h, w, d_t, d_h, d_w});
