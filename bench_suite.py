@@ -59,12 +59,12 @@ def peaks():
 class Layer:
     """Device buffers + the four launches of one carved-attention layer."""
 
-    def __init__(self, dims, n_cond, H, k_rate, seed=0):
+    def __init__(self, dims, n_cond, H, k_rate, seed=0, p_cut=0.0, beta=0.0):
         self.dims = tcb.GridDims(*dims)
         self.lay = tcb.build_layout(self.dims, 128, n_cond)
         self.st = tcb.StaticMasks.build(self.lay, self.dims, tcb.build_curve(self.dims))
         self.adja = self.st.packed(self.lay)
-        self.H, self.k = H, k_rate
+        self.H, self.k, self.p, self.beta = H, k_rate, p_cut, beta
         L = self.lay
         g = torch.Generator(device="cuda")
         g.manual_seed(seed)
@@ -83,14 +83,14 @@ class Layer:
 
     def mask(self):
         L, H = self.lay, self.H
-        n_floor = tcb.SelectionParams(k=self.k, p=0.0).n_floor(L.M_v)
+        n_floor = tcb.SelectionParams(k=self.k, p=self.p).n_floor(L.M_v)
         _native.call("tcb_block_pool", self.q.data_ptr(), self.kk.data_ptr(), 1, self.q.stride(0),
                      self.q.stride(1), H, 128, 128, L.M_v, L.M_total, L.n_valid, L.n_cond,
                      self.pq.data_ptr(), self.pk.data_ptr(), self.s)
         _native.call("tcb_block_scores", self.pq.data_ptr(), L.M_total, self.pk.data_ptr(), H, L.M_v,
                      L.M_total, 128, self.R.data_ptr(), self.s)
         _native.call("tcb_block_select_scores", self.R.data_ptr(), H, L.M_v, L.M_total,
-                     self.adja.data_ptr(), self.words, n_floor, 0.0, 1, self.bits.data_ptr(),
+                     self.adja.data_ptr(), self.words, n_floor, float(self.p), 1, self.bits.data_ptr(),
                      self.kv_idx.data_ptr(), self.kv_cnt.data_ptr(), self.s)
 
     def carve(self):
@@ -98,21 +98,21 @@ class Layer:
         _native.call("tcb_carve_fwd", self.q.data_ptr(), self.kk.data_ptr(), self.v.data_ptr(),
                      self.o.data_ptr(), 1, self.q.stride(0), self.q.stride(1),
                      self.kv_idx.data_ptr(), self.kv_cnt.data_ptr(), self.H, 128, 128, L.M_v,
-                     L.M_total, L.n_valid, L.n_cond, 0.0, self.work.data_ptr(), self.s)
+                     L.M_total, L.n_valid, L.n_cond, float(self.beta), self.work.data_ptr(), self.s)
 
     def pairs(self):
         return int(self.kv_cnt.sum().item()) + self.H * self.lay.M_c * self.lay.M_total
 
 
-def layer_record(name, dims, n_cond, H, k):
-    lay = Layer(dims, n_cond, H, k)
+def layer_record(name, dims, n_cond, H, k, p=0.0, beta=0.0):
+    lay = Layer(dims, n_cond, H, k, p_cut=p, beta=beta)
     t_mask = timed(lay.mask)
     lay.mask()
     t_carve = timed(lay.carve)
     pairs = lay.pairs()
     flops = 4.0 * 128 * 128 * 128 * pairs
     _, tf = peaks()
-    rec = {"config": name, "dims": list(dims), "heads": H, "k": k, "p": 0.0,
+    rec = {"config": name, "dims": list(dims), "heads": H, "k": k, "p": p, "beta": beta,
            "kept_pairs": pairs, "kept_fraction": round(pairs / (H * lay.lay.M_total ** 2), 4),
            "mask_ms": round(t_mask, 4), "carve_ms": round(t_carve, 4),
            "layer_ms": round(t_mask + t_carve, 4),
@@ -258,6 +258,16 @@ def main():
            "fused_f1": fused_records()}
     res["c3"] = layer_record("C3 Wan2.1-14B 480p 21x30x52, H=40, no text", (21, 30, 52), 0, 40, 0.08)
     res["c2"] = layer_record("C2 HunyuanVideo 720p 33x45x80 + 256 text, H=24", (33, 45, 80), 256, 24, 0.08)
+    # C4: the two stages of the stock 2-stage plan at 720p (cli.default_stage_plan: stage 1
+    # is 33x34x60, k=0.3, beta from rho=0.5; stage 2 the target, k=0.2; p=0.3), with the
+    # per-stage step counts of that plan (11 + 12 = 23 NFE)
+    beta1 = tcb.compute_beta(33 * 34 * 60, 33 * 45 * 80, 0.5)
+    s1 = layer_record("C4 stage 1 (0.75x): 33x34x60 + 256 text, H=24", (33, 34, 60), 256, 24, 0.3, 0.3, beta1)
+    s2 = layer_record("C4 stage 2 (1x): 33x45x80 + 256 text, H=24", (33, 45, 80), 256, 24, 0.2, 0.3)
+    res["c4_layers"] = {"stage1": s1, "stage2": s2, "nfe": [11, 12],
+                        "attention_ms_per_layer_sum_over_nfe": round(11 * s1["layer_ms"] + 12 * s2["layer_ms"], 2),
+                        "note": "x number of attention layers of the DiT (60 for HunyuanVideo-13B) for the "
+                                "sampler's attention time; stage switch kernels in c4_stage_switch"}
     if not a.skip_sweep:
         res["c5_sweep"] = [layer_record("C5 sweep on C2", (33, 45, 80), 256, 24, k)
                            for k in (0.01, 0.02, 0.05, 0.08, 0.10, 0.20, 0.30)]
