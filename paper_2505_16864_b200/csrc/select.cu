@@ -386,8 +386,9 @@ __global__ void __launch_bounds__(256) k_row_softmax(double* __restrict__ R, int
 //     and the total order is (key, column);
 //   * MSB-first radix select (8-bit digits, smem histograms) finds the top-K set of
 //     that order for any K without sorting;
-//   * for p > 0 a value-weighted radix pass bounds n_cut, only that many top columns
-//     are sorted (bitonic, smem) and scanned with the exact sequential prefix;
+//   * for p > 0 the top min(512, n) columns are radix-selected, sorted in registers
+//     (warp bitonic) and scanned with the exact sequential prefix; when the prefix
+//     cannot cross p inside that window the whole row is sorted in shared memory;
 //     p == 0 needs no sort at all (n_cut = 1 when the row max is > 0);
 //   * rows with negative entries (never produced by relevance) use a full sort.
 // The top-n_keep columns are ORed with the condition columns and the adjacency row
@@ -445,30 +446,25 @@ constexpr unsigned FULL = 0xffffffffu;
 
 struct RadixState {
   uint64_t prefix, mask;
-  int remaining;  // count mode: rank still needed inside the bin; weighted: count ranked before
+  int remaining;  // rank still needed inside the current bin
   int binc;       // elements in the chosen bin
-  double cum;     // weighted: value sum ranked before the candidate bin
-  int flag;       // weighted: the row total never exceeds p
 };
 
-// MSB-first radix select over the (key, column) order of keys[0, n) by one warp.
-// Count mode: the top-K set is {(key & mask) < prefix} U {first `remaining` columns with
-// (key & mask) == prefix}.  Weighted mode: locates where the cumulative value sum first
-// exceeds p; remaining + binc then bounds the rank of that crossing element.
-__device__ RadixState warp_radix(const uint64_t* keys, int n, int K, bool weighted, double p,
-                                 uint32_t* hist, double* hsum) {
+// MSB-first radix select over the (key, column) order of keys[0, n) by one warp: the
+// top-K set is {(key & mask) < prefix} U {first `remaining` columns with
+// (key & mask) == prefix}.  Bytes on which every key agrees (the sign/exponent bytes of a
+// row of probabilities) cannot split the candidates; they are folded into the prefix
+// without a histogram pass (AND/OR of all keys finds them).
+__device__ RadixState warp_radix(const uint64_t* keys, int n, int K, uint32_t* hist) {
   const int lane = threadIdx.x & 31;
-  RadixState r{0ull, 0ull, weighted ? 0 : K, 0, 0.0, 0};
-  // Count mode: bytes on which every key agrees (the sign/exponent bytes of a row of
-  // probabilities) cannot split the candidates; they are folded into the prefix without a
-  // histogram pass.  AND/OR of all keys finds them.
+  RadixState r{0ull, 0ull, K, 0};
   uint64_t kand = ~0ull, kor = 0ull;
-  if (!weighted) {
-    for (int j = lane; j < n; j += 32) {
-      const uint64_t k = keys[j];
-      kand &= k;
-      kor |= k;
-    }
+  for (int j = lane; j < n; j += 32) {
+    const uint64_t k = keys[j];
+    kand &= k;
+    kor |= k;
+  }
+  {
     const uint32_t al = __reduce_and_sync(FULL, (uint32_t)kand), ah = __reduce_and_sync(FULL, (uint32_t)(kand >> 32));
     const uint32_t ol = __reduce_or_sync(FULL, (uint32_t)kor), oh = __reduce_or_sync(FULL, (uint32_t)(kor >> 32));
     kand = ((uint64_t)ah << 32) | al;
@@ -476,82 +472,57 @@ __device__ RadixState warp_radix(const uint64_t* keys, int n, int K, bool weight
   }
   for (int byte = 7; byte >= 0; --byte) {
     const int sh = byte * 8;
-    if (!weighted && (((kand ^ kor) >> sh) & 0xFFull) == 0ull) {
+    if ((((kand ^ kor) >> sh) & 0xFFull) == 0ull) {
       r.prefix |= kand & (0xFFull << sh);
       r.mask |= 0xFFull << sh;
       continue;
     }
-    for (int i = lane; i < 256; i += 32) {
-      hist[i] = 0u;
-      if (weighted) hsum[i] = 0.0;
-    }
+    for (int i = lane; i < 256; i += 32) hist[i] = 0u;
     __syncwarp();
-    for (int j0 = 0; j0 < n; j0 += 32) {
-      const int j = j0 + lane;
-      if (j < n) {
-        const uint64_t k = keys[j];
-        if ((k & r.mask) == r.prefix) {
-          const int dg = (int)((k >> sh) & 0xFF);
-          atomicAdd(&hist[dg], 1u);  // digits are spread once constant bytes are skipped
-          if (weighted) atomicAdd(&hsum[dg], key_value(k));
-        }
-      }
+    for (int j = lane; j < n; j += 32) {
+      const uint64_t k = keys[j];
+      if ((k & r.mask) == r.prefix) atomicAdd(&hist[(int)((k >> sh) & 0xFF)], 1u);
     }
     __syncwarp();
     uint32_t c[8];
-    double sm[8];
     uint32_t ct = 0;
-    double st = 0.0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       c[i] = hist[lane * 8 + i];
-      sm[i] = weighted ? hsum[lane * 8 + i] : 0.0;
       ct += c[i];
-      st += sm[i];
     }
     uint32_t cin = ct;
-    double sin_ = st;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(FULL, cin, o);
-      const double z = __shfl_up_sync(FULL, sin_, o);
-      if (lane >= o) { cin += y; sin_ += z; }
+      if (lane >= o) cin += y;
     }
     uint32_t cex = cin - ct;
-    double sex = sin_ - st;
-    bool hit;
-    if (weighted) hit = (r.cum + sin_ > p) && !(r.cum + sex > p);
-    else hit = (cex < (uint32_t)r.remaining) && ((uint32_t)r.remaining <= cin);
+    const bool hit = (cex < (uint32_t)r.remaining) && ((uint32_t)r.remaining <= cin);
     const unsigned bal = __ballot_sync(FULL, hit);
-    if (bal == 0u) {  // weighted: candidates never push the sum past p
-      r.flag = 1;
-      return r;
-    }
     const int src = __ffs(bal) - 1;
     int bin = 7;
+    uint32_t binc = 0;
     if (lane == src) {
-      for (int i = 0; i < 8; ++i) {
-        const bool in = weighted ? (r.cum + sex + sm[i] > p) : ((uint32_t)r.remaining <= cex + c[i]);
-        if (in) { bin = i; break; }
-        cex += c[i];
-        sex += sm[i];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {  // unrolled: c[] stays in registers
+        if (bin == 7 && i < 7 && (uint32_t)r.remaining <= cex + c[i]) {
+          bin = i;
+          binc = c[i];
+        } else if (bin == 7 && i < 7) {
+          cex += c[i];
+        }
       }
+      if (bin == 7) binc = c[7];
     }
     const int dg = __shfl_sync(FULL, src * 8 + bin, src);
     const uint32_t before = __shfl_sync(FULL, cex, src);
-    const double before_sum = __shfl_sync(FULL, sex, src);
-    const uint32_t binc = __shfl_sync(FULL, c[bin], src);
+    binc = __shfl_sync(FULL, binc, src);
     r.prefix |= (uint64_t)dg << sh;
     r.mask |= 0xFFull << sh;
     r.binc = (int)binc;
-    if (weighted) {
-      r.cum += before_sum;
-      r.remaining += (int)before;
-      if (binc == 1u) return r;  // the crossing element is identified
-    } else {
-      r.remaining -= (int)before;
-      if ((int)binc == r.remaining) return r;  // whole bin selected
-    }
+    r.remaining -= (int)before;
+    if ((int)binc == r.remaining) return r;  // whole bin selected
     __syncwarp();
   }
   return r;
@@ -598,6 +569,85 @@ __device__ void warp_bitonic(uint64_t* key, int* col, int np2) {
   }
 }
 
+// Register bitonic sort of up to 512 (key, col) pairs by one warp: element e = 16*lane + r
+// lives in lane `lane`, register r.  Strides < 16 are in-register compare-exchanges,
+// strides >= 16 pair lane with lane ^ (stride / 16) through shuffles -- no shared memory,
+// no __syncwarp, full ILP.  Ascending (key, col) order == the reference's stable
+// descending argsort.
+struct KC {
+  uint64_t k;
+  int c;
+};
+__device__ __forceinline__ bool kc_less(const KC& a, const KC& b) {
+  return a.k < b.k || (a.k == b.k && a.c < b.c);
+}
+
+template <int KK, int JJ>
+__device__ __forceinline__ void reg_bitonic_stage(KC (&x)[16], int lane) {
+  if constexpr (JJ >= 16) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int e = lane * 16 + r;
+      KC o;
+      o.k = __shfl_xor_sync(FULL, x[r].k, JJ >> 4);
+      o.c = __shfl_xor_sync(FULL, x[r].c, JJ >> 4);
+      const bool up = (e & KK) == 0, lower = (e & JJ) == 0;
+      const bool take_o = (up == lower) ? kc_less(o, x[r]) : kc_less(x[r], o);
+      if (take_o) x[r] = o;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & JJ) continue;
+      const bool up = ((lane * 16 + r) & KK) == 0;
+      if (kc_less(x[r | JJ], x[r]) == up) {
+        const KC t = x[r];
+        x[r] = x[r | JJ];
+        x[r | JJ] = t;
+      }
+    }
+  }
+  if constexpr (JJ > 1) reg_bitonic_stage<KK, JJ / 2>(x, lane);
+}
+
+template <int KK>
+__device__ __forceinline__ void reg_bitonic_level(KC (&x)[16], int lane) {
+  reg_bitonic_stage<KK, KK / 2>(x, lane);
+  if constexpr (KK < 512) reg_bitonic_level<KK * 2>(x, lane);
+}
+
+__device__ __forceinline__ void reg_bitonic512(KC (&x)[16]) {
+  reg_bitonic_level<2>(x, threadIdx.x & 31);
+}
+
+// Exact np.cumsum scan of the sorted values: the sorted keys go back to the (padded)
+// staging buffer and lane 0 runs the dependent float64 add chain over them (loads
+// software-pipelined by the unrolled loop); returns 1 + #(prefix <= p), stopping at the
+// first crossing (the prefix of non-negative values is monotone).
+__device__ int reg_sorted_cut(const KC (&x)[16], uint64_t* stage, int cnt, double p,
+                              bool* crossed) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) stage[lane * 17 + r] = x[r].k;
+  __syncwarp();
+  int c = 0;
+  bool cr = false;
+  if (lane == 0) {
+    double pre = 0.0;
+#pragma unroll 8
+    for (int t = 0; t < cnt; ++t) {
+      pre = __dadd_rn(pre, key_value(stage[t + (t >> 4)]));  // np.cumsum order (masks.py:152)
+      if (pre > p) {
+        cr = true;
+        break;
+      }
+      ++c;
+    }
+  }
+  *crossed = __shfl_sync(FULL, (int)cr, 0) != 0;
+  return __shfl_sync(FULL, c, 0) + 1;
+}
+
 // Sort (key, col) pairs [0, cnt) of skey/scol (padded to np2) and return
 // 1 + #(sequential prefix <= p) over the sorted values; *crossed reports whether the
 // monotone prefix exceeded p inside the sorted window.
@@ -626,7 +676,7 @@ __device__ int warp_sorted_cut(uint64_t* skey, int* scol, int cnt, int np2, doub
 // One warp per (head, vision row).  RAW: the row holds scaled pooled scores and is first
 // turned into R in place (max, exp, numpy-pairwise sum, divide; masks.py:132-134).
 // Per-warp smem: keys[M_pad] | hist[256] | sbits[words_pad] | leaf[nslots] |
-//                (SORT) hsum[256] | skey[np2] | scol[np2]
+//                (SORT) skey[max(np2, 544)] | scol[max(np2, 544)]
 template <bool RAW, bool SORT>
 __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R, int64_t n_rows,
                                                           int M_v, int M_total, int np2,
@@ -657,9 +707,8 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
   uint32_t* sbits = hist + 256;
   const int words_pad = (words + 1) & ~1;
   double* leaf = reinterpret_cast<double*>(sbits + words_pad);
-  double* hsum = leaf + nslots;
-  uint64_t* skey = reinterpret_cast<uint64_t*>(hsum + 256);
-  int* scol = reinterpret_cast<int*>(skey + np2);
+  uint64_t* skey = reinterpret_cast<uint64_t*>(leaf + nslots);
+  int* scol = reinterpret_cast<int*>(skey + (np2 > 544 ? np2 : 544));
   const int i = (int)(row % M_v);
   double* Rr = R + row * M_total;
 
@@ -706,34 +755,72 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
 
   // ---- n_cut = 1 + #(sorted sequential prefix <= p)  (masks.py:150-153) ----
   int n_cut;
+  int reg_keep = 0;
+  bool reg_bits = false;  // the register path already wrote the top-keep set
   if (!neg && p == 0.0) {
     n_cut = pos ? 1 : M_total + 1;  // prefix_0 = row max
   } else if (SORT) {
-    int k_ub = M_total;
-    if (!neg) {
-      const RadixState w = warp_radix(keys, M_total, 0, true, p, hist, hsum);
-      if (!w.flag) {
-        const int est = w.remaining + w.binc;
-        k_ub = min(M_total, est + 16 + est / 64);  // margin for summation-order rounding
+    // Bound the crossing rank without a value-weighted histogram (fp64 shared atomics are
+    // CAS loops; they were half of this path's time): grow T (64, 128, ...) until the
+    // (any-order) sum of the top-T values exceeds p by more than the largest possible
+    // summation-order rounding difference, so the exact sequential prefix (np.cumsum
+    // order) crosses p within the top T.  Only those T are then sorted and scanned.
+    // The register path sorts the top min(512, M_total) (one radix select) and scans them
+    // exactly; it decides n_cut whenever the prefix crosses p inside that window (or the
+    // window is the whole row).  Otherwise (p close to the row total, or negative values
+    // from an external R) the smem path below sorts as much as needed.
+    const int k_ub = min(512, M_total);
+    bool done = false;
+    if (!neg && k_ub <= 512) {
+      // common case: the crossing lies in the top <= 512 -> register sort + shuffle scan
+      const RadixState t = warp_radix(keys, M_total, k_ub, hist);
+      uint64_t* stage_k = skey;  // staging with one pad slot per 16 (conflict-free lane reads)
+      int* stage_c = scol;
+      for (int e = lane; e < 512 + 32; e += 32) { stage_k[e] = ~0ull; stage_c[e] = 0x7fffffff; }
+      __syncwarp();
+      double part = 0.0;
+      warp_topk_visit(keys, M_total, t, [&](int j, int slot) {
+        stage_k[slot + (slot >> 4)] = keys[j];
+        stage_c[slot + (slot >> 4)] = j;
+        part += key_value(keys[j]);
+      });
+#pragma unroll
+      for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+      __syncwarp();
+      // the (any-order) window total must exceed p by more than any summation-order
+      // rounding for the exact prefix to cross inside the window; else go straight to the
+      // full sort
+      const bool window_ok = k_ub == M_total || part > p + 1e-12 * (1.0 + part);
+      if (window_ok) {
+      KC x[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        x[r].k = stage_k[lane * 17 + r];
+        x[r].c = stage_c[lane * 17 + r];
       }
+      reg_bitonic512(x);
+      bool crossed;
+      __syncwarp();
+      n_cut = reg_sorted_cut(x, stage_k, k_ub, p, &crossed);
+      if (crossed || k_ub == M_total) {
+        done = true;
+        reg_keep = max(n_cut, n_floor);
+        if (reg_keep <= k_ub) {  // the top-keep set is the first keep sorted slots
+#pragma unroll
+          for (int r = 0; r < 16; ++r)
+            if (lane * 16 + r < reg_keep) atomicOr(sbits + (x[r].c >> 5), 1u << (x[r].c & 31));
+          reg_bits = true;
+        }
+      }
+      }
+      __syncwarp();
     }
-    int cnt = M_total;
-    if (k_ub < M_total) {
-      const RadixState t = warp_radix(keys, M_total, k_ub, false, 0.0, hist, nullptr);
-      warp_topk_visit(keys, M_total, t, [&](int j, int slot) { skey[slot] = keys[j]; scol[slot] = j; });
-      cnt = k_ub;
-    } else {
-      for (int j = lane; j < M_total; j += 32) { skey[j] = keys[j]; scol[j] = j; }
-    }
-    int np = 2;
-    while (np < cnt) np <<= 1;
-    bool crossed;
-    n_cut = warp_sorted_cut(skey, scol, cnt, np, p, !neg, &crossed);
-    if (!neg && !crossed && cnt < M_total) {  // rounding pushed the cut past the window
+    if (!done) {  // full sort of the row in shared memory, exact scan
       for (int j = lane; j < M_total; j += 32) { skey[j] = keys[j]; scol[j] = j; }
       int npf = 2;
       while (npf < M_total) npf <<= 1;
-      n_cut = warp_sorted_cut(skey, scol, M_total, npf, p, true, &crossed);
+      bool crossed;
+      n_cut = warp_sorted_cut(skey, scol, M_total, npf, p, !neg, &crossed);
     }
   } else {
     n_cut = M_total + 1;  // unreachable: the host enables SORT whenever p > 0 or R is external
@@ -742,8 +829,8 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
   keep = min(keep, M_total);
 
   // ---- top-n_keep set -> bits, union, CSR ----
-  {
-    const RadixState t = warp_radix(keys, M_total, keep, false, 0.0, hist, nullptr);
+  if (!reg_bits) {
+    const RadixState t = warp_radix(keys, M_total, keep, hist);
     warp_topk_visit(keys, M_total, t,
                     [&](int j, int) { atomicOr(sbits + (j >> 5), 1u << (j & 31)); });
   }
@@ -926,7 +1013,8 @@ static int launch_select(double* R, bool raw, int H, int M_v, int M_total, const
   while (np2 < M_total) np2 <<= 1;
   const int M_pad = (M_total + 1) & ~1, words_pad = (words + 1) & ~1;
   size_t per_warp = (size_t)M_pad * 8 + 256 * 4 + (size_t)words_pad * 4 + (size_t)nslots * 8;
-  if (sort) per_warp += 256 * 8 + (size_t)np2 * 12;
+  // (np2 >= 544: the register-sort path stages 512 slots + one pad per 16 in skey/scol)
+  if (sort) per_warp += (size_t)(np2 > 544 ? np2 : 544) * 12;
   per_warp = (per_warp + 15) & ~size_t(15);
   const size_t smem = per_warp * SW_WARPS;
   const unsigned grid = (unsigned)ceil_div(n_rows, SW_WARPS);
