@@ -332,3 +332,35 @@ def test_token_major_head_shard_layout_bitwise():
     o_tm = tcb.carve_attention(tcb.AttentionInputs(q=qv, k=kv, v=vv, layout=lay), m_tm, beta)
     assert o_tm.stride() == qv.stride()
     assert torch.equal(o_tm, o_ref)
+
+
+@pytest.mark.parametrize("pattern", ["rising", "falling", "spiky"])
+def test_carve_bf16_online_softmax_extremes(pattern):
+    # forces the lazy-rescale path every block (rising scores), total underflow of late
+    # blocks (falling), and isolated huge logits (spiky) -- no NaN/Inf, oracle tolerance
+    dims = tcb.GridDims(4, 16, 24)
+    lay = tcb.build_layout(dims, 128, 30)
+    rng = np.random.default_rng(17)
+    H, d = 2, 128
+    N = lay.padded_total
+    q = rng.standard_normal((H, N, d)).astype(np.float32)
+    k = rng.standard_normal((H, N, d)).astype(np.float32)
+    v = rng.standard_normal((H, N, d)).astype(np.float32)
+    blk = (np.arange(N) // 128).astype(np.float32)
+    if pattern == "rising":
+        k *= (0.2 + 0.9 * blk)[None, :, None]
+    elif pattern == "falling":
+        k *= (8.0 / (1.0 + blk))[None, :, None]
+    else:
+        k[:, rng.integers(0, N, 16)] *= 40.0
+    bits = np.ones((H, lay.M_v, lay.M_total), bool)
+    qb, kb, vb = (_bf16(a) for a in (q, k, v))
+    out = tcb.carve_attention(tcb.AttentionInputs(q=qb, k=kb, v=vb, layout=lay),
+                              tcb.BlockMask(bits=bits), tcb.AmplifierBias(0.5))
+    got = out.float().cpu().numpy()
+    assert np.all(np.isfinite(got))
+    L = oracle.layout_scalars(dims.as_tuple(), 128, 30)
+    ref = oracle.carve(qb.float().cpu().numpy(), kb.float().cpu().numpy(), vb.float().cpu().numpy(),
+                       bits, L, 0.5, workers=8)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err <= 2e-2, err
