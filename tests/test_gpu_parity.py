@@ -364,3 +364,35 @@ def test_carve_bf16_online_softmax_extremes(pattern):
                        bits, L, 0.5, workers=8)
     err = np.abs(got - ref).max() / np.abs(ref).max()
     assert err <= 2e-2, err
+
+
+def test_carve_bf16_fuzz_random_layouts():
+    # random grids / text lengths / heads / selection rates / beta through both kernels:
+    # tcgen05 (bf16, m=128) vs the fp32 oracle on the same mask (2e-2), plus the fp32 SIMT
+    # kernel (1e-5) -- exercises 1-block rows, condition-only tails, partial blocks
+    rng = np.random.default_rng(2024)
+    for trial in range(10):
+        dims = tcb.GridDims(int(rng.integers(1, 5)), int(rng.integers(3, 20)), int(rng.integers(3, 24)))
+        n_cond = int(rng.choice([0, 1, 77, 128, 300]))
+        lay = tcb.build_layout(dims, 128, n_cond)
+        H = int(rng.integers(1, 4))
+        st = tcb.StaticMasks.build(lay, dims, tcb.build_curve(dims))
+        q, k, v = (rng.standard_normal((H, lay.padded_total, 128)).astype(np.float32)
+                   for _ in range(3))
+        qb, kb, vb = (_bf16(a) for a in (q, k, v))
+        params = tcb.SelectionParams(k=float(rng.choice([0.05, 0.3, 1.0])),
+                                     p=float(rng.choice([0.0, 0.3, 0.9])))
+        beta = float(rng.choice([0.0, 0.3]))
+        mask, _ = tcb.build_block_mask(qb, kb, lay, st, params)
+        out = tcb.carve_attention(tcb.AttentionInputs(q=qb, k=kb, v=vb, layout=lay), mask,
+                                  tcb.AmplifierBias(beta))
+        L = oracle.layout_scalars(dims.as_tuple(), 128, n_cond)
+        bits = mask.bits.cpu().numpy()
+        q32, k32, v32 = (t.float().cpu().numpy() for t in (qb, kb, vb))
+        ref = oracle.carve(q32, k32, v32, bits, L, beta, workers=8)
+        got = out.float().cpu().numpy()
+        err = np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30)
+        assert err <= 2e-2, (trial, dims.as_tuple(), n_cond, H, err)
+        o32 = tcb.carve_attention(tcb.AttentionInputs(q=q32, k=k32, v=v32, layout=lay),
+                                  tcb.BlockMask(bits=bits), tcb.AmplifierBias(beta))
+        np.testing.assert_allclose(o32, ref, rtol=1e-5, atol=1e-5)
