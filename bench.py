@@ -154,22 +154,25 @@ def run_gpu(args):
     n_floor = params.n_floor(Mv)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
-    def layer(qh, kh, vh, out, marks=None):
-        """The four launches of one carved-attention layer on head-major views."""
+    def layer(qh, kh, vh, out, marks=None, h0=0):
+        """The four launches of one carved-attention layer on head-major views; mask
+        buffers are used from local head h0 on (an exchange chunk's slice)."""
         sh, sn = qh.stride(0), qh.stride(1)
+        Hc = qh.shape[0]  # all local heads, or one exchange chunk of them
+        bq, bk, bR = pq[h0:h0 + Hc], pk[h0:h0 + Hc], R[h0:h0 + Hc]
+        bb, bi, bc = bits[h0:h0 + Hc], kv_idx[h0:h0 + Hc], kv_cnt[h0:h0 + Hc]
         if marks: marks[0].record()
-        _native.call("tcb_block_pool", qh.data_ptr(), kh.data_ptr(), 1, sh, sn, Hl, D, M, Mv, Mt,
-                     layout.n_valid, layout.n_cond, pq.data_ptr(), pk.data_ptr(), sptr)
+        _native.call("tcb_block_pool", qh.data_ptr(), kh.data_ptr(), 1, sh, sn, Hc, D, M, Mv, Mt,
+                     layout.n_valid, layout.n_cond, bq.data_ptr(), bk.data_ptr(), sptr)
         if marks: marks[1].record()
-        _native.call("tcb_block_scores", pq.data_ptr(), Mt, pk.data_ptr(), Hl, Mv, Mt, D,
-                     R.data_ptr(), sptr)
+        _native.call("tcb_block_scores", bq.data_ptr(), Mt, bk.data_ptr(), Hc, Mv, Mt, D,
+                     bR.data_ptr(), sptr)
         if marks: marks[2].record()
-        _native.call("tcb_block_select_scores", R.data_ptr(), Hl, Mv, Mt, adja.data_ptr(), words,
-                     n_floor, float(P_CUT), 1, bits.data_ptr(), kv_idx.data_ptr(),
-                     kv_cnt.data_ptr(), sptr)
+        _native.call("tcb_block_select_scores", bR.data_ptr(), Hc, Mv, Mt, adja.data_ptr(), words,
+                     n_floor, float(P_CUT), 1, bb.data_ptr(), bi.data_ptr(), bc.data_ptr(), sptr)
         if marks: marks[3].record()
         _native.call("tcb_carve_fwd", qh.data_ptr(), kh.data_ptr(), vh.data_ptr(), out.data_ptr(), 1,
-                     sh, sn, kv_idx.data_ptr(), kv_cnt.data_ptr(), Hl, D, M, Mv, Mt, layout.n_valid,
+                     sh, sn, bi.data_ptr(), bc.data_ptr(), Hc, D, M, Mv, Mt, layout.n_valid,
                      layout.n_cond, 0.0, work.data_ptr(), sptr)
         if marks: marks[4].record()
         return out
@@ -184,11 +187,32 @@ def run_gpu(args):
 
         oh = torch.empty((Np, Hl, D), dtype=torch.bfloat16, device=dev)
 
-        def step(marks=None):
-            qh, kh, vh = seq_to_head([q, k, v])
-            layer(qh.permute(1, 0, 2), kh.permute(1, 0, 2), vh.permute(1, 0, 2),
-                  oh.permute(1, 0, 2), marks)
-            return head_to_seq(oh)
+        if args.a2a_chunks > 1:
+            from paper_2505_16864_b200.ulysses import carve_layer_sp_chunked
+
+            chunk = [0]
+
+            def local(qh, kh, vh, _lay):
+                out = torch.empty_like(qh)  # same (token-major) strides as the inputs
+                h0 = chunk[0] * qh.shape[0]
+                chunk[0] += 1
+                return layer(qh, kh, vh, out, h0=h0)
+
+            def step(marks=None):
+                chunk[0] = 0
+                if marks:  # per-kernel marks are per chunk here; time the whole layer only
+                    marks[0].record()
+                r = carve_layer_sp_chunked(q, k, v, layout, local, chunks=args.a2a_chunks)
+                if marks:
+                    for mk in marks[1:]:
+                        mk.record()
+                return r
+        else:
+            def step(marks=None):
+                qh, kh, vh = seq_to_head([q, k, v])
+                layer(qh.permute(1, 0, 2), kh.permute(1, 0, 2), vh.permute(1, 0, 2),
+                      oh.permute(1, 0, 2), marks)
+                return head_to_seq(oh)
 
     red_dev = "cpu" if args.dist_backend == "gloo" else dev  # device of the scalar reductions
 
@@ -227,6 +251,10 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
     k_pool, k_rel, k_sel, k_carve = per.mean(axis=0)
+    chunked = world > 1 and args.a2a_chunks > 1
+    if chunked:  # per-kernel marks do not separate the pipelined chunks: use the layer time
+        k_pool = k_rel = k_sel = float("nan")
+        k_carve = ms_step
     flops = 4.0 * M * M * D * pairs
     flops_local = 4.0 * M * M * D * pairs_local
     hbm, tf_burst, tf_sust, peak_src = peaks()
@@ -286,12 +314,13 @@ def run_gpu(args):
         "config": {"workload": WORKLOAD, "tokens": Np, "heads": H, "d": D, "block": M,
                    "k": K_RATE, "p": P_CUT, "kept_pairs": pairs,
                    "kept_fraction": round(pairs / (H * Mt * Mt), 4),
-                   "parallelism": f"ulysses-heads{world}" if world > 1 else "single",
+                   "parallelism": (f"ulysses-heads{world}" + (f"-a2a{args.a2a_chunks}chunks" if chunked else ""))
+                   if world > 1 else "single",
                    "l2": "no flush: Q/K/V/O = 2.9 GB per layer > 126 MB L2"},
         "kept_block_tflops": round(carve_tflops, 1),
-        "kernels_ms": {"block_pool": round(float(k_pool), 4), "block_scores": round(float(k_rel), 4),
-                       "block_softmax_select": round(float(k_sel), 4),
-                       "carve_fwd": round(float(k_carve), 4)},
+        "kernels_ms": None if chunked else {
+            "block_pool": round(float(k_pool), 4), "block_scores": round(float(k_rel), 4),
+            "block_softmax_select": round(float(k_sel), 4), "carve_fwd": round(float(k_carve), 4)},
         "roofline": {"bound": "tensor", "kernel": "k_carve_tc<128>",
                      "achieved": round(carve_tflops, 1), "peak": tf_sust, "unit": "TFLOP/s",
                      "frac": round(carve_tflops / tf_sust, 4),
@@ -299,7 +328,7 @@ def run_gpu(args):
                      "frac_of_burst": round(carve_tflops / tf_burst, 4),
                      "traffic": traffic,
                      "algorithmic_flops_per_launch": flops_local,
-                     "pool_hbm_gbs": round(2 * Hl * Np * D * 2 / (k_pool * 1e-3) / 1e9, 1),
+                     "pool_hbm_gbs": None if chunked else round(2 * Hl * Np * D * 2 / (k_pool * 1e-3) / 1e9, 1),
                      "hbm_peak_gbs": hbm},
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -409,6 +438,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--a2a-chunks", type=int, default=1,
+                    help="N>1: pipeline the Ulysses all-to-all over this many head chunks")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help=argparse.SUPPRESS)
     args = ap.parse_args()

@@ -21,7 +21,7 @@ import torch.distributed as dist
 
 from .partition import BlockLayout
 
-__all__ = ["seq_to_head", "head_to_seq", "carve_layer_sp"]
+__all__ = ["seq_to_head", "head_to_seq", "carve_layer_sp", "carve_layer_sp_chunked"]
 
 
 def _all_to_all(recv: torch.Tensor, send: torch.Tensor, group=None) -> None:
@@ -75,3 +75,65 @@ def carve_layer_sp(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: Bl
     views = [t.permute(1, 0, 2) for t in (qh, kh, vh)]  # (H/G, N, d), stride (d, H/G*d, 1)
     oh = local_fn(*views, layout)
     return head_to_seq(oh.permute(1, 0, 2), group)
+
+
+def _a2a_async(recv: torch.Tensor, send: torch.Tensor, group=None):
+    """Asynchronous all-to-all (NCCL runs it on its own stream; the returned work's
+    ``wait()`` makes the current stream wait).  gloo stages through the host, synchronously."""
+    if recv.is_cuda and dist.get_backend(group) == "gloo":
+        _all_to_all(recv, send, group)
+        return None
+    return dist.all_to_all_single(recv, send, group=group, async_op=True)
+
+
+def carve_layer_sp_chunked(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: BlockLayout,
+                           local_fn: Callable, chunks: int = 2, group=None) -> torch.Tensor:
+    """``carve_layer_sp`` with the exchange pipelined over head chunks: the all-to-all of
+    chunk c+1 (NCCL, async) runs while chunk c is pooled / selected / carved, and chunk c's
+    output all-to-all runs under chunk c+1's compute.  Each rank's H/G heads are split into
+    ``chunks`` groups; chunk c carries heads [c*hc, (c+1)*hc) of every rank's slice.  Carved
+    attention is independent per head, so the result equals the unchunked exchange
+    bitwise."""
+    G = dist.get_world_size(group)
+    n_loc, H, d = q.shape
+    if H % G:
+        raise ValueError(f"heads {H} not divisible by world size {G}")
+    hg = H // G
+    chunks = max(1, min(chunks, hg))
+    if hg % chunks:
+        raise ValueError(f"{hg} heads per rank not divisible into {chunks} chunks")
+    hc = hg // chunks
+
+    def send_of(x, c):  # (G, n_loc, hc, d): for rank r, our tokens of its chunk-c heads
+        return x.view(n_loc, G, hg, d)[:, :, c * hc:(c + 1) * hc].permute(1, 0, 2, 3).contiguous()
+
+    def post_in(c):
+        ins, works = [], []
+        for x in (q, k, v):
+            send = send_of(x, c)
+            recv = torch.empty_like(send)
+            works.append(_a2a_async(recv, send, group))
+            ins.append(recv)
+        return ins, works
+
+    out = torch.empty_like(q)
+    pending = post_in(0)
+    outs = []
+    for c in range(chunks):
+        ins, works = pending
+        if c + 1 < chunks:
+            pending = post_in(c + 1)  # exchange of the next chunk overlaps this compute
+        for w in works:
+            if w is not None:
+                w.wait()
+        views = [t.view(G * n_loc, hc, d).permute(1, 0, 2) for t in ins]  # (hc, N, d)
+        oh = local_fn(*views, layout)  # (hc, N, d) head-major view of a token-major shard
+        send = oh.permute(1, 0, 2).contiguous().view(G, n_loc, hc, d)
+        recv = torch.empty_like(send)
+        outs.append((c, recv, _a2a_async(recv, send, group)))
+    ov = out.view(n_loc, G, hg, d)
+    for c, recv, w in outs:
+        if w is not None:
+            w.wait()
+        ov[:, :, c * hc:(c + 1) * hc] = recv.permute(1, 0, 2, 3)
+    return out

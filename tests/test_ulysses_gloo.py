@@ -31,10 +31,10 @@ def _case():
     return dims, L, q, k, v, adja
 
 
-def _worker(rank, world, port, out_path):
+def _worker(rank, world, port, out_path, chunks=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2505_16864_b200.ulysses import carve_layer_sp
+    from paper_2505_16864_b200.ulysses import carve_layer_sp, carve_layer_sp_chunked
 
     dims, L, q, k, v, adja = _case()
     N = L["padded_total"]
@@ -49,19 +49,23 @@ def _worker(rank, world, port, out_path):
         bits, _ = oracle.block_mask(qn, kn, L, adja, 0.3, 0.3)
         return torch.from_numpy(oracle.carve(qn, kn, vn, bits, L, 0.25))
 
-    o = carve_layer_sp(shard(q), shard(k), shard(v), None, local)
+    if chunks:
+        o = carve_layer_sp_chunked(shard(q), shard(k), shard(v), None, local, chunks=chunks)
+    else:
+        o = carve_layer_sp(shard(q), shard(k), shard(v), None, local)
     torch.save(o, f"{out_path}.{rank}")
     dist.destroy_process_group()
 
 
-def test_ulysses_roundtrip_world2(tmp_path):
+@pytest.mark.parametrize("chunks", [0, 1, 2])
+def test_ulysses_roundtrip_world2(tmp_path, chunks):
     if not dist.is_gloo_available():
         pytest.skip("gloo missing")
     N_pad = _case()[1]["padded_total"]
     assert N_pad % 2 == 0
     port = _free_port()
     out = str(tmp_path / "o")
-    mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, port, out, chunks), nprocs=2, join=True)
     dims, L, q, k, v, adja = _case()
     bits, _ = oracle.block_mask(q, k, L, adja, 0.3, 0.3)
     full = oracle.carve(q, k, v, bits, L, 0.25).transpose(1, 0, 2)  # (N, H, d)
