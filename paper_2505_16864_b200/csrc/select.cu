@@ -677,7 +677,12 @@ __device__ int warp_sorted_cut(uint64_t* skey, int* scol, int cnt, int np2, doub
 // turned into R in place (max, exp, numpy-pairwise sum, divide; masks.py:132-134).
 // Per-warp smem: keys[M_pad] | hist[256] | sbits[words_pad] | leaf[nslots] |
 //                (SORT) skey[max(np2, 544)] | scol[max(np2, 544)]
-template <bool RAW, bool SORT>
+// MODE 0: complete kernel (shared memory for a full-row sort).  MODE 1: slim main pass for
+// the cutoff path -- staging for the register sort only; a row whose cut cannot be decided
+// in the top-512 window (p near the row total, or negative values) is marked kv_cnt = -1
+// and left to MODE 2, which re-runs only the marked rows with the full-sort memory (R has
+// already been turned into probabilities by MODE 1, so MODE 2 runs with RAW = false).
+template <bool RAW, bool SORT, int MODE = 0>
 __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R, int64_t n_rows,
                                                           int M_v, int M_total, int np2,
                                                           const uint32_t* __restrict__ adja,
@@ -699,6 +704,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
   __syncthreads();
   const int64_t row = (int64_t)blockIdx.x * SW_WARPS + warp;
   if (row >= n_rows) return;
+  if (MODE == 2 && kv_cnt[row] != -1) return;
   unsigned char* base = smem + (size_t)warp * per_warp_bytes;
   const int M_pad = (M_total + 1) & ~1;
   uint64_t* keys = reinterpret_cast<uint64_t*>(base);
@@ -708,7 +714,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
   const int words_pad = (words + 1) & ~1;
   double* leaf = reinterpret_cast<double*>(sbits + words_pad);
   uint64_t* skey = reinterpret_cast<uint64_t*>(leaf + nslots);
-  int* scol = reinterpret_cast<int*>(skey + (np2 > 544 ? np2 : 544));
+  int* scol = reinterpret_cast<int*>(skey + (MODE == 1 ? 544 : (np2 > 544 ? np2 : 544)));
   const int i = (int)(row % M_v);
   double* Rr = R + row * M_total;
 
@@ -814,6 +820,10 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
       }
       }
       __syncwarp();
+    }
+    if (MODE == 1 && !done) {  // decided by the MODE 2 pass
+      if (lane == 0) kv_cnt[row] = -1;
+      return;
     }
     if (!done) {  // full sort of the row in shared memory, exact scan
       for (int j = lane; j < M_total; j += 32) { skey[j] = keys[j]; scol[j] = j; }
@@ -1018,15 +1028,21 @@ static int launch_select(double* R, bool raw, int H, int M_v, int M_total, const
   per_warp = (per_warp + 15) & ~size_t(15);
   const size_t smem = per_warp * SW_WARPS;
   const unsigned grid = (unsigned)ceil_div(n_rows, SW_WARPS);
-  auto go = [&](auto kern) -> int {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto go = [&](auto kern, size_t sm) -> int {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "k_select smem: %s", cudaGetErrorString(e));
-    kern<<<grid, SW_WARPS * 32, smem, s>>>(R, n_rows, M_v, M_total, np2, adja, words, n_floor, p,
-                                          with_union, bits, kv_idx, kv_cnt, (int)per_warp, nslots);
+    kern<<<grid, SW_WARPS * 32, sm, s>>>(R, n_rows, M_v, M_total, np2, adja, words, n_floor, p,
+                                         with_union, bits, kv_idx, kv_cnt, (int)(sm / SW_WARPS), nslots);
     return check_launch("k_select");
   };
-  if (raw) return sort ? go(k_select<true, true>) : go(k_select<true, false>);
-  return go(k_select<false, true>);
+  if (raw && !sort) return go(k_select<true, false>, smem);
+  // cutoff path: slim pass (register sort of the top-512 window, ~35 % less shared memory
+  // per warp -> 1.5x the resident warps), then the full-sort pass over the rows it left
+  size_t slim = (size_t)M_pad * 8 + 256 * 4 + (size_t)words_pad * 4 + (size_t)nslots * 8 + 544 * 12;
+  slim = ((slim + 15) & ~size_t(15)) * SW_WARPS;
+  int rc = raw ? go(k_select<true, true, 1>, slim) : go(k_select<false, true, 1>, slim);
+  if (rc) return rc;
+  return go(k_select<false, true, 2>, smem);
 }
 
 extern "C" int tcb_block_select(const double* R, int H, int M_v, int M_total,
