@@ -249,6 +249,45 @@ def fused_records():
     return recs
 
 
+def c1_record():
+    """C1: the reference's CPU-runnable case (8x16x16 + 64 text, H=4, d=64, m=64, fp32, the
+    paper-default k=0.3/p=0.3): fp32 SIMT carve path (the 1e-5 parity path) + mask build."""
+    dims = tcb.GridDims(8, 16, 16)
+    lay = tcb.build_layout(dims, 64, 64)
+    st = tcb.StaticMasks.build(lay, dims, tcb.build_curve(dims))
+    rng = np.random.default_rng(0)
+    q, k, v = (torch.from_numpy(rng.standard_normal((4, lay.padded_total, 64), dtype=np.float32)).cuda()
+               for _ in range(3))
+    prm = tcb.SelectionParams(k=0.3, p=0.3)
+    mask, _ = tcb.build_block_mask(q, k, lay, st, prm)
+    inp = tcb.AttentionInputs(q=q, k=k, v=v, layout=lay)
+    t_mask = timed(lambda: tcb.build_block_mask(q, k, lay, st, prm))
+    t_carve = timed(lambda: tcb.carve_attention(inp, mask))
+    return {"config": "C1 8x16x16 + 64 text, H=4, d=64, m=64, fp32, k=0.3 p=0.3", "mask_ms": round(t_mask, 4),
+            "carve_ms": round(t_carve, 4), "kept_fraction": round(mask.selected_fraction, 4),
+            "note": "tiled fp32 kernel k_carve_f32t (fp32 inputs keep fp32 math for the 1e-5 parity); "
+                    "latency-bound at this size; the reference takes 0.13-0.16 s (SURVEY §6)"}
+
+
+def c2_fp32_record():
+    """C2 with fp32 Q/K/V (the reference's dtype, what a numpy caller gets): fp32-math tiled
+    carve (k_carve_f32t) -- the 1e-5 path at full size."""
+    g = tcb.GridDims(33, 45, 80)
+    lay = tcb.build_layout(g, 128, 256)
+    st = tcb.StaticMasks.build(lay, g, tcb.build_curve(g))
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    q, k, v = (torch.randn((24, lay.padded_total, 128), generator=gen, device="cuda") for _ in range(3))
+    prm = tcb.SelectionParams(k=0.08, p=0.0)
+    mask, _ = tcb.build_block_mask(q, k, lay, st, prm)
+    inp = tcb.AttentionInputs(q=q, k=k, v=v, layout=lay)
+    t_mask = timed(lambda: tcb.build_block_mask(q, k, lay, st, prm), reps=3, warm=1)
+    t_carve = timed(lambda: tcb.carve_attention(inp, mask), reps=3, warm=1)
+    pairs = int(mask.kv_cnt.sum().item()) + 24 * lay.M_c * lay.M_total
+    return {"config": "C2 with fp32 inputs (fp32 math)", "mask_ms": round(t_mask, 3),
+            "carve_ms": round(t_carve, 3), "layer_ms": round(t_mask + t_carve, 3),
+            "fp32_tflops": round(4.0 * 128 ** 3 * pairs / (t_carve * 1e-3) / 1e12, 1)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
@@ -256,6 +295,8 @@ def main():
     a = ap.parse_args()
     res = {"device": torch.cuda.get_device_name(0), "hbm": hbm_records(), "c4_stage_switch": c4_records(),
            "fused_f1": fused_records()}
+    res["c1"] = c1_record()
+    res["c2_fp32"] = c2_fp32_record()
     res["c3"] = layer_record("C3 Wan2.1-14B 480p 21x30x52, H=40, no text", (21, 30, 52), 0, 40, 0.08)
     res["c2"] = layer_record("C2 HunyuanVideo 720p 33x45x80 + 256 text, H=24", (33, 45, 80), 256, 24, 0.08)
     # C4: the two stages of the stock 2-stage plan at 720p (cli.default_stage_plan: stage 1

@@ -160,6 +160,140 @@ __global__ void __launch_bounds__(128) k_carve_simt(const T* __restrict__ q,
 }
 
 // =====================================================================================
+// Tiled fp32 kernel (the reference's dtype at real sizes).  CTA = one (head, q-block) item,
+// 256 threads as a 16 x 16 grid; thread (ty, tx) owns query rows ty + 16 i and key / value
+// columns tx + 16 j, i.e. an (MT x MT) tile of S and an (MT x DT) tile of O in registers
+// (m = 16 MT, d = 16 DT).  Per kv block, in the reference's order (attention.py:184-201):
+// S = (q * scale) K^T from shared-memory tiles (fp32 FMA), padding keys -> -inf, +beta on
+// condition keys of vision rows, block row max (shuffles across the 16 threads of a row),
+// alpha = exp(m - m_new), p = exp(s - m_new), l = l * alpha + sum p, O = O * alpha + P V
+// with P staged through shared memory.  expf (not ex2.approx) and fp32 accumulation keep
+// it within the north_star's 1e-5 of the reference; only the summation order of the
+// length-d / length-m dot products differs.
+// =====================================================================================
+template <typename T, int MT, int DT>
+__global__ void __launch_bounds__(256, 1) k_carve_f32t(const T* __restrict__ q, const T* __restrict__ k,
+                                                       const T* __restrict__ v, T* __restrict__ o,
+                                                       CarveShape s, const int32_t* __restrict__ kv_idx,
+                                                       const int32_t* __restrict__ kv_cnt, float beta,
+                                                       float scale) {
+  constexpr int M = 16 * MT, D = 16 * DT;
+  constexpr int QP = D + 1;   // padded row pitch (floats) of Q / K / V tiles
+  constexpr int PP = M + 1;   // padded row pitch of P
+  extern __shared__ float sm_f32t[];
+  float* sQ = sm_f32t;
+  float* sK = sQ + M * QP;
+  float* sV = sK + M * QP;
+  float* sP = (M * PP <= M * QP) ? sK : sV + M * QP;  // P reuses K's tile when it fits
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int h = blockIdx.x / s.M_total;
+  const int qb = blockIdx.x - h * s.M_total;
+  const bool vis = qb < s.M_v;
+  const int nkv = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
+  const int32_t* list = vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr;
+  const int qvalid = block_valid(qb, M, s.M_v, s.n_valid, s.n_cond);
+  const T* qh = q + (int64_t)h * s.sh;
+  const T* kh = k + (int64_t)h * s.sh;
+  const T* vh = v + (int64_t)h * s.sh;
+  for (int e = tid; e < M * D; e += 256) {  // q pre-scaled in fp32 (attention.py:184)
+    const int r = e / D, c = e - r * D;
+    sQ[r * QP + c] = ldf(qh + ((int64_t)qb * M + r) * s.sn + c) * scale;
+  }
+  float acc[MT][DT], mrow[MT], lrow[MT];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    mrow[i] = -INFINITY;
+    lrow[i] = 0.f;
+#pragma unroll
+    for (int j = 0; j < DT; ++j) acc[i][j] = 0.f;
+  }
+  for (int t = 0; t < nkv; ++t) {
+    const int b = vis ? __ldg(list + t) : t;
+    const int kvalid = block_valid(b, M, s.M_v, s.n_valid, s.n_cond);
+    const bool add_beta = vis && beta != 0.f && b >= s.M_v;
+    __syncthreads();  // previous block's P / V reads done
+    for (int e = tid; e < M * D; e += 256) {
+      const int r = e / D, c = e - r * D;
+      const int64_t g = ((int64_t)b * M + r) * s.sn + c;
+      sK[r * QP + c] = ldf(kh + g);
+      sV[r * QP + c] = ldf(vh + g);
+    }
+    __syncthreads();
+    float sc[MT][MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < MT; ++j) sc[i][j] = 0.f;
+#pragma unroll 4
+    for (int c = 0; c < D; ++c) {
+      float a[MT], bk[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) a[i] = sQ[(ty + 16 * i) * QP + c];
+#pragma unroll
+      for (int j = 0; j < MT; ++j) bk[j] = sK[(tx + 16 * j) * QP + c];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < MT; ++j) sc[i][j] = fmaf(a[i], bk[j], sc[i][j]);
+    }
+    __syncthreads();  // K tile consumed (P may overwrite it)
+    float alpha[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      float bm = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < MT; ++j) {
+        float x = (tx + 16 * j < kvalid) ? sc[i][j] : -INFINITY;  // attention.py:193
+        if (add_beta) x = x + beta;
+        sc[i][j] = x;
+        bm = fmaxf(bm, x);
+      }
+#pragma unroll
+      for (int off = 8; off > 0; off >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, off));
+      const float mn = fmaxf(mrow[i], bm);
+      alpha[i] = expf(mrow[i] - mn);
+      float ps = 0.f;
+#pragma unroll
+      for (int j = 0; j < MT; ++j) {
+        const float pj = expf(sc[i][j] - mn);
+        sP[(ty + 16 * i) * PP + tx + 16 * j] = pj;
+        ps += pj;
+      }
+#pragma unroll
+      for (int off = 8; off > 0; off >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+      lrow[i] = lrow[i] * alpha[i] + ps;
+      mrow[i] = mn;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < DT; ++j) acc[i][j] *= alpha[i];
+#pragma unroll 4
+    for (int jk = 0; jk < M; ++jk) {
+      float pr[MT], vv[DT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) pr[i] = sP[(ty + 16 * i) * PP + jk];
+#pragma unroll
+      for (int j = 0; j < DT; ++j) vv[j] = sV[jk * QP + tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < DT; ++j) acc[i][j] = fmaf(pr[i], vv[j], acc[i][j]);
+    }
+  }
+  T* oh = o + (int64_t)h * s.sh;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int r = ty + 16 * i;
+    T* orow = oh + ((int64_t)qb * M + r) * s.sn;
+#pragma unroll
+    for (int j = 0; j < DT; ++j)
+      orow[tx + 16 * j] = stf<T>(r < qvalid ? acc[i][j] / lrow[i] : 0.f);  // attention.py:203-206
+  }
+}
+
+// =====================================================================================
 // tcgen05 kernel
 // =====================================================================================
 namespace tc {
@@ -657,9 +791,50 @@ static int validate(const void* q, const void* k, const void* v, void* o, int dt
 
 using namespace tcb;
 
+template <typename T, int MT, int DT>
+static int launch_f32t(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
+                       const int32_t* kv_idx, const int32_t* kv_cnt, float beta, cudaStream_t st) {
+  constexpr int M = 16 * MT, D = 16 * DT;
+  size_t smem = (size_t)3 * M * (D + 1) * sizeof(float);
+  if (M * (M + 1) > M * (D + 1)) smem += (size_t)M * (M + 1) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_carve_f32t<T, MT, DT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_error(TCB_ECUDA, "f32t smem: %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  const float scale = (float)(1.0 / sqrt((double)s.d));
+  k_carve_f32t<T, MT, DT><<<(unsigned)((int64_t)s.H * s.M_total), 256, smem, st>>>(
+      (const T*)q, (const T*)k, (const T*)v, (T*)o, s, kv_idx, kv_cnt, beta, scale);
+  return check_launch("k_carve_f32t");
+}
+
+template <typename T>
+static int try_f32t(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
+                    const int32_t* kv_idx, const int32_t* kv_cnt, float beta, cudaStream_t st) {
+  const int key = (s.m << 16) | s.d;
+  switch (key) {
+    case (128 << 16) | 128: return launch_f32t<T, 8, 8>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    case (128 << 16) | 64: return launch_f32t<T, 8, 4>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    case (64 << 16) | 128: return launch_f32t<T, 4, 8>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    case (64 << 16) | 64: return launch_f32t<T, 4, 4>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    case (64 << 16) | 32: return launch_f32t<T, 4, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    case (32 << 16) | 64: return launch_f32t<T, 2, 4>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    case (32 << 16) | 32: return launch_f32t<T, 2, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    case (16 << 16) | 16: return launch_f32t<T, 1, 1>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    default: return -1;  // not tiled: the per-row kernel takes it
+  }
+}
+
 static int launch_simt(const void* q, const void* k, const void* v, void* o, int dtype,
                        const CarveShape& s, const int32_t* kv_idx, const int32_t* kv_cnt,
                        float beta, cudaStream_t st) {
+  {  // tiled fp32-math kernel for the common block / head sizes
+    const int rc = dtype == TCB_F32 ? try_f32t<float>(q, k, v, o, s, kv_idx, kv_cnt, beta, st)
+                                    : try_f32t<__nv_bfloat16>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    if (rc != -1) return rc;
+  }
   TCB_CHECK_ARG(s.d <= 32 * SIMT_MAXC, TCB_ESIZE, "SIMT carve supports d <= %d", 32 * SIMT_MAXC);
   const size_t smem = (size_t)4 * (s.m + s.d) * sizeof(float);
   const float scale = (float)(1.0 / sqrt((double)s.d));
