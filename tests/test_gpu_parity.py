@@ -396,3 +396,49 @@ def test_carve_bf16_fuzz_random_layouts():
         o32 = tcb.carve_attention(tcb.AttentionInputs(q=q32, k=k32, v=v32, layout=lay),
                                   tcb.BlockMask(bits=bits), tcb.AmplifierBias(beta))
         np.testing.assert_allclose(o32, ref, rtol=1e-5, atol=1e-5)
+
+
+# ----------------------------------------------------------------- reference acceptance
+def _random_instance(rng, max_tokens=512):
+    """The reference's random_instance (test_acceptance.py:64-77) generator."""
+    while True:
+        m = int(rng.choice([4, 8, 16, 32]))
+        dims = tcb.GridDims(*(int(x) for x in rng.integers(1, 7, size=3)))
+        n_cond = int(rng.choice([0, 1, m // 2, m, m + 3]))
+        lay = tcb.build_layout(dims, m, n_cond)
+        if lay.padded_total <= max_tokens:
+            break
+    H = int(rng.integers(1, 5))
+    d = int(rng.choice([4, 8, 16, 64]))
+    q, k, v = (rng.standard_normal((H, lay.padded_total, d)).astype(np.float32) for _ in range(3))
+    return dims, lay, q, k, v
+
+
+def test_acceptance_02_full_mask_equals_dense():
+    # criterion 02 (test_acceptance.py:127-146): carve == dense on all-true masks, 100 instances
+    rng = np.random.default_rng(20240202)
+    worst = 0.0
+    for _ in range(100):
+        dims, lay, q, k, v = _random_instance(rng)
+        bits = np.ones((q.shape[0], lay.M_v, lay.M_total), bool)
+        got = tcb.carve_attention(tcb.AttentionInputs(q=q, k=k, v=v, layout=lay), tcb.BlockMask(bits=bits))
+        L = oracle.layout_scalars(dims.as_tuple(), lay.m, lay.n_cond)
+        want = oracle.dense_reference(q, k, v, None, oracle.token_valid(L))
+        worst = max(worst, float(np.abs(got - want).max()))
+    assert worst <= 1e-5, worst
+
+
+def test_acceptance_03_masked_equals_dense_with_bias():
+    # criterion 03 (test_acceptance.py:149-167): carve == -inf-logit dense oracle, 100 pairs
+    rng = np.random.default_rng(30303)
+    worst = 0.0
+    for _ in range(100):
+        dims, lay, q, k, v = _random_instance(rng, max_tokens=256)
+        bits = rng.random((q.shape[0], lay.M_v, lay.M_total)) < rng.uniform(0.2, 0.9)
+        idx = np.arange(lay.M_v)
+        bits[:, idx, idx] = True
+        got = tcb.carve_attention(tcb.AttentionInputs(q=q, k=k, v=v, layout=lay), tcb.BlockMask(bits=bits))
+        L = oracle.layout_scalars(dims.as_tuple(), lay.m, lay.n_cond)
+        want = oracle.dense_reference(q, k, v, oracle.mask_to_bias(bits, L), oracle.token_valid(L))
+        worst = max(worst, float(np.abs(got - want).max()))
+    assert worst <= 1e-5, worst
