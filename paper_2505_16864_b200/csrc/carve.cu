@@ -822,6 +822,9 @@ static int try_f32t(const void* q, const void* k, const void* v, void* o, const 
     case (64 << 16) | 32: return launch_f32t<T, 4, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
     case (32 << 16) | 64: return launch_f32t<T, 2, 4>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
     case (32 << 16) | 32: return launch_f32t<T, 2, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    case (128 << 16) | 32: return launch_f32t<T, 8, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    case (128 << 16) | 16: return launch_f32t<T, 8, 1>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    case (64 << 16) | 16: return launch_f32t<T, 4, 1>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
     case (16 << 16) | 16: return launch_f32t<T, 1, 1>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
     default: return -1;  // not tiled: the per-row kernel takes it
   }
