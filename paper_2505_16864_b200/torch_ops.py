@@ -1,0 +1,75 @@
+"""PyTorch operator registration of the path (``torch.ops.tokencarve.*``).
+
+A PyTorch DiT calls carved attention inside its own (possibly ``torch.compile``-d) forward;
+registering the C-ABI launches as custom operators with fake (meta) implementations makes
+them opaque graph nodes with known output shapes, so the surrounding model can be traced
+without breaking the graph at every layer.  The ops launch the same sm_100a kernels on the
+current stream as the ``tokencarve``-API functions:
+
+* ``tokencarve::block_mask(q, k, adja_bits, m, M_v, M_total, n_valid, n_cond, n_floor, p)``
+  -> (words, kv_idx, kv_cnt): pool -> scores -> select/union (masks.py:178-199);
+* ``tokencarve::carve(q, k, v, kv_idx, kv_cnt, m, M_v, M_total, n_valid, n_cond, beta)``
+  -> out: block-sparse attention (attention.py:209-243).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _dev, _native
+from .attention import _workspace
+from .partition import mask_words
+
+__all__ = ["block_mask", "carve"]
+
+
+@torch.library.custom_op("tokencarve::block_mask", mutates_args=())
+def block_mask(q: torch.Tensor, k: torch.Tensor, adja_bits: torch.Tensor, m: int, M_v: int,
+               M_total: int, n_valid: int, n_cond: int, n_floor: int,
+               p: float) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    H, _, d = q.shape
+    dev = q.device
+    s = torch.cuda.current_stream(dev).cuda_stream
+    pq = torch.empty((H, M_total, d), dtype=torch.float64, device=dev)
+    pk = torch.empty_like(pq)
+    R = torch.empty((H, M_v, M_total), dtype=torch.float64, device=dev)
+    words = mask_words(M_total)
+    bits = torch.empty((H, M_v, words), dtype=torch.int32, device=dev)
+    kv_idx = torch.empty((H, M_v, M_total), dtype=torch.int32, device=dev)
+    kv_cnt = torch.empty((H, M_v), dtype=torch.int32, device=dev)
+    _native.call("tcb_block_pool", q.data_ptr(), k.data_ptr(), _dev.code_of(q.dtype), q.stride(0),
+                 q.stride(1), H, d, m, M_v, M_total, n_valid, n_cond, pq.data_ptr(), pk.data_ptr(), s)
+    _native.call("tcb_block_scores", pq.data_ptr(), M_total, pk.data_ptr(), H, M_v, M_total, d,
+                 R.data_ptr(), s)
+    _native.call("tcb_block_select_scores", R.data_ptr(), H, M_v, M_total, adja_bits.data_ptr(),
+                 words, n_floor, float(p), 1, bits.data_ptr(), kv_idx.data_ptr(), kv_cnt.data_ptr(), s)
+    return bits, kv_idx, kv_cnt
+
+
+@block_mask.register_fake
+def _(q, k, adja_bits, m, M_v, M_total, n_valid, n_cond, n_floor, p):
+    H = q.shape[0]
+    words = mask_words(M_total)
+    return (q.new_empty((H, M_v, words), dtype=torch.int32),
+            q.new_empty((H, M_v, M_total), dtype=torch.int32),
+            q.new_empty((H, M_v), dtype=torch.int32))
+
+
+@torch.library.custom_op("tokencarve::carve", mutates_args=())
+def carve(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, kv_idx: torch.Tensor,
+          kv_cnt: torch.Tensor, m: int, M_v: int, M_total: int, n_valid: int, n_cond: int,
+          beta: float) -> torch.Tensor:
+    if k.stride() != q.stride() or v.stride() != q.stride() or q.stride(2) != 1:
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    out = torch.empty_like(q)
+    H, _, d = q.shape
+    _native.call("tcb_carve_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                 _dev.code_of(q.dtype), q.stride(0), q.stride(1), kv_idx.data_ptr(),
+                 kv_cnt.data_ptr(), H, d, m, M_v, M_total, n_valid, n_cond, float(beta),
+                 _workspace(q.device).data_ptr(), torch.cuda.current_stream(q.device).cuda_stream)
+    return out
+
+
+@carve.register_fake
+def _(q, k, v, kv_idx, kv_cnt, m, M_v, M_total, n_valid, n_cond, beta):
+    return torch.empty_like(q)

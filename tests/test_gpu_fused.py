@@ -115,3 +115,37 @@ def test_curve_positions_match_reference_loop_fixture():
         assert np.array_equal(pos, g[key])
     big = fused.curve_positions(tcb.build_curve(tcb.GridDims(33, 45, 80))).cpu().numpy()
     assert np.array_equal(big[:64], g["c2_head"])
+
+
+def test_torch_ops_eager_and_compiled_match_api():
+    # torch.ops.tokencarve.* (opaque custom ops with fake impls) inside a compiled model
+    # function give the same bits as the API calls
+    from paper_2505_16864_b200 import torch_ops  # noqa: F401
+
+    dims = tcb.GridDims(3, 16, 24)
+    lay = tcb.build_layout(dims, 128, 40)
+    st = tcb.StaticMasks.build(lay, dims, tcb.build_curve(dims))
+    prm = tcb.SelectionParams(k=0.3, p=0.0)
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    x = torch.randn((lay.padded_total, 64), generator=gen, device="cuda")
+    w = torch.randn((3, 64, 2 * 128), generator=gen, device="cuda") * 0.1
+    adja = st.packed(lay)
+    args = (lay.m, lay.M_v, lay.M_total, lay.n_valid, lay.n_cond)
+
+    def layer(x):
+        q, k, v = (torch.einsum("nf,fhd->hnd", x, w[i].view(64, 2, 128)).to(torch.bfloat16).contiguous()
+                   for i in range(3))
+        bits, kv_idx, kv_cnt = torch.ops.tokencarve.block_mask(q, k, adja, *args, prm.n_floor(lay.M_v), 0.0)
+        o = torch.ops.tokencarve.carve(q, k, v, kv_idx, kv_cnt, *args, 0.0)
+        return o.float().sum(dim=0), bits
+
+    eager, bits = layer(x)
+    # aot_eager traces the whole function through the fake impls (fullgraph: no graph
+    # breaks at the custom ops) without inductor codegen, which takes minutes cold
+    compiled, bits_c = torch.compile(layer, fullgraph=True, backend="aot_eager")(x)
+    assert torch.equal(bits, bits_c)
+    torch.testing.assert_close(compiled, eager, rtol=2e-2, atol=2e-2)
+    q = torch.einsum("nf,fhd->hnd", x, w[0].view(64, 2, 128)).to(torch.bfloat16).contiguous()
+    k = torch.einsum("nf,fhd->hnd", x, w[1].view(64, 2, 128)).to(torch.bfloat16).contiguous()
+    m_api, _ = tcb.build_block_mask(q, k, lay, st, prm)
+    assert torch.equal(m_api.words, bits)
