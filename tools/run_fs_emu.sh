@@ -1,0 +1,4 @@
+# full-step kernel with FMA-pipe exp2 shares: cycles / clock / time under ncu
+for emu in 0 2 3 4; do
+  TCB_CARVE_IMPL=2 TCB_CARVE_EMU=$emu timeout 300 ncu --metrics gpu__time_duration.sum,sm__cycles_elapsed.avg,gpc__cycles_elapsed.avg.per_second,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed --clock-control none -k "regex:k_carve" -s 3 -c 1 python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e 2>&1 | grep -E "gpu__|sm__|gpc__" | sed "s/^/emu=$emu /"
+done
