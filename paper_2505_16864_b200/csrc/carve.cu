@@ -738,335 +738,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
 
 }  // namespace tc
 
-// =====================================================================================
-// tcgen05 kernel, full-block steps ("fs").  Same roles as k_carve_tc, but each step is a
-// whole 128-key block: S = Q K^T with N = 128 (Q read from shared memory once per block
-// instead of once per 64-key half: 160 instead of 192 KB of shared-memory traffic per
-// kept pair), single S buffer (TMEM per CTA: S [0,128), O [128, 256)), so within a CTA
-// the chain is QK(t) -> softmax(t) -> PV(t), QK(t+1) (issued back to back; the tensor
-// pipe runs them in order) and the two CTAs of an SM fill each other's softmax gaps.
-// The softmax reads S from TMEM twice (row max, then exp2 / pack) to keep 32 scores in
-// registers at a time; P(t) goes over S columns [0, 64) as bf16.  K and V stream through
-// one full-tile slot each (Q 32 + K 32 + V 32 KB per CTA).
-// =====================================================================================
-namespace fs {
-
-using tc::BM;
-using tc::BK;
-using tc::NUM_THREADS;
-using tc::RESCALE_THRESHOLD;
-constexpr int TMEM_COLS = 256;
-constexpr int S_COL = 0;
-constexpr int O_COL = 128;
-
-template <int D>
-struct Smem {
-  static constexpr int TILE = BM * D * 2;   // 128 x D bf16
-  static constexpr int CHUNKS = D / 64;
-  static constexpr int CHUNK = BM * 128;    // bytes per 64-column chunk of a tile
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + TILE;
-  static constexpr int OFF_V = OFF_K + TILE;
-  static constexpr int OFF_BAR = OFF_V + TILE;
-  static constexpr int BYTES = OFF_BAR + 256;
-};
-
-struct Bars {
-  uint64_t q_full, q_empty, k_full, k_empty, v_full, v_empty, s_full, p_full, o_full;
-  uint64_t sched_full[2], sched_empty[2];
-  int sched_item[2];
-  uint32_t tmem_base;
-};
-
-template <int D, int EMU>
-__global__ void __launch_bounds__(NUM_THREADS, 2)
-    k_carve_fs(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
-               CarveShape s, const int32_t* __restrict__ kv_idx,
-               const int32_t* __restrict__ kv_cnt, int* __restrict__ counter, int total_items,
-               float scale_log2, float beta_log2) {
-  using L = Smem<D>;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sQ = smem + L::OFF_Q;
-  uint8_t* sK = smem + L::OFF_K;
-  uint8_t* sV = smem + L::OFF_V;
-  Bars* bars = reinterpret_cast<Bars*>(smem + L::OFF_BAR);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    if (ptx::smem_u32(smem) & 1023u) __trap();
-    ptx::mbar_init(&bars->q_full, 1);
-    ptx::mbar_init(&bars->q_empty, 1);
-    ptx::mbar_init(&bars->k_full, 1);
-    ptx::mbar_init(&bars->k_empty, 1);
-    ptx::mbar_init(&bars->v_full, 1);
-    ptx::mbar_init(&bars->v_empty, 1);
-    ptx::mbar_init(&bars->s_full, 1);
-    ptx::mbar_init(&bars->p_full, 128);
-    ptx::mbar_init(&bars->o_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&bars->sched_full[i], 1);
-      ptx::mbar_init(&bars->sched_empty[i], 1 + 4);
-    }
-    ptx::fence_mbar_init();
-    ptx::tma_prefetch_desc(&tm_q);
-    ptx::tma_prefetch_desc(&tm_k);
-    ptx::tma_prefetch_desc(&tm_v);
-  }
-  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(&bars->tmem_base);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
-
-  if (warp == 0) {
-    // ============================ TMA producer + scheduler ============================
-    const uint64_t pol_kv = ptx::policy_evict_last();
-    const uint64_t pol_q = ptx::policy_evict_first();
-    uint32_t it = 0, gk = 0, gv = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      int item = 0;
-      if (lane == 0) {
-        ptx::mbar_wait(&bars->sched_empty[slot], ((it >> 1) & 1) ^ 1);
-        item = atomicAdd(counter, 1);
-        if (item >= total_items) item = -1;
-        bars->sched_item[slot] = item;
-        ptx::mbar_arrive(&bars->sched_full[slot]);
-      }
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      if (lane == 0) {
-        ptx::mbar_wait(&bars->q_empty, (it & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&bars->q_full, L::TILE);
-#pragma unroll
-        for (int c = 0; c < L::CHUNKS; ++c)
-          ptx::tma_load_3d(sQ + c * L::CHUNK, &tm_q, &bars->q_full, c * 64, qb * BM, h, pol_q);
-      }
-      auto load = [&](const CUtensorMap* tm, uint8_t* base, uint64_t* full, uint64_t* empty,
-                      uint32_t& cnt, int t) {
-        const int b = kl.block(t);
-        if (lane == 0) {
-          ptx::mbar_wait(empty, (cnt & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(full, L::TILE);
-#pragma unroll
-          for (int c = 0; c < L::CHUNKS; ++c)
-            ptx::tma_load_3d(base + c * L::CHUNK, tm, full, c * 64, b * BK, h,
-                             vis ? pol_kv : pol_q);
-        }
-        ++cnt;
-      };
-      for (int t = 0; t < n; ++t) {  // consumption order: K0 V0 K1 V1 ...
-        load(&tm_k, sK, &bars->k_full, &bars->k_empty, gk, t);
-        load(&tm_v, sV, &bars->v_full, &bars->v_empty, gv, t);
-      }
-    }
-  } else if (warp == 1) {
-    // ============================ MMA issuer (whole warp, one elected lane) ==============
-    constexpr uint32_t IDESC_S = tc::make_idesc(BM, BK, 0);  // Q (K-major) x K (K-major), N=128
-    constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, 1);   // P (TMEM) x V (MN-major)
-    const uint32_t aQ = ptx::smem_u32(sQ), aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
-    uint32_t it = 0, gk = 0, gv = 0, gp = 0;
-    auto issue_s = [&]() {
-      ptx::mbar_wait(&bars->k_full, gk & 1);
-      ptx::tc_fence_after();
-      if (ptx::elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * L::CHUNK + (kk & 3) * 32;
-          ptx::mma_ss(tmem + S_COL, tc::make_sdesc(aQ + off, 16, 1024),
-                      tc::make_sdesc(aK + off, 16, 1024), IDESC_S, kk > 0 ? 1u : 0u);
-        }
-        ptx::mma_commit(&bars->k_empty);
-        ptx::mma_commit(&bars->s_full);
-      }
-      __syncwarp();
-      ++gk;
-    };
-    for (;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
-      const int item = bars->sched_item[slot];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      ptx::mbar_wait(&bars->q_full, it & 1);
-      if (n == 0) {
-        if (ptx::elect_one()) {
-          ptx::mma_commit(&bars->q_empty);
-          ptx::mma_commit(&bars->o_full);
-        }
-        __syncwarp();
-        continue;
-      }
-      issue_s();
-      for (int t = 0; t < n; ++t) {
-        ptx::mbar_wait(&bars->p_full, gp & 1);
-        ptx::mbar_wait(&bars->v_full, gv & 1);
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            ptx::mma_ts(tmem + O_COL, tmem + S_COL + kk * 8,
-                        tc::make_sdesc(aV + kk * 16 * 128, L::CHUNK, 1024), IDESC_O,
-                        (t > 0 || kk > 0) ? 1u : 0u);
-          ptx::mma_commit(&bars->v_empty);
-          if (t + 1 == n) ptx::mma_commit(&bars->q_empty);
-        }
-        __syncwarp();
-        ++gv;
-        ++gp;
-        if (t + 1 < n) issue_s();  // in order behind PV(t): overwrites P(t) after it is read
-      }
-      if (ptx::elect_one()) ptx::mma_commit(&bars->o_full);
-      __syncwarp();
-    }
-  } else {
-    // ============================ softmax / correction / epilogue ============================
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
-    uint32_t it = 0, g = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
-      const int item = bars->sched_item[slot];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      float m_run = -INFINITY, l_run = 0.f;
-      for (int t = 0; t < n; ++t, ++g) {
-        const int b = kl.block(t);
-        const int kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond);
-        const float bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
-        ptx::mbar_wait(&bars->s_full, g & 1);
-        ptx::tc_fence_after();
-        // pass 1: row max over the 128 keys (32 scores in registers at a time)
-        float mx = -INFINITY;
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t sr[32];
-          ptx::tmem_ld32(t_row + S_COL + c * 32, sr);
-          ptx::tmem_wait_ld();
-          if (kvalid < BK) {  // padding keys of a partial block -> -inf (attention.py:193)
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (c * 32 + e >= kvalid) sr[e] = __float_as_uint(-INFINITY);
-          }
-          float m8[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) m8[e] = __uint_as_float(sr[e]);
-#pragma unroll
-          for (int e = 8; e < 32; e += 16)
-#pragma unroll
-            for (int qq = 0; qq < 8; ++qq)
-              m8[qq] = tc::fmax3(m8[qq], __uint_as_float(sr[e + qq]), __uint_as_float(sr[e + 8 + qq]));
-          mx = tc::fmax3(mx, tc::fmax3(m8[0], m8[1], m8[2]), tc::fmax3(m8[3], m8[4], tc::fmax3(m8[5], m8[6], m8[7])));
-        }
-        const float m_blk = (mx == -INFINITY) ? -INFINITY : fmaf(mx, scale_log2, bias);
-        const float m_new = fmaxf(m_run, m_blk);
-        const bool first = (t == 0);
-        const bool need = !first && (m_new > m_run + RESCALE_THRESHOLD);
-        const float m_use = (first || need) ? m_new : m_run;
-        const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
-        const float c0 = bias - m_use;
-        const uint64_t sc2 = tc::f2_pack(scale_log2, scale_log2), c02 = tc::f2_pack(c0, c0);
-        uint64_t acc2[4] = {0, 0, 0, 0};
-        // pass 2: p = 2^(s * scale_log2 + bias - m) in 32-key chunks; P chunk c (16 packed
-        // columns) lands on S columns [16c, 16c + 16), already consumed
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t sr[32];
-          ptx::tmem_ld32(t_row + S_COL + c * 32, sr);
-          ptx::tmem_wait_ld();
-          if (kvalid < BK) {
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (c * 32 + e >= kvalid) sr[e] = __float_as_uint(-INFINITY);
-          }
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const uint64_t x = tc::ffma2(tc::f2_pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])),
-                                         sc2, c02);
-            float p0, p1;
-            if ((e & 7) >= 8 - EMU) {  // FMA-pipe exp2 for EMU of every 8 pairs
-              const uint64_t pp = tc::exp2_poly2(x);
-              p0 = tc::f2_lo(pp);
-              p1 = tc::f2_hi(pp);
-            } else {
-              p0 = ptx::ex2(tc::f2_lo(x));
-              p1 = ptx::ex2(tc::f2_hi(x));
-            }
-            acc2[e & 3] = tc::fadd2(acc2[e & 3], tc::f2_pack(p0, p1));
-            pk[e] = ptx::pack_bf16(p0, p1);
-          }
-          ptx::tmem_st16(t_row + S_COL + c * 16, pk);
-        }
-        const uint64_t sum2 = tc::fadd2(tc::fadd2(acc2[0], acc2[1]), tc::fadd2(acc2[2], acc2[3]));
-        l_run = l_run * alpha + (tc::f2_lo(sum2) + tc::f2_hi(sum2));
-        m_run = m_use;
-        if (__any_sync(0xffffffffu, need)) {  // O holds PV(t-1): covered by the s_full commit
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            ptx::tmem_ld32(t_row + O_COL + c * 32, ov);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            ptx::tmem_st32(t_row + O_COL + c * 32, ov);
-          }
-        }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars->p_full);
-      }
-      ptx::mbar_wait(&bars->o_full, it & 1);
-      ptx::tc_fence_after();
-      const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
-      const float inv_l = (row < qvalid) ? 1.f / l_run : 0.f;
-      __nv_bfloat16* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t ov[32];
-        ptx::tmem_ld32(t_row + O_COL + c * 32, ov);
-        ptx::tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pk[e] = ptx::pack_bf16(__uint_as_float(ov[2 * e]) * inv_l, __uint_as_float(ov[2 * e + 1]) * inv_l);
-        int4* dst = reinterpret_cast<int4*>(orow + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          __stcs(dst + e, make_int4((int)pk[4 * e], (int)pk[4 * e + 1], (int)pk[4 * e + 2], (int)pk[4 * e + 3]));
-      }
-      ptx::tc_fence_before();
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<TMEM_COLS>(tmem);
-  }
-}
-
-}  // namespace fs
 
 
 
@@ -1239,39 +910,6 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
 
 
 
-template <int D, int EMU>
-static int launch_fs(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                     const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
-                     cudaStream_t st) {
-  CUtensorMap tq, tk, tv;
-  const int64_t n_pad = (int64_t)s.M_total * s.m;
-  int rc;
-  if ((rc = make_tmap(&tq, q, D, n_pad, s.H, s.sh, s.sn, tc::BM))) return rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::BK))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::BK))) return rc;
-  const int smem = fs::Smem<D>::BYTES;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fs::k_carve_fs<D, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         smem);
-    if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve fs smem attr: %s", cudaGetErrorString(e));
-    attr_set = true;
-  }
-  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
-  if (e != cudaSuccess) return set_error(TCB_ECUDA, "memset counter: %s", cudaGetErrorString(e));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int total = s.H * s.M_total;
-  int grid = 2 * sms;
-  if (grid > total) grid = total;
-  const float LOG2E = 1.4426950408889634f;
-  const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  fs::k_carve_fs<D, EMU><<<grid, tc::NUM_THREADS, smem, st>>>(tq, tk, tv, (__nv_bfloat16*)o, s, kv_idx,
-                                                       kv_cnt, work, total, scale_log2, beta * LOG2E);
-  return check_launch("k_carve_fs");
-}
-
 extern "C" int tcb_carve_fwd_simt(const void* q, const void* k, const void* v, void* o, int dtype,
                                   int64_t stride_h, int64_t stride_n, const int32_t* kv_idx,
                                   const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
@@ -1304,22 +942,6 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
     if (emu != 0 && emu != 2 && emu != 3 && emu != 4) emu = 0;
   }
   cudaStream_t st = as_stream(stream);
-  static int impl = -1;  // TCB_CARVE_IMPL=2: full-block-step kernel (A/B)
-  if (impl < 0) {
-    const char* env = getenv("TCB_CARVE_IMPL");
-    impl = env ? atoi(env) : 0;
-  }
-  if (impl == 2) {
-    if (d == 128) {
-      switch (emu) {
-        case 2: return launch_fs<128, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-        case 3: return launch_fs<128, 3>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-        case 4: return launch_fs<128, 4>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-        default: return launch_fs<128, 0>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-      }
-    }
-    return launch_fs<64, 0>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-  }
   if (d == 128) {
     switch (emu) {
       case 3: return launch_tc<128, 3>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
