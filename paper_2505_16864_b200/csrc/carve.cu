@@ -738,355 +738,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
 
 }  // namespace tc
 
-// =====================================================================================
-// tcgen05 kernel, one CTA per SM with Q in TMEM and 8 softmax warps ("w8").
-// TMEM (512 columns): Q [0,64) packed bf16 (TS-form QK^T: the tensor core reads only K and
-// V from shared memory), S0 [64,192) and S1 [192,320) full 128-key score buffers (QK(t+1)
-// runs while the softmax works on S(t)), O [320,448).  Each row's 128 keys are split
-// between the two softmax warps of its TMEM lane quarter (64 keys each); they combine the
-// block row max through shared memory under a 64-thread named barrier, so both apply the
-// same running max, lazy-rescale decision and scale; each rescales / stores half of O's
-// columns and the row sums are combined at the epilogue.  K and V stream through 3 + 3
-// full-tile slots (192 KB).  MMAs are issued by one elected lane of a converged warp.
-// =====================================================================================
-namespace w8 {
-
-using tc::BM;
-using tc::BK;
-using tc::RESCALE_THRESHOLD;
-constexpr int NUM_THREADS = 320;  // w0 TMA + scheduler, w1 MMA + TMEM owner, w2..w9 softmax
-constexpr int TMEM_COLS = 512;
-constexpr int Q_COL = 0;
-constexpr int S_COL = 64;
-constexpr int O_COL = 320;
-constexpr int K_SLOTS = 3;
-constexpr int V_SLOTS = 3;
-
-template <int D>
-struct Smem {
-  static constexpr int TILE = BK * D * 2;
-  static constexpr int CHUNKS = D / 64;
-  static constexpr int CHUNK = BK * 128;
-  static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = OFF_K + K_SLOTS * TILE;
-  static constexpr int OFF_RED = OFF_V + V_SLOTS * TILE;  // float red[2][2][128], lsum[2][128]
-  static constexpr int OFF_BAR = OFF_RED + 6 * 128 * 4;
-  static constexpr int BYTES = OFF_BAR + 512;
-};
-
-struct Bars {
-  uint64_t q_full, o_full, o_done;
-  uint64_t s_full[2], p_full[2];
-  uint64_t k_full[K_SLOTS], k_empty[K_SLOTS];
-  uint64_t v_full[V_SLOTS], v_empty[V_SLOTS];
-  uint64_t sched_full[2], sched_empty[2];
-  int sched_item[2];
-  uint32_t tmem_base;
-};
-static_assert(sizeof(Bars) <= 512, "barrier block must fit the reserved smem");
-
-template <int D>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    k_carve_w8(const __nv_bfloat16* __restrict__ q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
-               CarveShape s, const int32_t* __restrict__ kv_idx,
-               const int32_t* __restrict__ kv_cnt, int* __restrict__ counter, int total_items,
-               float scale_log2, float beta_log2) {
-  using L = Smem<D>;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sK = smem + L::OFF_K;
-  uint8_t* sV = smem + L::OFF_V;
-  float* red = reinterpret_cast<float*>(smem + L::OFF_RED);  // [parity][half][row]
-  float* lsum = red + 4 * 128;                                // [half][row]
-  Bars* bars = reinterpret_cast<Bars*>(smem + L::OFF_BAR);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    if (ptx::smem_u32(smem) & 1023u) __trap();
-    ptx::mbar_init(&bars->q_full, 128);
-    ptx::mbar_init(&bars->o_full, 1);
-    ptx::mbar_init(&bars->o_done, 1);
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&bars->s_full[i], 1);
-      ptx::mbar_init(&bars->p_full[i], 256);
-      ptx::mbar_init(&bars->sched_full[i], 1);
-      ptx::mbar_init(&bars->sched_empty[i], 1 + 8);
-    }
-    for (int i = 0; i < K_SLOTS; ++i) {
-      ptx::mbar_init(&bars->k_full[i], 1);
-      ptx::mbar_init(&bars->k_empty[i], 1);
-    }
-    for (int i = 0; i < V_SLOTS; ++i) {
-      ptx::mbar_init(&bars->v_full[i], 1);
-      ptx::mbar_init(&bars->v_empty[i], 1);
-    }
-    ptx::fence_mbar_init();
-    ptx::tma_prefetch_desc(&tm_k);
-    ptx::tma_prefetch_desc(&tm_v);
-  }
-  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(&bars->tmem_base);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
-
-  if (warp == 0) {
-    // ============================ TMA producer + scheduler ============================
-    const uint64_t pol_kv = ptx::policy_evict_last();
-    const uint64_t pol_stream = ptx::policy_evict_first();
-    uint32_t it = 0, gk = 0, gv = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      int item = 0;
-      if (lane == 0) {
-        ptx::mbar_wait(&bars->sched_empty[slot], ((it >> 1) & 1) ^ 1);
-        item = atomicAdd(counter, 1);
-        if (item >= total_items) item = -1;
-        bars->sched_item[slot] = item;
-        ptx::mbar_arrive(&bars->sched_full[slot]);
-      }
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      auto load = [&](const CUtensorMap* tm, uint8_t* base, uint64_t* full, uint64_t* empty,
-                      int slots, uint32_t& cnt, int b) {
-        if (lane == 0) {
-          const int sl = cnt % slots;
-          ptx::mbar_wait(&empty[sl], ((cnt / slots) & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[sl], L::TILE);
-#pragma unroll
-          for (int c = 0; c < L::CHUNKS; ++c)
-            ptx::tma_load_3d(base + sl * L::TILE + c * L::CHUNK, tm, &full[sl], c * 64, b * BK, h,
-                             vis ? pol_kv : pol_stream);
-        }
-        ++cnt;
-      };
-      for (int t = 0; t < n; ++t) {
-        const int b = kl.block(t);
-        load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, b);
-        load(&tm_v, sV, bars->v_full, bars->v_empty, V_SLOTS, gv, b);
-      }
-    }
-  } else if (warp == 1) {
-    // ============================ MMA issuer ============================
-    constexpr uint32_t IDESC_S = tc::make_idesc(BM, BK, 0);  // Q (TMEM) x K (K-major), N = 128
-    constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, 1);   // P (TMEM) x V (MN-major)
-    const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
-    uint32_t it = 0, gk = 0, gv = 0, gs = 0, gp = 0;
-    auto issue_s = [&]() {  // S[gs & 1] = Q K(gk)^T
-      const int sl = gk % K_SLOTS;
-      ptx::mbar_wait(&bars->k_full[sl], (gk / K_SLOTS) & 1);
-      ptx::tc_fence_after();
-      const uint32_t kb = aK + sl * L::TILE;
-      if (ptx::elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t koff = (kk >> 2) * L::CHUNK + (kk & 3) * 32;
-          ptx::mma_ts(tmem + S_COL + (gs & 1) * BK, tmem + Q_COL + kk * 8,
-                      tc::make_sdesc(kb + koff, 16, 1024), IDESC_S, kk > 0 ? 1u : 0u);
-        }
-        ptx::mma_commit(&bars->k_empty[sl]);
-        ptx::mma_commit(&bars->s_full[gs & 1]);
-      }
-      __syncwarp();
-      ++gk;
-      ++gs;
-    };
-    for (;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
-      const int item = bars->sched_item[slot];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      ptx::mbar_wait(&bars->q_full, it & 1);  // Q in TMEM (previous item's O read out)
-      ptx::tc_fence_after();
-      if (n == 0) {
-        if (ptx::elect_one()) ptx::mma_commit(&bars->o_full);
-        __syncwarp();
-        continue;
-      }
-      issue_s();
-      for (int t = 0; t < n; ++t) {
-        if (t + 1 < n) issue_s();  // S(t+1) into the other buffer while softmax(t) runs
-        ptx::mbar_wait(&bars->p_full[gp & 1], (gp >> 1) & 1);
-        const int vs = gv % V_SLOTS;
-        ptx::mbar_wait(&bars->v_full[vs], (gv / V_SLOTS) & 1);
-        ptx::tc_fence_after();
-        const uint32_t vb = aV + vs * L::TILE;
-        const uint32_t pcol = tmem + S_COL + (gp & 1) * BK;
-        if (ptx::elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            ptx::mma_ts(tmem + O_COL, pcol + kk * 8, tc::make_sdesc(vb + kk * 16 * 128, L::CHUNK, 1024),
-                        IDESC_O, (t > 0 || kk > 0) ? 1u : 0u);
-          ptx::mma_commit(&bars->v_empty[vs]);
-          ptx::mma_commit(&bars->o_done);
-        }
-        __syncwarp();
-        ++gv;
-        ++gp;
-      }
-      if (ptx::elect_one()) ptx::mma_commit(&bars->o_full);
-      __syncwarp();
-    }
-  } else {
-    // ============================ Q load / softmax / epilogue ============================
-    const int quarter = warp & 3;              // TMEM lane quarter
-    const int half = (warp - 2) >> 2;          // keys [64 half, 64 half + 64) of every block
-    const int row = quarter * 32 + lane;
-    const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
-    const int bar_id = 1 + quarter;            // the two warps of this lane quarter
-    uint32_t it = 0, g = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
-      const int item = bars->sched_item[slot];
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      if (half == 0) {  // this row of Q -> TMEM lane `row`, columns Q_COL.. (bf16 pairs)
-        const int4* src = reinterpret_cast<const int4*>(q + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          uint32_t w[32];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int4 x = __ldg(src + c * 8 + e);
-            w[4 * e] = (uint32_t)x.x;
-            w[4 * e + 1] = (uint32_t)x.y;
-            w[4 * e + 2] = (uint32_t)x.z;
-            w[4 * e + 3] = (uint32_t)x.w;
-          }
-          ptx::tmem_st32(t_row + Q_COL + c * 32, w);
-        }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars->q_full);
-      }
-      float m_run = -INFINITY, l_run = 0.f;
-      for (int t = 0; t < n; ++t, ++g) {
-        const int b = kl.block(t);
-        const int kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond) - half * 64;
-        const float bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
-        ptx::mbar_wait(&bars->s_full[g & 1], (g >> 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t scol = S_COL + (g & 1) * BK;
-        uint32_t sr[64];
-        ptx::tmem_ld32(t_row + scol + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-        ptx::tmem_ld32(t_row + scol + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-        ptx::tmem_wait_ld();
-        if (kvalid < 64) {  // padding keys of a partial block -> -inf (attention.py:193)
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (e >= kvalid) sr[e] = __float_as_uint(-INFINITY);
-        }
-        float mx8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
-#pragma unroll
-        for (int e = 8; e < 64; e += 16)
-#pragma unroll
-          for (int qq = 0; qq < 8; ++qq)
-            mx8[qq] = tc::fmax3(mx8[qq], __uint_as_float(sr[e + qq]), __uint_as_float(sr[e + 8 + qq]));
-        const float m_loc = tc::fmax3(tc::fmax3(mx8[0], mx8[1], mx8[2]), tc::fmax3(mx8[3], mx8[4], mx8[5]),
-                                      fmaxf(mx8[6], mx8[7]));
-        // combine with the other half of the row; both halves have read their S columns,
-        // so after this barrier half 1 may write P over S columns [32, 64)
-        red[((g & 1) * 2 + half) * 128 + row] = m_loc;
-        ptx::named_bar_sync(bar_id, 64);
-        const float mraw = fmaxf(m_loc, red[((g & 1) * 2 + (half ^ 1)) * 128 + row]);
-        const float m_blk = (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
-        const float m_new = fmaxf(m_run, m_blk);
-        const bool first = (t == 0);
-        const bool need = !first && (m_new > m_run + RESCALE_THRESHOLD);
-        const float m_use = (first || need) ? m_new : m_run;
-        const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
-        const float c0 = bias - m_use;
-        const uint64_t sc2 = tc::f2_pack(scale_log2, scale_log2), c02 = tc::f2_pack(c0, c0);
-        uint64_t acc2[4] = {0, 0, 0, 0};
-        uint32_t pk[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const uint64_t x = tc::ffma2(tc::f2_pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])),
-                                       sc2, c02);
-          const float p0 = ptx::ex2(tc::f2_lo(x)), p1 = ptx::ex2(tc::f2_hi(x));
-          acc2[e & 3] = tc::fadd2(acc2[e & 3], tc::f2_pack(p0, p1));
-          pk[e] = ptx::pack_bf16(p0, p1);
-        }
-        ptx::tmem_st32(t_row + scol + half * 32, pk);  // P keys [64 half, +64) -> 32 columns
-        const uint64_t sum2 = tc::fadd2(tc::fadd2(acc2[0], acc2[1]), tc::fadd2(acc2[2], acc2[3]));
-        l_run = l_run * alpha + (tc::f2_lo(sum2) + tc::f2_hi(sum2));
-        m_run = m_use;
-        if (__any_sync(0xffffffffu, need)) {
-          // O is final only once PV(t-1) retired: o_done completes once per PV
-          ptx::mbar_wait(&bars->o_done, (g - 1) & 1);
-          ptx::tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < D / 64; ++c) {  // this half's O columns
-            uint32_t ov[32];
-            const uint32_t oc = O_COL + half * (D / 2) + c * 32;
-            ptx::tmem_ld32(t_row + oc, ov);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            ptx::tmem_st32(t_row + oc, ov);
-          }
-        }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars->p_full[g & 1]);
-      }
-      // ---- epilogue: O / (l_0 + l_1) -> bf16, this half's columns; padding rows zero
-      lsum[half * 128 + row] = l_run;
-      ptx::named_bar_sync(bar_id, 64);
-      const float l_tot = lsum[row] + lsum[128 + row];
-      ptx::mbar_wait(&bars->o_full, it & 1);
-      ptx::tc_fence_after();
-      const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
-      const float inv_l = (row < qvalid) ? 1.f / l_tot : 0.f;
-      __nv_bfloat16* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn + half * (D / 2);
-#pragma unroll 1
-      for (int c = 0; c < D / 64; ++c) {
-        uint32_t ov[32];
-        ptx::tmem_ld32(t_row + O_COL + half * (D / 2) + c * 32, ov);
-        ptx::tmem_wait_ld();
-        uint32_t pkk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pkk[e] = ptx::pack_bf16(__uint_as_float(ov[2 * e]) * inv_l, __uint_as_float(ov[2 * e + 1]) * inv_l);
-        int4* dst = reinterpret_cast<int4*>(orow + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          __stcs(dst + e, make_int4((int)pkk[4 * e], (int)pkk[4 * e + 1], (int)pkk[4 * e + 2], (int)pkk[4 * e + 3]));
-      }
-      ptx::named_bar_sync(bar_id, 64);  // lsum reuse by the next item
-      ptx::tc_fence_before();
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<TMEM_COLS>(tmem);
-  }
-}
-
-}  // namespace w8
 
 
 
@@ -1261,38 +912,6 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
 
 
 
-template <int D>
-static int launch_w8(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                     const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
-                     cudaStream_t st) {
-  CUtensorMap tk, tv;
-  const int64_t n_pad = (int64_t)s.M_total * s.m;
-  int rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::BK))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::BK))) return rc;
-  const int smem = w8::Smem<D>::BYTES;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(w8::k_carve_w8<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         smem);
-    if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve w8 smem attr: %s", cudaGetErrorString(e));
-    attr_set = true;
-  }
-  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
-  if (e != cudaSuccess) return set_error(TCB_ECUDA, "memset counter: %s", cudaGetErrorString(e));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int total = s.H * s.M_total;
-  const int grid = sms < total ? sms : total;
-  const float LOG2E = 1.4426950408889634f;
-  const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  w8::k_carve_w8<D><<<grid, w8::NUM_THREADS, smem, st>>>((const __nv_bfloat16*)q, tk, tv,
-                                                        (__nv_bfloat16*)o, s, kv_idx, kv_cnt, work,
-                                                        total, scale_log2, beta * LOG2E);
-  return check_launch("k_carve_w8");
-}
-
 extern "C" int tcb_carve_fwd_simt(const void* q, const void* k, const void* v, void* o, int dtype,
                                   int64_t stride_h, int64_t stride_n, const int32_t* kv_idx,
                                   const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
@@ -1325,12 +944,6 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
     if (emu != 0 && emu != 2 && emu != 3 && emu != 4) emu = 0;
   }
   cudaStream_t st = as_stream(stream);
-  static int impl = -1;  // TCB_CARVE_IMPL=3: one CTA per SM, Q in TMEM, 8 softmax warps (A/B)
-  if (impl < 0) {
-    const char* env = getenv("TCB_CARVE_IMPL");
-    impl = env ? atoi(env) : 0;
-  }
-  if (impl == 3 && d == 128) return launch_w8<128>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
   if (d == 128) {
     switch (emu) {
       case 3: return launch_tc<128, 3>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
