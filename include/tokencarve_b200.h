@@ -34,6 +34,7 @@ extern "C" {
 /* element types for tensors whose dtype is not fixed */
 #define TCB_F32 0
 #define TCB_BF16 1
+#define TCB_F16 2
 
 const char* tcb_last_error(void);
 int tcb_abi_version(void);
@@ -106,7 +107,7 @@ int tcb_mask_unpack(const uint32_t* bits, int64_t rows, int M_total, int words, 
  * head h streams kv blocks kv_idx[h,i,:kv_cnt[h,i]] (ascending); condition
  * q-blocks attend all M_total blocks; padding keys get -inf, beta is added on
  * condition keys of vision rows, padding rows of o are zeroed.
- * dtype TCB_BF16 with m == 128 and d in {64,128} runs the tcgen05/TMEM/TMA
+ * dtype TCB_BF16 or TCB_F16 with m == 128 and d in {64,128} runs the tcgen05/TMEM/TMA
  * kernel; everything else runs the fp32 SIMT kernel (parity path).
  * work: caller-provided scratch of >= 16 bytes (scheduler counter). */
 int tcb_carve_fwd(const void* q, const void* k, const void* v, void* o, int dtype,

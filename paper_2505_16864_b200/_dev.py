@@ -41,7 +41,9 @@ def code_of(dtype: torch.dtype) -> int:
         return _native.F32
     if dtype == torch.bfloat16:
         return _native.BF16
-    raise TypeError(f"unsupported dtype {dtype} (float32 or bfloat16)")
+    if dtype == torch.float16:
+        return _native.F16
+    raise TypeError(f"unsupported dtype {dtype} (float32, bfloat16 or float16)")
 
 
 def stream() -> int:

@@ -15,7 +15,7 @@ from .errors import ContractError, DomainError, ShapeError, SizeError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libtcb200.so")
 
-F32, BF16 = 0, 1
+F32, BF16, F16 = 0, 1, 2
 
 _P = C.c_void_p
 _I = C.c_int

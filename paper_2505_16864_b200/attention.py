@@ -121,7 +121,7 @@ def carve_attention(inputs: AttentionInputs, mask: BlockMask,
     if layout.M_v:
         mask.check_nonempty()
     q, k, v = (_dev.as_cuda(x) for x in (inputs.q, inputs.k, inputs.v))
-    if q.dtype not in (torch.float32, torch.bfloat16):
+    if q.dtype not in (torch.float32, torch.bfloat16, torch.float16):
         q, k, v = q.float(), k.float(), v.float()
     out = carve_raw(q, k, v, mask, layout, beta.beta)
     return _dev.to_like(out, inputs.q)

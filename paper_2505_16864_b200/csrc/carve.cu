@@ -19,6 +19,7 @@
 
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <math.h>
 #include <stdlib.h>
 
@@ -60,8 +61,16 @@ template <>
 __device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) {
   return __bfloat162float(*p);
 }
+template <>
+__device__ __forceinline__ float ldf<__half>(const __half* p) {
+  return __half2float(*p);
+}
 template <typename T>
 __device__ __forceinline__ T stf(float v);
+template <>
+__device__ __forceinline__ __half stf<__half>(float v) {
+  return __float2half_rn(v);
+}
 template <>
 __device__ __forceinline__ float stf<float>(float v) {
   return v;
@@ -338,11 +347,30 @@ struct Bars {
 };
 static_assert(sizeof(Bars) <= 256, "barrier block must fit the reserved smem");
 
-// instruction descriptor, kind::f16: bf16 x bf16 -> f32, K-major A, B major per arg
-__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int b_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) |
+// instruction descriptor, kind::f16: {bf16|f16} x {bf16|f16} -> f32, K-major A, B major per
+// arg (a/b type field: 1 = bf16, 0 = f16)
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int b_mn_major, int bf16 = 1) {
+  return (1u << 4) | ((uint32_t)bf16 << 7) | ((uint32_t)bf16 << 10) | ((uint32_t)b_mn_major << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+
+// element traits of the 16-bit input / P / output type
+template <typename E>
+struct Elem;
+template <>
+struct Elem<__nv_bfloat16> {
+  static constexpr int kBf16 = 1;
+  __device__ static uint32_t pack(float lo, float hi) { return ptx::pack_bf16(lo, hi); }
+};
+template <>
+struct Elem<__half> {
+  static constexpr int kBf16 = 0;
+  __device__ static uint32_t pack(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+  }
+};
 
 // smem matrix descriptor, SWIZZLE_128B, sm_100 version bits
 __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -410,10 +438,10 @@ struct KvList {
   }
 };
 
-template <int D, int EMU>
+template <int D, int EMU, typename E = __nv_bfloat16>
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     k_carve_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-               const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
+               const __grid_constant__ CUtensorMap tm_v, E* __restrict__ o,
                CarveShape s, const int32_t* __restrict__ kv_idx,
                const int32_t* __restrict__ kv_cnt, int* __restrict__ counter, int total_items,
                float scale_log2, float beta_log2, int dbg) {
@@ -520,8 +548,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
     // Whole warp runs the loop; one elected lane issues (uniform-register descriptors).
-    constexpr uint32_t IDESC_S = make_idesc(BM, HN, 0);  // Q (K-major) x K (K-major)
-    constexpr uint32_t IDESC_O = make_idesc(BM, D, 1);   // P (TMEM)   x V (MN-major)
+    constexpr uint32_t IDESC_S = make_idesc(BM, HN, 0, Elem<E>::kBf16);  // Q (K-major) x K (K-major)
+    constexpr uint32_t IDESC_O = make_idesc(BM, D, 1, Elem<E>::kBf16);   // P (TMEM)   x V (MN-major)
     const uint32_t aQ = ptx::smem_u32(sQ), aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
     uint32_t it = 0, gk = 0, gv = 0, gs = 0, gp = 0;
     auto issue_s = [&]() {  // S(gs) = Q K(gs)^T into buffer gs & 1
@@ -679,7 +707,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
             p1 = ptx::ex2(f2_hi(x));
           }
           acc2[e & 3] = fadd2(acc2[e & 3], f2_pack(p0, p1));
-          pk[e] = ptx::pack_bf16(p0, p1);
+          pk[e] = Elem<E>::pack(p0, p1);
         }
         ptx::tmem_st32(t_row + (g & 1) * HN, pk);
         const uint64_t sum2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
@@ -708,7 +736,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       ptx::tc_fence_after();
       const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
       const float inv_l = (row < qvalid) ? 1.f / l_run : 0.f;
-      __nv_bfloat16* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
+      E* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
         uint32_t ov[32];
@@ -717,7 +745,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          pk[e] = ptx::pack_bf16(__uint_as_float(ov[2 * e]) * inv_l,
+          pk[e] = Elem<E>::pack(__uint_as_float(ov[2 * e]) * inv_l,
                                  __uint_as_float(ov[2 * e + 1]) * inv_l);
         int4* dst = reinterpret_cast<int4*>(orow + c * 32);
 #pragma unroll
@@ -763,14 +791,15 @@ static PFN_encodeTiled get_encode() {
 
 // (d, N_pad, H) bf16 view with box (64, 128, 1), 128-byte swizzle
 static int make_tmap(CUtensorMap* tm, const void* base, int d, int64_t n_pad, int H, int64_t sh,
-                     int64_t sn, int box_rows) {
+                     int64_t sn, int box_rows, bool f16 = false) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return set_error(TCB_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)n_pad, (cuuint64_t)H};
   cuuint64_t strides[2] = {(cuuint64_t)sn * 2, (cuuint64_t)sh * 2};
   cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+  CUresult r = enc(tm, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                   const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(TCB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -780,7 +809,8 @@ static int make_tmap(CUtensorMap* tm, const void* base, int d, int64_t n_pad, in
 static int validate(const void* q, const void* k, const void* v, void* o, int dtype,
                     const int32_t* kv_idx, const int32_t* kv_cnt, const CarveShape& s) {
   TCB_CHECK_ARG(q && k && v && o, TCB_ESHAPE, "null q/k/v/o");
-  TCB_CHECK_ARG(dtype == TCB_F32 || dtype == TCB_BF16, TCB_EDOMAIN, "unsupported dtype %d", dtype);
+  TCB_CHECK_ARG(dtype == TCB_F32 || dtype == TCB_BF16 || dtype == TCB_F16, TCB_EDOMAIN,
+                "unsupported dtype %d", dtype);
   TCB_CHECK_ARG(s.H >= 1 && s.d >= 1 && s.m >= 1 && s.M_v >= 0 && s.M_total >= s.M_v &&
                     s.M_total >= 1,
                 TCB_ESHAPE, "bad carve shape");
@@ -832,12 +862,11 @@ static int try_f32t(const void* q, const void* k, const void* v, void* o, const 
   }
 }
 
-static int launch_simt(const void* q, const void* k, const void* v, void* o, int dtype,
-                       const CarveShape& s, const int32_t* kv_idx, const int32_t* kv_cnt,
-                       float beta, cudaStream_t st) {
+template <typename T>
+static int launch_simt_t(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
+                         const int32_t* kv_idx, const int32_t* kv_cnt, float beta, cudaStream_t st) {
   {  // tiled fp32-math kernel for the common block / head sizes
-    const int rc = dtype == TCB_F32 ? try_f32t<float>(q, k, v, o, s, kv_idx, kv_cnt, beta, st)
-                                    : try_f32t<__nv_bfloat16>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    const int rc = try_f32t<T>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
     if (rc != -1) return rc;
   }
   TCB_CHECK_ARG(s.d <= 32 * SIMT_MAXC, TCB_ESIZE, "SIMT carve supports d <= %d", 32 * SIMT_MAXC);
@@ -845,23 +874,21 @@ static int launch_simt(const void* q, const void* k, const void* v, void* o, int
   const float scale = (float)(1.0 / sqrt((double)s.d));
   const unsigned grid = (unsigned)((int64_t)s.H * s.M_total);
   if (smem > 48 * 1024) {
-    cudaError_t e;
-    if (dtype == TCB_F32)
-      e = cudaFuncSetAttribute(k_carve_simt<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem);
-    else
-      e = cudaFuncSetAttribute(k_carve_simt<__nv_bfloat16>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_carve_simt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "simt smem: %s", cudaGetErrorString(e));
   }
-  if (dtype == TCB_F32)
-    k_carve_simt<float><<<grid, 128, smem, st>>>((const float*)q, (const float*)k, (const float*)v,
-                                                 (float*)o, s, kv_idx, kv_cnt, beta, scale);
-  else
-    k_carve_simt<__nv_bfloat16><<<grid, 128, smem, st>>>(
-        (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
-        (__nv_bfloat16*)o, s, kv_idx, kv_cnt, beta, scale);
+  k_carve_simt<T><<<grid, 128, smem, st>>>((const T*)q, (const T*)k, (const T*)v, (T*)o, s, kv_idx,
+                                           kv_cnt, beta, scale);
   return check_launch("k_carve_simt");
+}
+
+static int launch_simt(const void* q, const void* k, const void* v, void* o, int dtype,
+                       const CarveShape& s, const int32_t* kv_idx, const int32_t* kv_cnt,
+                       float beta, cudaStream_t st) {
+  if (dtype == TCB_F32) return launch_simt_t<float>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+  if (dtype == TCB_BF16) return launch_simt_t<__nv_bfloat16>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+  return launch_simt_t<__half>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
 }
 
 // TCB_CARVE_DEBUG bit 0: stream no K/V after the first ring fill; bit 1: skip the softmax
@@ -875,20 +902,20 @@ static int dbg_flags() {
   return v;
 }
 
-template <int D, int EMU>
+template <int D, int EMU, typename E = __nv_bfloat16>
 static int launch_tc(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
                      const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
                      cudaStream_t st) {
   CUtensorMap tq, tk, tv;
   const int64_t n_pad = (int64_t)s.M_total * s.m;
   int rc;
-  if ((rc = make_tmap(&tq, q, D, n_pad, s.H, s.sh, s.sn, tc::BM))) return rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::HN))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::HN))) return rc;
+  if ((rc = make_tmap(&tq, q, D, n_pad, s.H, s.sh, s.sn, tc::BM, !tc::Elem<E>::kBf16))) return rc;
+  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::HN, !tc::Elem<E>::kBf16))) return rc;
+  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::HN, !tc::Elem<E>::kBf16))) return rc;
   const int smem = tc::Smem<D>::BYTES;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc::k_carve_tc<D, EMU>,
+    cudaError_t e = cudaFuncSetAttribute(tc::k_carve_tc<D, EMU, E>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
     attr_set = true;
@@ -903,7 +930,7 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
   if (grid > total) grid = total;
   const float LOG2E = 1.4426950408889634f;
   const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  tc::k_carve_tc<D, EMU><<<grid, tc::NUM_THREADS, smem, st>>>(tq, tk, tv, (__nv_bfloat16*)o, s, kv_idx,
+  tc::k_carve_tc<D, EMU, E><<<grid, tc::NUM_THREADS, smem, st>>>(tq, tk, tv, (E*)o, s, kv_idx,
                                                          kv_cnt, work, total, scale_log2,
                                                          beta * LOG2E, dbg_flags());
   return check_launch("k_carve_tc");
@@ -933,8 +960,8 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
   const bool aligned = ((uintptr_t)q % 16 == 0) && ((uintptr_t)k % 16 == 0) &&
                        ((uintptr_t)v % 16 == 0) && ((uintptr_t)o % 16 == 0) &&
                        (stride_n * 2) % 16 == 0 && (stride_h * 2) % 16 == 0;
-  const bool tc_ok = dtype == TCB_BF16 && m == 128 && (d == 128 || d == 64) && aligned && work &&
-                     M_v > 0;
+  const bool tc_ok = (dtype == TCB_BF16 || dtype == TCB_F16) && m == 128 && (d == 128 || d == 64) &&
+                     aligned && work && M_v > 0;
   if (!tc_ok) return launch_simt(q, k, v, o, dtype, s, kv_idx, kv_cnt, beta, as_stream(stream));
   // pairs (of 8) whose exp2 runs on the FMA pipe instead of MUFU; TCB_CARVE_EMU overrides
   static int emu = -1;
@@ -944,6 +971,9 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
     if (emu != 0 && emu != 2 && emu != 3 && emu != 4) emu = 0;
   }
   cudaStream_t st = as_stream(stream);
+  if (dtype == TCB_F16)  // fp16 operands and P (kind::f16 with f16 inputs), f32 accumulation
+    return d == 128 ? launch_tc<128, 0, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
+                    : launch_tc<64, 0, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
   if (d == 128) {
     switch (emu) {
       case 3: return launch_tc<128, 3>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);

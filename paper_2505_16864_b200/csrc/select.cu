@@ -7,6 +7,7 @@
 #include "common.cuh"
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <math.h>
 #include <stdlib.h>
 
@@ -38,6 +39,21 @@ struct Vec16<__nv_bfloat16> {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       float2 f = __bfloat1622float2(h[i]);
+      o[2 * i] = f.x;
+      o[2 * i + 1] = f.y;
+    }
+  }
+};
+
+template <>
+struct Vec16<__half> {
+  static constexpr int VE = 8;
+  __device__ static void load(const __half* p, double* o) {
+    int4 v = __ldcs(reinterpret_cast<const int4*>(p));
+    const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __half22float2(h[i]);
       o[2 * i] = f.x;
       o[2 * i + 1] = f.y;
     }
@@ -942,7 +958,8 @@ extern "C" int tcb_block_pool(const void* x0, const void* x1, int dtype, int64_t
   TCB_CHECK_ARG((x1 == nullptr) == (out1 == nullptr), TCB_ESHAPE, "x1/out1 must both be set");
   TCB_CHECK_ARG(H >= 1 && d >= 1 && m >= 1 && M_total >= M_v && M_v >= 0, TCB_ESHAPE,
                 "bad pool shape");
-  TCB_CHECK_ARG(dtype == TCB_F32 || dtype == TCB_BF16, TCB_EDOMAIN, "unsupported dtype %d", dtype);
+  TCB_CHECK_ARG(dtype == TCB_F32 || dtype == TCB_BF16 || dtype == TCB_F16, TCB_EDOMAIN,
+                "unsupported dtype %d", dtype);
   if ((int64_t)H * M_total == 0) return TCB_OK;
   const int esz = dtype == TCB_F32 ? 4 : 2;
   const int VE = 16 / esz;
@@ -964,8 +981,18 @@ extern "C" int tcb_block_pool(const void* x0, const void* x1, int dtype, int64_t
       k_pool<float, false><<<grid, 128, 0, s>>>((const float*)x0, (const float*)x1, stride_h,
                                                 stride_n, H, d, m, M_v, M_total, n_valid, n_cond,
                                                 out0, out1, G, chunks);
-  } else {
+  } else if (dtype == TCB_BF16) {
     using B = __nv_bfloat16;
+    if (vec)
+      k_pool<B, true><<<grid, 128, 0, s>>>((const B*)x0, (const B*)x1, stride_h, stride_n, H, d,
+                                           m, M_v, M_total, n_valid, n_cond, out0, out1, G,
+                                           chunks);
+    else
+      k_pool<B, false><<<grid, 128, 0, s>>>((const B*)x0, (const B*)x1, stride_h, stride_n, H, d,
+                                            m, M_v, M_total, n_valid, n_cond, out0, out1, G,
+                                            chunks);
+  } else {
+    using B = __half;
     if (vec)
       k_pool<B, true><<<grid, 128, 0, s>>>((const B*)x0, (const B*)x1, stride_h, stride_n, H, d,
                                            m, M_v, M_total, n_valid, n_cond, out0, out1, G,

@@ -442,3 +442,28 @@ def test_acceptance_03_masked_equals_dense_with_bias():
         want = oracle.dense_reference(q, k, v, oracle.mask_to_bias(bits, L), oracle.token_valid(L))
         worst = max(worst, float(np.abs(got - want).max()))
     assert worst <= 1e-5, worst
+
+
+@pytest.mark.parametrize("d", [128, 64])
+def test_carve_fp16_tcgen05_and_pool(d):
+    # fp16 inputs run the same tcgen05 kernel with f16 operands / P (f32 accumulation) and
+    # the same pool; tolerance as bf16 (fp16 has the finer mantissa)
+    dims = tcb.GridDims(4, 16, 24)
+    lay = tcb.build_layout(dims, 128, 60)
+    st = tcb.StaticMasks.build(lay, dims, tcb.build_curve(dims))
+    rng = np.random.default_rng(12)
+    q, k, v = (rng.standard_normal((2, lay.padded_total, d)).astype(np.float32) for _ in range(3))
+    qh, kh, vh = (torch.from_numpy(a).cuda().half() for a in (q, k, v))
+    mask, R = tcb.build_block_mask(qh, kh, lay, st, tcb.SelectionParams(k=0.3, p=0.0))
+    L = oracle.layout_scalars(dims.as_tuple(), 128, 60)
+    q32, k32, v32 = (t.float().cpu().numpy() for t in (qh, kh, vh))
+    pq, _ = oracle.pool_blocks(q32, L)  # fp16 values pool bit-exactly in float64
+    got_pq = tcb.block_pool(qh, lay).values.cpu().numpy()
+    assert np.array_equal(got_pq, pq)
+    out = tcb.carve_attention(tcb.AttentionInputs(q=qh, k=kh, v=vh, layout=lay), mask, tcb.AmplifierBias(0.3))
+    assert out.dtype == torch.float16
+    ref = oracle.carve(q32, k32, v32, mask.bits.cpu().numpy(), L, 0.3, workers=8)
+    got = out.float().cpu().numpy()
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err <= 1e-2, err
+    assert np.all(got[:, ~oracle.token_valid(L)] == 0.0)
