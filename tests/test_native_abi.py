@@ -49,6 +49,37 @@ def test_error_mapping_without_gpu():
                      None)
     with pytest.raises(DomainError):
         _native.call("tcb_block_pool", 1, None, 7, 0, 0, 1, 1, 1, 1, 1, 1, 0, 1, None, None)
+    # carve: unknown dtype, shape errors, too many work items
+    with pytest.raises(DomainError):
+        _native.call("tcb_carve_fwd", 1, 1, 1, 1, 9, 128, 128, 1, 1, 1, 128, 128, 1, 1, 1, 0, 0.0, 1,
+                     None)
+    with pytest.raises(ShapeError):
+        _native.call("tcb_carve_fwd", None, 1, 1, 1, 1, 128, 128, 1, 1, 1, 128, 128, 1, 1, 1, 0, 0.0,
+                     1, None)
+    with pytest.raises(SizeError):
+        _native.call("tcb_carve_fwd", 1, 1, 1, 1, 1, 128, 128, 1, 1, 1 << 20, 128, 128, 4096, 4096,
+                     1, 0, 0.0, 1, None)
+    # selection: M_total beyond the supported range, n_floor < 1
+    with pytest.raises(SizeError):
+        _native.call("tcb_block_select", 1, 1, 9000, 9000, None, 300, 1, 0.0, 1, 1, 1, 1, None)
+    with pytest.raises(DomainError):
+        _native.call("tcb_block_select", 1, 1, 4, 4, None, 1, 0, 0.0, 1, 1, 1, 1, None)
+    # fused neighbours: bad rope sections / strides / patch sizes / grid mismatch
+    import ctypes as C
+    one = (C.c_void_p * 1)(16)
+    rot = (C.c_int * 1)(1)
+    with pytest.raises(DomainError):
+        _native.call("tcb_rope_permute", C.cast(one, C.c_void_p), 64, 64, C.cast(one, C.c_void_p), 64,
+                     64, C.cast(rot, C.c_void_p), 1, 16, 2, 2, 2, 1, 64, 16, 10, 30, 30, None)
+    with pytest.raises(ShapeError):
+        _native.call("tcb_rope_permute", C.cast(one, C.c_void_p), 63, 64, C.cast(one, C.c_void_p), 64,
+                     64, C.cast(rot, C.c_void_p), 1, 16, 2, 2, 2, 1, 64, 16, 0, 32, 32, None)
+    with pytest.raises(DomainError):
+        _native.call("tcb_unpermute_euler", 1, 1, 1, 2, 2, 2, 0, 1, 1, 1, -0.1, 1, None)
+    with pytest.raises(ShapeError):
+        _native.call("tcb_curve_positions", 1, 7, 2, 2, 2, 1, None)
+    with pytest.raises(ShapeError):
+        _native.call("tcb_mask_words_to_packbits", 1, 4, 100, 3, 1, None)
 
 
 @pytest.fixture(scope="module")
