@@ -1,19 +1,22 @@
 // K7/K8 block-sparse flash-attention forward (carve_attention, attention.py:162-243).
 //
-//  * k_carve_tc   -- bf16, m == 128, d in {64,128}: persistent warp-specialised
+//  * k_carve_tc   -- bf16 / fp16, m == 128, d in {64,128}: persistent warp-specialised
 //                    tcgen05 kernel.  TMA loads Q/K/V tiles (128B swizzle) into smem
-//                    under mbarriers, one thread issues tcgen05.mma for S = Q K^T
-//                    into TMEM, four softmax warps read S with tcgen05.ld, do the
-//                    online softmax in registers (exp2, lazy rescale), write P as
-//                    bf16 back into TMEM over S, and the MMA thread issues
-//                    O += P V with A read from TMEM.  Two CTAs per SM interleave so
-//                    one CTA's softmax overlaps the other's MMAs.  Work items
-//                    (head, q-block) come from a global atomic counter, condition
-//                    q-blocks (full rows, ~10x longer) first, then vision q-blocks
-//                    head-major so concurrently running items share a head's K/V
-//                    in L2.
-//  * k_carve_simt -- fp32 math for any (m, d, dtype): the parity path that mirrors
-//                    the reference's per-block streaming softmax order.
+//                    under mbarriers, one elected lane of the MMA warp issues
+//                    tcgen05.mma for S = Q K^T into TMEM (64-key half-steps, S
+//                    double-buffered), four softmax warps read S with tcgen05.ld, do
+//                    the online softmax in registers (exp2, lazy rescale), write P as
+//                    16-bit back into TMEM over S, and the MMA warp issues O += P V with
+//                    A read from TMEM.  Two CTAs per SM interleave so one CTA's softmax
+//                    overlaps the other's MMAs.  Work items (head, q-block) come from a
+//                    global atomic counter, condition q-blocks (full rows, ~10x longer)
+//                    first, then vision q-blocks head-major so concurrently running
+//                    items share a head's K/V in L2.  DESIGN.md §4.1 has the measured
+//                    bounds and the rejected variants.
+//  * k_carve_f32t -- fp32 math on shared-memory tiles with register-blocked S / O for
+//                    the common (m, d): fp32 inputs and shapes the tcgen05 kernel does
+//                    not take; mirrors the reference's per-block streaming order (1e-5).
+//  * k_carve_simt -- fp32 math, one warp per query row, any (m, d): the fallback.
 #include "common.cuh"
 #include "ptx.cuh"
 
