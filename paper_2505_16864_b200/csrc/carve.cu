@@ -575,6 +575,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       ++gk;
       ++gs;
     };
+    // S(gs), S(gs+1) with the two MMAs of each k-step back to back on the same Q slice:
+    // the tensor core reuses the A operand, so the pair reads Q from shared memory once
+    // (tests/native/mma_rate.cu MODE 5: full rate vs 67 % for lone SS N=64 MMAs).
+    auto issue_pair = [&]() {
+      const int sl0 = gk % K_SLOTS, sl1 = (gk + 1) % K_SLOTS;
+      ptx::mbar_wait(&bars->k_full[sl0], (gk / K_SLOTS) & 1);
+      ptx::mbar_wait(&bars->k_full[sl1], ((gk + 1) / K_SLOTS) & 1);
+      ptx::tc_fence_after();
+      const uint32_t kb0 = aK + sl0 * L::HALF_BYTES, kb1 = aK + sl1 * L::HALF_BYTES;
+      if (ptx::elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t qoff = (kk >> 2) * L::Q_CHUNK + (kk & 3) * 32;
+          const uint32_t koff = (kk >> 2) * L::H_CHUNK + (kk & 3) * 32;
+          const uint64_t qd = make_sdesc(aQ + qoff, 16, 1024);
+          ptx::mma_ss(tmem + (gs & 1) * HN, qd, make_sdesc(kb0 + koff, 16, 1024), IDESC_S,
+                      kk > 0 ? 1u : 0u);
+          ptx::mma_ss(tmem + ((gs + 1) & 1) * HN, qd, make_sdesc(kb1 + koff, 16, 1024), IDESC_S,
+                      kk > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(&bars->k_empty[sl0]);
+        ptx::mma_commit(&bars->k_empty[sl1]);
+        ptx::mma_commit(&bars->s_full[gs & 1]);
+        ptx::mma_commit(&bars->s_full[(gs + 1) & 1]);
+      }
+      __syncwarp();
+      gk += 2;
+      gs += 2;
+    };
     for (;; ++it) {
       const int slot = it & 1;
       ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
@@ -596,9 +625,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         __syncwarp();
         continue;
       }
-      issue_s();
+      const bool pair = (dbg & 4) != 0;
+      if (pair) issue_pair(); else issue_s();
       for (int t = 0; t < T; ++t) {
-        if (t + 1 < T) {
+        if (pair) {
+          // paired issue: S(t+1), S(t+2) once PV(t-1) and PV(t) are queued (both S buffers free)
+        } else if (t + 1 < T) {
           issue_s();
           if (t + 2 == T) {
             if (ptx::elect_one()) ptx::mma_commit(&bars->q_empty);
@@ -625,6 +657,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         __syncwarp();
         ++gv;
         ++gp;
+        if (pair && (t & 1) && t + 1 < T) {
+          issue_pair();
+          if (t + 3 == T) {
+            if (ptx::elect_one()) ptx::mma_commit(&bars->q_empty);
+            __syncwarp();
+          }
+        }
+      }
+      if (pair && T == 2) {
+        if (ptx::elect_one()) ptx::mma_commit(&bars->q_empty);
+        __syncwarp();
       }
       if (ptx::elect_one()) ptx::mma_commit(&bars->o_full);
       __syncwarp();

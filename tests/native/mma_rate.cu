@@ -121,6 +121,15 @@ __global__ void __launch_bounds__(128) k_rate(int iters, unsigned long long* cyc
                       kk > 0);
         }
       }
+      if (MODE == 5) {  // same A (Q slice) for two consecutive MMAs into two S buffers
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          const uint32_t koff = (kk >> 2) * (N * 128) + (kk & 3) * 32;
+          ptx::mma_ss(Sc, make_sdesc(aQ + off, 16, 1024), make_sdesc(aK + koff, 16, 1024), IS, kk > 0);
+          ptx::mma_ss(Sc + N, make_sdesc(aQ + off, 16, 1024), make_sdesc(aV + koff, 16, 1024), IS, kk > 0);
+        }
+      }
       if (MODE == 1 || MODE == 4) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -128,7 +137,7 @@ __global__ void __launch_bounds__(128) k_rate(int iters, unsigned long long* cyc
           ptx::mma_ts(Sc, Qc + kk * 8, make_sdesc(aK + koff, 16, 1024), IS, kk > 0);
         }
       }
-      if (MODE >= 2) {
+      if (MODE >= 2 && MODE != 5) {
 #pragma unroll
         for (int kk = 0; kk < N / 16; ++kk)
           ptx::mma_ts(Oc, Qc + kk * 8, make_sdesc(aV + kk * 16 * 128, N * 128, 1024), IO, 1);
@@ -180,7 +189,8 @@ void run(const char* name, int occ) {
   unsigned long long mx = 0;
   for (auto v : h) mx = v > mx ? v : mx;
   double macs = 0;
-  if (MODE == 0 || MODE == 1 || MODE >= 3) macs += 128.0 * N * D;
+  if (MODE == 0 || MODE == 1 || (MODE >= 3 && MODE != 5)) macs += 128.0 * N * D;
+  if (MODE == 5) macs += 2 * 128.0 * N * D;
   if (MODE >= 2) macs += 128.0 * N * D;
   const double per_sm_cyc = (double)mx / iters / occ;  // cycles per iteration per SM
   const double tflops = 2.0 * macs * iters * grid / (ms * 1e-3) / 1e12;
@@ -200,17 +210,9 @@ int main() {
   setvbuf(stdout, nullptr, _IONBF, 0);
   cudaMalloc(&g_src, SRC_BYTES);
   cudaMemset(g_src, 0x3c, SRC_BYTES);
-  run<64, 0, 256>("SS QK thread", 1);
-  run<64, 0, 256, 0, 1, 0, 1>("SS QK warp-elect", 1);
-  run<128, 0, 256, 0, 1, 0, 1>("SS QK warp-elect", 1);
-  run<64, 1, 256, 0, 1, 0, 1>("TS QK warp-elect", 1);
-  run<64, 2, 256, 0, 1, 0, 1>("TS PV warp-elect", 1);
-  run<128, 2, 256, 0, 1, 0, 1>("TS PV warp-elect", 1);
-  run<64, 3, 256, 0, 1, 0, 1>("SS QK + TS PV warp-elect", 1);
-  run<64, 3, 256, 0, 1, 0, 1>("SS QK + TS PV warp-elect", 2);
-  run<64, 4, 256, 0, 1, 0, 1>("TS QK + TS PV warp-elect", 1);
-  run<128, 4, 512, 0, 1, 0, 1>("TS QK + TS PV warp-elect", 1);
-  run<64, 3, 256, 0, 4, 1, 1>("SS QK + TS PV warp + free copy", 1);
-  run<64, 4, 256, 0, 4, 1, 1>("TS QK + TS PV warp + free copy", 1);
+  run<64, 0, 256, 0, 1, 0, 1>("SS QK N64 warp", 2);
+  run<64, 5, 256, 0, 1, 0, 1>("SS QK N64 A-shared pairs", 2);
+  run<64, 5, 256, 0, 1, 0, 1>("SS QK N64 A-shared pairs", 1);
+  run<128, 0, 256, 0, 1, 0, 1>("SS QK N128 warp", 2);
   return 0;
 }

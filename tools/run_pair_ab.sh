@@ -1,0 +1,9 @@
+# paired-QK issue (TCB_CARVE_DEBUG=4) vs the shipped order: parity, ncu cycles/clock, bench time
+set -x
+TCB_CARVE_DEBUG=4 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -3
+for dbg in 0 4; do
+  TCB_CARVE_DEBUG=$dbg timeout 300 ncu --metrics gpu__time_duration.sum,sm__cycles_elapsed.avg,gpc__cycles_elapsed.avg.per_second,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum --clock-control none -k regex:k_carve_tc -s 3 -c 1 python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e 2>&1 | grep -E "gpu__|sm__|gpc__|l1tex" | sed "s/^/dbg=$dbg /"
+done
+for rep in 1 2; do for dbg in 0 4; do
+  TCB_CARVE_DEBUG=$dbg timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('dbg=$dbg', d['ms_per_step'], d.get('kernels_ms'), d['clocks'])"
+done; done
