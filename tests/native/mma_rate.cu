@@ -8,6 +8,7 @@
 //   2 TS  O += P V       (A = P in TMEM, B = V MN-major), K = N keys
 //   3 SS QK + TS PV      (the round-1 kernel's half-step)
 //   4 TS QK + TS PV      (Q resident in TMEM)
+//   5 two SS N=64 MMAs sharing A;  6-9 two-tile carve turn patterns (see the MODE >= 6 block)
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -137,7 +138,27 @@ __global__ void __launch_bounds__(128) k_rate(int iters, unsigned long long* cyc
           ptx::mma_ts(Sc, Qc + kk * 8, make_sdesc(aK + koff, 16, 1024), IS, kk > 0);
         }
       }
-      if (MODE >= 2 && MODE != 5) {
+      if (MODE >= 6) {  // two-tile carve turn patterns, N = 128 keys, P aliased over S
+        const uint32_t S0 = tmem, O0 = tmem + 128, S1 = tmem + 256, O1 = tmem + 384;
+        auto pv = [&](uint32_t S, uint32_t O) {
+#pragma unroll
+          for (int kk = 0; kk < N / 16; ++kk)
+            ptx::mma_ts(O, S + kk * 8, make_sdesc(aV + kk * 16 * 128, N * 128, 1024), IO, 1);
+        };
+        auto qk = [&](uint32_t S) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+            const uint32_t koff = (kk >> 2) * (N * 128) + (kk & 3) * 32;
+            ptx::mma_ss(S, make_sdesc(aQ + off, 16, 1024), make_sdesc(aK + koff, 16, 1024), IS, kk > 0);
+          }
+        };
+        if (MODE == 6) { pv(S0, O0); qk(S0); }                       // one tile: WAR on S
+        if (MODE == 7) { pv(S0, O0); qk(S0); pv(S1, O1); qk(S1); }   // two tiles, turn order
+        if (MODE == 8) { pv(S0, O0); pv(S1, O1); qk(S0); qk(S1); }   // two tiles, WAR spread
+        if (MODE == 9) { qk(S0); pv(S0, O0); }                       // one tile: RAW on S
+      }
+      if (MODE >= 2 && MODE != 5 && MODE < 6) {
 #pragma unroll
         for (int kk = 0; kk < N / 16; ++kk)
           ptx::mma_ts(Oc, Qc + kk * 8, make_sdesc(aV + kk * 16 * 128, N * 128, 1024), IO, 1);
@@ -191,7 +212,9 @@ void run(const char* name, int occ) {
   double macs = 0;
   if (MODE == 0 || MODE == 1 || (MODE >= 3 && MODE != 5)) macs += 128.0 * N * D;
   if (MODE == 5) macs += 2 * 128.0 * N * D;
-  if (MODE >= 2) macs += 128.0 * N * D;
+  if (MODE >= 2 && MODE != 5 && MODE < 6) macs += 128.0 * N * D;
+  if (MODE == 6 || MODE == 9) macs = 2 * 128.0 * N * D;
+  if (MODE == 7 || MODE == 8) macs = 4 * 128.0 * N * D;
   const double per_sm_cyc = (double)mx / iters / occ;  // cycles per iteration per SM
   const double tflops = 2.0 * macs * iters * grid / (ms * 1e-3) / 1e12;
   if (FREE) {
@@ -210,9 +233,10 @@ int main() {
   setvbuf(stdout, nullptr, _IONBF, 0);
   cudaMalloc(&g_src, SRC_BYTES);
   cudaMemset(g_src, 0x3c, SRC_BYTES);
-  run<64, 0, 256, 0, 1, 0, 1>("SS QK N64 warp", 2);
-  run<64, 5, 256, 0, 1, 0, 1>("SS QK N64 A-shared pairs", 2);
-  run<64, 5, 256, 0, 1, 0, 1>("SS QK N64 A-shared pairs", 1);
-  run<128, 0, 256, 0, 1, 0, 1>("SS QK N128 warp", 2);
+  run<128, 3, 256, 0, 1, 0, 1>("SS QK + TS PV (indep.)", 1);
+  run<128, 9, 512, 0, 1, 0, 1>("1 tile QK->PV (RAW on S)", 1);
+  run<128, 6, 512, 0, 1, 0, 1>("1 tile PV->QK (WAR on S)", 1);
+  run<128, 7, 512, 0, 1, 0, 1>("2 tiles PV0 QK0 PV1 QK1", 1);
+  run<128, 8, 512, 0, 1, 0, 1>("2 tiles PV0 PV1 QK0 QK1", 1);
   return 0;
 }

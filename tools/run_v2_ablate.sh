@@ -1,0 +1,4 @@
+# two-tile kernel ablations under ncu (cycles are clock-independent)
+for dbg in 0 1 2 3; do
+  TCB_CARVE_V2=1 TCB_CARVE_DEBUG=$dbg timeout 300 ncu --metrics gpu__time_duration.sum,sm__cycles_elapsed.avg,gpc__cycles_elapsed.avg.per_second,sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active --clock-control none -k regex:k_carve_tc -s 3 -c 1 python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e 2>&1 | grep -E "gpu__|sm__|gpc__" | sed "s/^/dbg=$dbg /"
+done
