@@ -429,7 +429,6 @@ struct KvList {
   const int32_t* list;
   int n, lane, chunk, cache;
   __device__ KvList(const int32_t* l, int n_, int lane_) : list(l), n(n_), lane(lane_), chunk(-1), cache(0) {}
-  __device__ KvList() : list(nullptr), n(0), lane(threadIdx.x & 31), chunk(-1), cache(0) {}
   __device__ __forceinline__ int block(int j) {
     if (!list) return j;
     const int c = j >> 5;
@@ -576,35 +575,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       ++gk;
       ++gs;
     };
-    // S(gs), S(gs+1) with the two MMAs of each k-step back to back on the same Q slice:
-    // the tensor core reuses the A operand, so the pair reads Q from shared memory once
-    // (tests/native/mma_rate.cu MODE 5: full rate vs 67 % for lone SS N=64 MMAs).
-    auto issue_pair = [&]() {
-      const int sl0 = gk % K_SLOTS, sl1 = (gk + 1) % K_SLOTS;
-      ptx::mbar_wait(&bars->k_full[sl0], (gk / K_SLOTS) & 1);
-      ptx::mbar_wait(&bars->k_full[sl1], ((gk + 1) / K_SLOTS) & 1);
-      ptx::tc_fence_after();
-      const uint32_t kb0 = aK + sl0 * L::HALF_BYTES, kb1 = aK + sl1 * L::HALF_BYTES;
-      if (ptx::elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t qoff = (kk >> 2) * L::Q_CHUNK + (kk & 3) * 32;
-          const uint32_t koff = (kk >> 2) * L::H_CHUNK + (kk & 3) * 32;
-          const uint64_t qd = make_sdesc(aQ + qoff, 16, 1024);
-          ptx::mma_ss(tmem + (gs & 1) * HN, qd, make_sdesc(kb0 + koff, 16, 1024), IDESC_S,
-                      kk > 0 ? 1u : 0u);
-          ptx::mma_ss(tmem + ((gs + 1) & 1) * HN, qd, make_sdesc(kb1 + koff, 16, 1024), IDESC_S,
-                      kk > 0 ? 1u : 0u);
-        }
-        ptx::mma_commit(&bars->k_empty[sl0]);
-        ptx::mma_commit(&bars->k_empty[sl1]);
-        ptx::mma_commit(&bars->s_full[gs & 1]);
-        ptx::mma_commit(&bars->s_full[(gs + 1) & 1]);
-      }
-      __syncwarp();
-      gk += 2;
-      gs += 2;
-    };
     for (;; ++it) {
       const int slot = it & 1;
       ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
@@ -626,12 +596,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         __syncwarp();
         continue;
       }
-      const bool pair = (dbg & 4) != 0;
-      if (pair) issue_pair(); else issue_s();
+      issue_s();
       for (int t = 0; t < T; ++t) {
-        if (pair) {
-          // paired issue: S(t+1), S(t+2) once PV(t-1) and PV(t) are queued (both S buffers free)
-        } else if (t + 1 < T) {
+        if (t + 1 < T) {
           issue_s();
           if (t + 2 == T) {
             if (ptx::elect_one()) ptx::mma_commit(&bars->q_empty);
@@ -658,17 +625,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         __syncwarp();
         ++gv;
         ++gp;
-        if (pair && (t & 1) && t + 1 < T) {
-          issue_pair();
-          if (t + 3 == T) {
-            if (ptx::elect_one()) ptx::mma_commit(&bars->q_empty);
-            __syncwarp();
-          }
-        }
-      }
-      if (pair && T == 2) {
-        if (ptx::elect_one()) ptx::mma_commit(&bars->q_empty);
-        __syncwarp();
       }
       if (ptx::elect_one()) ptx::mma_commit(&bars->o_full);
       __syncwarp();
@@ -812,1567 +768,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
 }
 
 }  // namespace tc
-
-// =====================================================================================
-// tcgen05 kernel, two-tile variant: one CTA per SM holding TWO independent query tiles
-// (two work items, each its own (head, q-block) and kv list).  Each tile owns 256 TMEM
-// columns: S [0,128) for a full 128-key block, O [128, 256).  The MMA warp alternates the
-// tiles turn by turn -- QK0(0) QK1(0) | PV0(0) QK0(1) | PV1(0) QK1(1) | PV0(1) QK0(2) ... --
-// so one tile's softmax always overlaps the other tile's MMAs.  QK^T for a 128-key block
-// is one N=128 MMA per k-step (a lone SS N=64 MMA is shared-memory-port bound at 67 %).
-// K and V arrive as full 128-key tiles through ONE ring in the MMA's consumption order, so
-// the producer can run ahead by the whole ring.
-// =====================================================================================
-namespace tc2 {
-
-using tc::BM;
-using tc::BK;
-using tc::HN;
-// NT query tiles per CTA: NT = 2 -> one CTA per SM, one MMA warp alternating both tiles;
-// NT = 1 -> two CTAs per SM, each an independent tile pipeline (two MMA issuers per SM).
-template <int NT>
-struct Cfg {
-  static constexpr int NUM_THREADS = 64 + 128 * NT;  // w0 TMA+scheduler, w1 MMA, 4 warps/tile
-  static constexpr int TMEM_COLS = 256 * NT;         // tile a: S [256a, +128), O [256a+128, +128)
-  static constexpr int MAX_SMEM = NT == 2 ? 232448 : 115712;  // per CTA at 1 / 2 CTAs per SM
-};
-constexpr float RESCALE_THRESHOLD = 8.0f;
-
-template <int D, int NT>
-struct Smem {
-  static constexpr int Q_BYTES = BM * D * 2;
-  static constexpr int TILE_BYTES = BK * D * 2;   // one K or V block
-  static constexpr int CHUNKS = D / 64;
-  static constexpr int CHUNK = BM * 128;          // bytes per 64-col (128 B swizzle) chunk
-  static constexpr int BAR_BYTES = 1024;
-  static constexpr int R0 = (Cfg<NT>::MAX_SMEM - BAR_BYTES - NT * Q_BYTES) / TILE_BYTES;
-  static constexpr int RING = R0 > 16 ? 16 : R0;  // K/V tiles in flight
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_RING = NT * Q_BYTES;
-  static constexpr int OFF_BAR = OFF_RING + RING * TILE_BYTES;
-  static constexpr int BYTES = OFF_BAR + BAR_BYTES;
-};
-
-struct Bars {
-  uint64_t q_full[2], q_empty[2], s_full[2], p_full[2], o_full[2], o_empty[2];
-  uint64_t sched_full[2][2], sched_empty[2][2];
-  uint64_t r_full[16], r_empty[16];
-  int sched_item[2][2];
-  uint32_t tmem_base;
-};
-static_assert(sizeof(Bars) <= 1024, "barrier block must fit the reserved smem");
-
-// Per-tile progress of the turn schedule; the producer and the MMA warp step identical
-// copies of it so they agree on the ring order without talking to each other.
-struct TileState {
-  int n = 0, j = 0;        // steps of the current item, next QK step
-  bool pending = false;    // a QK was issued whose PV has not been
-  bool active = true;
-  uint32_t items = 0;      // items taken (incl. empty ones): sched ring / o_full phases
-  uint32_t qloads = 0;     // items with n > 0: Q ring phases
-};
-
-// Debug timeline (TCB_CARVE_DEBUG bit 3): CTA 0 records (event, step, clock) so the
-// pipeline's critical path can be read without a profiler.  Off in production.
-constexpr int TRACE_EV = 24, TRACE_STEPS = 4096;
-__device__ unsigned long long g_trace[TRACE_EV][TRACE_STEPS];  // clock per (event, step)
-__device__ __forceinline__ void trace(int dbg, int ev, int step) {
-  if ((dbg & 8) && blockIdx.x == 0 && step < TRACE_STEPS) g_trace[ev][step] = clock64();
-}
-
-template <int D, int NT, typename E = __nv_bfloat16>
-__global__ void __launch_bounds__(Cfg<NT>::NUM_THREADS, 3 - NT)
-    k_carve_tc2(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                const __grid_constant__ CUtensorMap tm_v, E* __restrict__ o, CarveShape s,
-                const int32_t* __restrict__ kv_idx, const int32_t* __restrict__ kv_cnt,
-                int* __restrict__ counter, int total_items, float scale_log2, float beta_log2,
-                int dbg) {
-  using L = Smem<D, NT>;
-  constexpr int TMEM_COLS = Cfg<NT>::TMEM_COLS;
-  constexpr int RING = L::RING;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sQ = smem + L::OFF_Q;
-  uint8_t* sR = smem + L::OFF_RING;
-  Bars* bars = reinterpret_cast<Bars*>(smem + L::OFF_BAR);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    if (ptx::smem_u32(smem) & 1023u) __trap();
-    for (int a = 0; a < NT; ++a) {
-      ptx::mbar_init(&bars->q_full[a], 1);
-      ptx::mbar_init(&bars->q_empty[a], 1);
-      ptx::mbar_init(&bars->s_full[a], 1);
-      ptx::mbar_init(&bars->p_full[a], 128);
-      ptx::mbar_init(&bars->o_full[a], 1);
-      ptx::mbar_init(&bars->o_empty[a], 128);
-      for (int i = 0; i < 2; ++i) {
-        ptx::mbar_init(&bars->sched_full[a][i], 1);
-        ptx::mbar_init(&bars->sched_empty[a][i], 2);  // MMA warp + the tile's softmax group
-      }
-    }
-    for (int i = 0; i < RING; ++i) {
-      ptx::mbar_init(&bars->r_full[i], 1);
-      ptx::mbar_init(&bars->r_empty[i], 1);
-    }
-    ptx::fence_mbar_init();
-    ptx::tma_prefetch_desc(&tm_q);
-    ptx::tma_prefetch_desc(&tm_k);
-    ptx::tma_prefetch_desc(&tm_v);
-  }
-  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(&bars->tmem_base);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
-
-  if (warp == 0) {
-    // ============================ TMA producer + scheduler ============================
-    const uint64_t pol_kv = ptx::policy_evict_last();
-    const uint64_t pol_q = ptx::policy_evict_first();
-    TileState ts[NT];
-    tc::KvList kl[NT];
-    int head[NT] = {0}, qblk[NT] = {0};
-    bool visr[NT] = {false};
-    uint32_t gr = 0;
-    auto load_tile = [&](int a, int b, bool is_v) {
-      if (lane == 0) {
-        const int sl = gr % RING;
-        ptx::mbar_wait(&bars->r_empty[sl], ((gr / RING) & 1) ^ 1);
-        if ((dbg & 1) && gr >= (uint32_t)RING) {  // timing experiment: no operand traffic
-          ptx::mbar_arrive(&bars->r_full[sl]);
-        } else {
-          ptx::mbar_arrive_expect_tx(&bars->r_full[sl], L::TILE_BYTES);
-#pragma unroll
-          for (int c = 0; c < L::CHUNKS; ++c)
-            ptx::tma_load_3d(sR + sl * L::TILE_BYTES + c * L::CHUNK, is_v ? &tm_v : &tm_k,
-                             &bars->r_full[sl], c * 64, b * BK, head[a], visr[a] ? pol_kv : pol_q);
-        }
-      }
-      ++gr;
-    };
-    while (ts[0].active || (NT == 2 && ts[NT - 1].active)) {
-#pragma unroll
-      for (int a = 0; a < NT; ++a) {
-        TileState& t = ts[a];
-        if (!t.active) continue;
-        if (t.pending) {  // V tile of the step whose PV comes next
-          load_tile(a, kl[a].block(t.j - 1), true);
-          t.pending = false;
-        }
-        while (t.j == t.n) {  // take the next item for this tile
-          const int slot = t.items & 1;
-          int item = 0;
-          if (lane == 0) {
-            ptx::mbar_wait(&bars->sched_empty[a][slot], ((t.items >> 1) & 1) ^ 1);
-            item = atomicAdd(counter, 1);
-            if (item >= total_items) item = -1;
-            bars->sched_item[a][slot] = item;
-            ptx::mbar_arrive(&bars->sched_full[a][slot]);
-          }
-          item = __shfl_sync(0xffffffffu, item, 0);
-          ++t.items;
-          if (item < 0) {
-            t.active = false;
-            break;
-          }
-          int h, qb;
-          decode_item(item, s, h, qb);
-          const bool vis = qb < s.M_v;
-          t.n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-          t.j = 0;
-          head[a] = h;
-          qblk[a] = qb;
-          visr[a] = vis;
-          kl[a] = tc::KvList(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, t.n,
-                             lane);
-          if (t.n > 0) {
-            if (lane == 0) {
-              ptx::mbar_wait(&bars->q_empty[a], (t.qloads & 1) ^ 1);
-              ptx::mbar_arrive_expect_tx(&bars->q_full[a], L::Q_BYTES);
-#pragma unroll
-              for (int c = 0; c < L::CHUNKS; ++c)
-                ptx::tma_load_3d(sQ + a * L::Q_BYTES + c * L::CHUNK, &tm_q, &bars->q_full[a],
-                                 c * 64, qb * BM, h, pol_q);
-            }
-            ++t.qloads;
-          }
-        }
-        if (!t.active) continue;
-        load_tile(a, kl[a].block(t.j), false);  // K tile of the next QK
-        ++t.j;
-        t.pending = true;
-      }
-    }
-  } else if (warp == 1) {
-    // ============================ MMA issuer ============================
-    constexpr uint32_t IDESC_S = tc::make_idesc(BM, BK, 0, tc::Elem<E>::kBf16);
-    constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, 1, tc::Elem<E>::kBf16);
-    const uint32_t aQ = ptx::smem_u32(sQ), aR = ptx::smem_u32(sR);
-    TileState ts[NT];
-    uint32_t gr = 0, gp[NT] = {0}, gq[NT] = {0};
-    auto take = [&]() {  // next ring slot (in consumption order), waited full
-      const int sl = gr % RING;
-      ptx::mbar_wait(&bars->r_full[sl], (gr / RING) & 1);
-      ++gr;
-      return sl;
-    };
-    while (ts[0].active || (NT == 2 && ts[NT - 1].active)) {
-#pragma unroll
-      for (int a = 0; a < NT; ++a) {
-        TileState& t = ts[a];
-        if (!t.active) continue;
-        const uint32_t s_col = tmem + a * 256, o_col = s_col + 128;
-        if (t.pending) {  // ---- O += P(j-1) V(j-1), A = P from TMEM (64 packed columns)
-          if (t.j == 1 && t.items > 1) {  // O still holds the previous item until its epilogue
-            ptx::mbar_wait(&bars->o_empty[a], (t.items - 2) & 1);
-          }
-          if (lane == 0) trace(dbg, 1 + a, gp[a]);
-          ptx::mbar_wait(&bars->p_full[a], gp[a] & 1);
-          if (lane == 0) trace(dbg, 3 + a, gp[a]);
-          ++gp[a];
-          const int vt = take();
-          if (lane == 0) trace(dbg, 16 + a, gp[a] - 1);
-          ptx::tc_fence_after();
-          if (ptx::elect_one()) {
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint32_t vb = aR + vt * L::TILE_BYTES + kk * 16 * 128;
-              ptx::mma_ts(o_col, s_col + kk * 8, tc::make_sdesc(vb, L::CHUNK, 1024), IDESC_O,
-                          (t.j > 1 || kk > 0) ? 1u : 0u);
-            }
-            ptx::mma_commit(&bars->r_empty[vt]);
-            if (t.j == t.n) ptx::mma_commit(&bars->o_full[a]);
-          }
-          __syncwarp();
-          if (lane == 0) trace(dbg, 20 + a, gp[a] - 1);
-          t.pending = false;
-        }
-        while (t.j == t.n) {
-          const int slot = t.items & 1;
-          ptx::mbar_wait(&bars->sched_full[a][slot], (t.items >> 1) & 1);
-          // broadcast so the compiler sees warp-uniform values: descriptors built from them
-          // stay in uniform registers (no per-MMA R2UR/ELECT waterfall)
-          const int item = __shfl_sync(0xffffffffu, bars->sched_item[a][slot], 0);
-          if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[a][slot]);
-          ++t.items;
-          if (item < 0) {
-            t.active = false;
-            break;
-          }
-          int h, qb;
-          decode_item(item, s, h, qb);
-          const bool vis = qb < s.M_v;
-          t.n = __shfl_sync(0xffffffffu, vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total, 0);
-          t.j = 0;
-          if (t.n == 0) {  // cannot come from build_block_mask; keep the epilogue in step
-            if (t.items > 1) ptx::mbar_wait(&bars->o_empty[a], (t.items - 2) & 1);
-            if (ptx::elect_one()) ptx::mma_commit(&bars->o_full[a]);
-            __syncwarp();
-          } else {
-            ptx::mbar_wait(&bars->q_full[a], t.qloads & 1);
-            ++t.qloads;
-          }
-        }
-        if (!t.active) continue;
-        // ---- S = Q K(j)^T, M = N = 128
-        if (lane == 0) trace(dbg, 7 + a, gq[a]);
-        const int kt = take();
-        if (lane == 0) trace(dbg, 5 + a, gq[a]);
-        ++gq[a];
-        ptx::tc_fence_after();
-        const uint32_t qa = aQ + a * L::Q_BYTES, kb = aR + kt * L::TILE_BYTES;
-        if (ptx::elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * L::CHUNK + (kk & 3) * 32;
-            ptx::mma_ss(s_col, tc::make_sdesc(qa + off, 16, 1024), tc::make_sdesc(kb + off, 16, 1024),
-                        IDESC_S, kk > 0 ? 1u : 0u);
-          }
-          ptx::mma_commit(&bars->r_empty[kt]);
-          ptx::mma_commit(&bars->s_full[a]);
-          if (t.j + 1 == t.n) ptx::mma_commit(&bars->q_empty[a]);
-        }
-        __syncwarp();
-        if (lane == 0) trace(dbg, 18 + a, gq[a] - 1);
-        ++t.j;
-        t.pending = true;
-      }
-    }
-  } else {
-    // ============================ softmax / correction / epilogue ============================
-    const int a = (warp - 2) >> 2;  // tile of this warp group
-    const int quarter = warp & 3;   // TMEM lane quarter this warp may access
-    const int row = quarter * 32 + lane;
-    const uint32_t t_row = tmem + a * 256 + ((uint32_t)(quarter * 32) << 16);
-    const uint32_t s_col = 0, o_col = 128;
-    uint32_t it = 0, g = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&bars->sched_full[a][slot], (it >> 1) & 1);
-      const int item = bars->sched_item[a][slot];
-      ptx::named_bar_sync(1 + a, 128);  // all 128 threads read the slot before it is released
-      if (threadIdx.x == 64 + a * 128) ptx::mbar_arrive(&bars->sched_empty[a][slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      float m_run = -INFINITY, l_run = 0.f;
-      for (int j = 0; j < n; ++j, ++g) {
-        const int b = kl.block(j);
-        const int kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond);
-        const float bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
-        if (lane == 0 && (warp & 3) == 2) trace(dbg, 10 + a, g);
-        ptx::mbar_wait(&bars->s_full[a], g & 1);
-        if (lane == 0 && (warp & 3) == 2) trace(dbg, 12 + a, g);
-        ptx::tc_fence_after();
-        if (dbg & 2) {  // timing experiment: no softmax work
-          l_run = 1.f;
-          ptx::mbar_arrive(&bars->p_full[a]);
-          continue;
-        }
-        uint32_t sr[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          ptx::tmem_ld32(t_row + s_col + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
-        ptx::tmem_wait_ld();
-        if (kvalid < BK) {  // padding keys of a partial block -> -inf (attention.py:193)
-#pragma unroll
-          for (int e = 0; e < 128; ++e)
-            if (e >= kvalid) sr[e] = __float_as_uint(-INFINITY);
-        }
-        float mx8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
-#pragma unroll
-        for (int e = 8; e < 120; e += 16)
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            mx8[q] = tc::fmax3(mx8[q], __uint_as_float(sr[e + q]), __uint_as_float(sr[e + 8 + q]));
-#pragma unroll
-        for (int q = 0; q < 8; ++q) mx8[q] = fmaxf(mx8[q], __uint_as_float(sr[120 + q]));
-        const float mraw = tc::fmax3(tc::fmax3(mx8[0], mx8[1], mx8[2]),
-                                     tc::fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-        const float m_blk = (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
-        const float m_new = fmaxf(m_run, m_blk);
-        const bool first = (j == 0);
-        const bool need = !first && (m_new > m_run + RESCALE_THRESHOLD);
-        const float m_use = (first || need) ? m_new : m_run;
-        const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
-        const float c0 = bias - m_use;
-        const uint64_t sc2 = tc::f2_pack(scale_log2, scale_log2), c02 = tc::f2_pack(c0, c0);
-        uint64_t acc2[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {  // 32 keys -> 16 packed columns per store
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int k = 32 * c + 2 * e;
-            const uint64_t x = tc::ffma2(
-                tc::f2_pack(__uint_as_float(sr[k]), __uint_as_float(sr[k + 1])), sc2, c02);
-            const float p0 = ptx::ex2(tc::f2_lo(x)), p1 = ptx::ex2(tc::f2_hi(x));
-            acc2[e & 3] = tc::fadd2(acc2[e & 3], tc::f2_pack(p0, p1));
-            pk[e] = tc::Elem<E>::pack(p0, p1);
-          }
-          ptx::tmem_st16(t_row + s_col + 16 * c, pk);
-        }
-        const uint64_t sum2 = tc::fadd2(tc::fadd2(acc2[0], acc2[1]), tc::fadd2(acc2[2], acc2[3]));
-        l_run = l_run * alpha + (tc::f2_lo(sum2) + tc::f2_hi(sum2));
-        m_run = m_use;
-        if (__any_sync(0xffffffffu, need)) {
-          // PV(j-1) retired before S(j) was committed (same issuing thread, in order)
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            ptx::tmem_ld32(t_row + o_col + c * 32, ov);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            ptx::tmem_st32(t_row + o_col + c * 32, ov);
-          }
-        }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars->p_full[a]);
-        if (lane == 0 && (warp & 3) == 2) trace(dbg, 14 + a, g);
-      }
-      // ---- epilogue: O / l -> row, padding rows zero (attention.py:203-206)
-      ptx::mbar_wait(&bars->o_full[a], it & 1);
-      ptx::tc_fence_after();
-      const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
-      const float inv_l = (row < qvalid && n > 0) ? 1.f / l_run : 0.f;
-      E* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t ov[32];
-        ptx::tmem_ld32(t_row + o_col + c * 32, ov);
-        ptx::tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pk[e] = n > 0 ? tc::Elem<E>::pack(__uint_as_float(ov[2 * e]) * inv_l,
-                                            __uint_as_float(ov[2 * e + 1]) * inv_l)
-                        : 0u;
-        int4* dst = reinterpret_cast<int4*>(orow + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          __stcs(dst + e, make_int4((int)pk[4 * e], (int)pk[4 * e + 1], (int)pk[4 * e + 2],
-                                    (int)pk[4 * e + 3]));
-      }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&bars->o_empty[a]);
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<TMEM_COLS>(tmem);
-  }
-}
-
-}  // namespace tc2
-
-// =====================================================================================
-// tcgen05 kernel, full-block steps with split issue (TCB_CARVE_V2=3 while under test).
-// Two CTAs per SM, each one query tile with S [0,128) (a full 128-key block) and
-// O [128, 256) in TMEM, so every QK^T runs at N = 128 (full tensor rate; N = 64 is
-// shared-memory-port bound at 67 %) and the two CTAs' MMA warps keep the pipe fed.  The
-// per-tile chain QK -> softmax -> PV -> QK is shortened by splitting both ends:
-//   * as soon as the softmax warps have S(j) in registers (s_read), the MMA warp computes
-//     keys 64..127 of S(j+1) into columns [64,128) -- P(j) only occupies [0,64);
-//   * P(j) is published in two halves (p_half[0], p_half[1]); PV(j) over keys 0..63 runs
-//     while the softmax computes keys 64..127;
-//   * after PV(j) the MMA warp fills keys 0..63 of S(j+1) over P(j)'s columns.
-// O rescales (lazy, threshold 8) happen before the first half of P(j) is published, so
-// they never race PV(j).
-// =====================================================================================
-namespace tc3 {
-
-using tc::BM;
-using tc::BK;
-using tc::HN;
-constexpr int NUM_THREADS = 192;  // w0 TMA+scheduler, w1 MMA+TMEM owner, w2..5 softmax
-constexpr int TMEM_COLS = 256;
-constexpr int MAX_SMEM = 115712;  // per CTA at two CTAs per SM
-constexpr float RESCALE_THRESHOLD = 8.0f;
-
-template <int D>
-struct Smem {
-  static constexpr int Q_BYTES = BM * D * 2;
-  static constexpr int TILE_BYTES = BK * D * 2;
-  static constexpr int CHUNKS = D / 64;
-  static constexpr int CHUNK = BM * 128;
-  static constexpr int BAR_BYTES = 512;
-  static constexpr int R0 = (MAX_SMEM - BAR_BYTES - Q_BYTES) / TILE_BYTES;
-  static constexpr int RING = R0 > 8 ? 8 : R0;  // K/V tiles in flight (2 at d = 128)
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_RING = Q_BYTES;
-  static constexpr int OFF_BAR = OFF_RING + RING * TILE_BYTES;
-  static constexpr int BYTES = OFF_BAR + BAR_BYTES;
-};
-
-struct Bars {
-  uint64_t q_full, q_empty, s_full, s_read, o_full, o_empty;
-  uint64_t p_half[2];
-  uint64_t sched_full[2], sched_empty[2];
-  uint64_t r_full[8], r_empty[8];
-  int sched_item[2];
-  uint32_t tmem_base;
-};
-static_assert(sizeof(Bars) <= 512, "barrier block must fit the reserved smem");
-
-template <int D, typename E = __nv_bfloat16>
-__global__ void __launch_bounds__(NUM_THREADS, 2)
-    k_carve_tc3(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                const __grid_constant__ CUtensorMap tm_v, E* __restrict__ o, CarveShape s,
-                const int32_t* __restrict__ kv_idx, const int32_t* __restrict__ kv_cnt,
-                int* __restrict__ counter, int total_items, float scale_log2, float beta_log2,
-                int dbg) {
-  using L = Smem<D>;
-  constexpr int RING = L::RING;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sQ = smem + L::OFF_Q;
-  uint8_t* sR = smem + L::OFF_RING;
-  Bars* bars = reinterpret_cast<Bars*>(smem + L::OFF_BAR);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    if (ptx::smem_u32(smem) & 1023u) __trap();
-    ptx::mbar_init(&bars->q_full, 1);
-    ptx::mbar_init(&bars->q_empty, 1);
-    ptx::mbar_init(&bars->s_full, 1);
-    ptx::mbar_init(&bars->s_read, 128);
-    ptx::mbar_init(&bars->o_full, 1);
-    ptx::mbar_init(&bars->o_empty, 128);
-    ptx::mbar_init(&bars->p_half[0], 128);
-    ptx::mbar_init(&bars->p_half[1], 128);
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&bars->sched_full[i], 1);
-      ptx::mbar_init(&bars->sched_empty[i], 2);  // MMA warp + softmax group
-    }
-    for (int i = 0; i < RING; ++i) {
-      ptx::mbar_init(&bars->r_full[i], 1);
-      ptx::mbar_init(&bars->r_empty[i], 1);
-    }
-    ptx::fence_mbar_init();
-    ptx::tma_prefetch_desc(&tm_q);
-    ptx::tma_prefetch_desc(&tm_k);
-    ptx::tma_prefetch_desc(&tm_v);
-  }
-  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(&bars->tmem_base);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
-
-  if (warp == 0) {
-    // ============================ TMA producer + scheduler ============================
-    // Ring order = MMA consumption order: K(0), then K(j+1) before V(j).
-    const uint64_t pol_kv = ptx::policy_evict_last();
-    const uint64_t pol_q = ptx::policy_evict_first();
-    uint32_t it = 0, gr = 0, qloads = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      int item = 0;
-      if (lane == 0) {
-        ptx::mbar_wait(&bars->sched_empty[slot], ((it >> 1) & 1) ^ 1);
-        item = atomicAdd(counter, 1);
-        if (item >= total_items) item = -1;
-        bars->sched_item[slot] = item;
-        ptx::mbar_arrive(&bars->sched_full[slot]);
-      }
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-      if (n == 0) continue;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      const uint64_t pol = vis ? pol_kv : pol_q;
-      if (lane == 0) {
-        ptx::mbar_wait(&bars->q_empty, (qloads & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&bars->q_full, L::Q_BYTES);
-#pragma unroll
-        for (int c = 0; c < L::CHUNKS; ++c)
-          ptx::tma_load_3d(sQ + c * L::CHUNK, &tm_q, &bars->q_full, c * 64, qb * BM, h, pol_q);
-      }
-      ++qloads;
-      auto load = [&](const CUtensorMap* tm, int b) {
-        if (lane == 0) {
-          const int sl = gr % RING;
-          ptx::mbar_wait(&bars->r_empty[sl], ((gr / RING) & 1) ^ 1);
-          if ((dbg & 1) && gr >= (uint32_t)RING) {  // timing experiment: no operand traffic
-            ptx::mbar_arrive(&bars->r_full[sl]);
-          } else {
-            ptx::mbar_arrive_expect_tx(&bars->r_full[sl], L::TILE_BYTES);
-#pragma unroll
-            for (int c = 0; c < L::CHUNKS; ++c)
-              ptx::tma_load_3d(sR + sl * L::TILE_BYTES + c * L::CHUNK, tm, &bars->r_full[sl],
-                               c * 64, b * BK, h, pol);
-          }
-        }
-        ++gr;
-      };
-      load(&tm_k, kl.block(0));
-      for (int j = 0; j < n; ++j) {
-        if (j + 1 < n) load(&tm_k, kl.block(j + 1));
-        load(&tm_v, kl.block(j));
-      }
-    }
-  } else if (warp == 1) {
-    // ============================ MMA issuer ============================
-    constexpr uint32_t IDESC_S = tc::make_idesc(BM, BK, 0, tc::Elem<E>::kBf16);
-    constexpr uint32_t IDESC_H = tc::make_idesc(BM, HN, 0, tc::Elem<E>::kBf16);
-    constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, 1, tc::Elem<E>::kBf16);
-    const uint32_t aQ = ptx::smem_u32(sQ), aR = ptx::smem_u32(sR);
-    const uint32_t s_col = tmem, o_col = tmem + 128;
-    uint32_t it = 0, gr = 0, gs = 0, qloads = 0;
-    auto take = [&]() {
-      const int sl = gr % RING;
-      ptx::mbar_wait(&bars->r_full[sl], (gr / RING) & 1);
-      ++gr;
-      return sl;
-    };
-    // S columns [c0, c0 + N) = Q K^T over key rows [r0, r0 + N) of the K tile in slot kt
-    auto qk = [&](int kt, int r0, uint32_t c0, uint32_t idesc) {
-      const uint32_t kb = aR + kt * L::TILE_BYTES + r0 * 128;
-#pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const uint32_t off = (kk >> 2) * L::CHUNK + (kk & 3) * 32;
-        ptx::mma_ss(s_col + c0, tc::make_sdesc(aQ + off, 16, 1024),
-                    tc::make_sdesc(kb + off, 16, 1024), idesc, kk > 0 ? 1u : 0u);
-      }
-    };
-    // O (+)= P[keys 64h .. 64h+63] V[same keys]
-    auto pv = [&](int vt, int half, bool first) {
-#pragma unroll
-      for (int kk = 4 * half; kk < 4 * half + 4; ++kk) {
-        const uint32_t vb = aR + vt * L::TILE_BYTES + kk * 16 * 128;
-        ptx::mma_ts(o_col, s_col + kk * 8, tc::make_sdesc(vb, L::CHUNK, 1024), IDESC_O,
-                    (!first || kk > 0) ? 1u : 0u);
-      }
-    };
-    for (;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
-      const int item = __shfl_sync(0xffffffffu, bars->sched_item[slot], 0);
-      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = __shfl_sync(0xffffffffu, vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total, 0);
-      if (n == 0) {  // cannot come from build_block_mask; keep the epilogue in step
-        if (it > 0) ptx::mbar_wait(&bars->o_empty, (it - 1) & 1);
-        if (ptx::elect_one()) ptx::mma_commit(&bars->o_full);
-        __syncwarp();
-        continue;
-      }
-      ptx::mbar_wait(&bars->q_full, qloads & 1);
-      ++qloads;
-      int kt = take();
-      ptx::tc_fence_after();
-      if (ptx::elect_one()) {
-        qk(kt, 0, 0, IDESC_S);
-        ptx::mma_commit(&bars->r_empty[kt]);
-        ptx::mma_commit(&bars->s_full);
-        if (n == 1) ptx::mma_commit(&bars->q_empty);
-      }
-      __syncwarp();
-      for (int j = 0; j < n; ++j, ++gs) {
-        const bool more = j + 1 < n;
-        ptx::mbar_wait(&bars->s_read, gs & 1);  // S(j) is in the softmax registers
-        if (more) {
-          kt = take();
-          ptx::tc_fence_after();
-          if (ptx::elect_one()) qk(kt, HN, HN, IDESC_H);  // keys 64..127 of S(j+1)
-          __syncwarp();
-        }
-        ptx::mbar_wait(&bars->p_half[0], gs & 1);
-        if (j == 0 && it > 0) ptx::mbar_wait(&bars->o_empty, (it - 1) & 1);  // epilogue read O
-        const int vt = take();
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) pv(vt, 0, j == 0);
-        __syncwarp();
-        ptx::mbar_wait(&bars->p_half[1], gs & 1);
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          pv(vt, 1, false);
-          ptx::mma_commit(&bars->r_empty[vt]);
-          if (more) {
-            qk(kt, 0, 0, IDESC_H);  // keys 0..63 of S(j+1), over P(j)'s columns
-            ptx::mma_commit(&bars->r_empty[kt]);
-            ptx::mma_commit(&bars->s_full);
-            if (j + 2 == n) ptx::mma_commit(&bars->q_empty);
-          } else {
-            ptx::mma_commit(&bars->o_full);
-          }
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    // ============================ softmax / correction / epilogue ============================
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
-    constexpr uint32_t s_col = 0, o_col = 128;
-    uint32_t it = 0, g = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
-      const int item = bars->sched_item[slot];
-      ptx::named_bar_sync(1, 128);
-      if (threadIdx.x == 64) ptx::mbar_arrive(&bars->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      float m_run = -INFINITY, l_run = 0.f;
-      for (int j = 0; j < n; ++j, ++g) {
-        const int b = kl.block(j);
-        const int kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond);
-        const float bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
-        ptx::mbar_wait(&bars->s_full, g & 1);
-        ptx::tc_fence_after();
-        uint32_t sr[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          ptx::tmem_ld32(t_row + s_col + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
-        ptx::tmem_wait_ld();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars->s_read);
-        if (dbg & 2) {  // timing experiment: no softmax work
-          l_run = 1.f;
-          ptx::mbar_arrive(&bars->p_half[0]);
-          ptx::mbar_arrive(&bars->p_half[1]);
-          continue;
-        }
-        if (kvalid < BK) {  // padding keys of a partial block -> -inf (attention.py:193)
-#pragma unroll
-          for (int e = 0; e < 128; ++e)
-            if (e >= kvalid) sr[e] = __float_as_uint(-INFINITY);
-        }
-        float mx8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
-#pragma unroll
-        for (int e = 8; e < 120; e += 16)
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            mx8[q] = tc::fmax3(mx8[q], __uint_as_float(sr[e + q]), __uint_as_float(sr[e + 8 + q]));
-#pragma unroll
-        for (int q = 0; q < 8; ++q) mx8[q] = fmaxf(mx8[q], __uint_as_float(sr[120 + q]));
-        const float mraw = tc::fmax3(tc::fmax3(mx8[0], mx8[1], mx8[2]),
-                                     tc::fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-        const float m_blk = (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
-        const float m_new = fmaxf(m_run, m_blk);
-        const bool first = (j == 0);
-        const bool need = !first && (m_new > m_run + RESCALE_THRESHOLD);
-        const float m_use = (first || need) ? m_new : m_run;
-        const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
-        if (__any_sync(0xffffffffu, need)) {
-          // PV(j-1) retired before S(j) was committed; PV(j) waits for p_half[0] below
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            ptx::tmem_ld32(t_row + o_col + c * 32, ov);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            ptx::tmem_st32(t_row + o_col + c * 32, ov);
-          }
-        }
-        const float c0 = bias - m_use;
-        const uint64_t sc2 = tc::f2_pack(scale_log2, scale_log2), c02 = tc::f2_pack(c0, c0);
-        uint64_t acc2[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {  // 32 keys -> 16 packed columns per store
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int k = 32 * c + 2 * e;
-            const uint64_t x = tc::ffma2(
-                tc::f2_pack(__uint_as_float(sr[k]), __uint_as_float(sr[k + 1])), sc2, c02);
-            const float p0 = ptx::ex2(tc::f2_lo(x)), p1 = ptx::ex2(tc::f2_hi(x));
-            acc2[e & 3] = tc::fadd2(acc2[e & 3], tc::f2_pack(p0, p1));
-            pk[e] = tc::Elem<E>::pack(p0, p1);
-          }
-          ptx::tmem_st16(t_row + s_col + 16 * c, pk);
-          if (c & 1) {  // keys [0,64) then [64,128) published for PV
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&bars->p_half[c >> 1]);
-          }
-        }
-        const uint64_t sum2 = tc::fadd2(tc::fadd2(acc2[0], acc2[1]), tc::fadd2(acc2[2], acc2[3]));
-        l_run = l_run * alpha + (tc::f2_lo(sum2) + tc::f2_hi(sum2));
-        m_run = m_use;
-      }
-      // ---- epilogue: O / l -> row, padding rows zero (attention.py:203-206)
-      ptx::mbar_wait(&bars->o_full, it & 1);
-      ptx::tc_fence_after();
-      const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
-      const float inv_l = (row < qvalid && n > 0) ? 1.f / l_run : 0.f;
-      E* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t ov[32];
-        ptx::tmem_ld32(t_row + o_col + c * 32, ov);
-        ptx::tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pk[e] = n > 0 ? tc::Elem<E>::pack(__uint_as_float(ov[2 * e]) * inv_l,
-                                            __uint_as_float(ov[2 * e + 1]) * inv_l)
-                        : 0u;
-        int4* dst = reinterpret_cast<int4*>(orow + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          __stcs(dst + e, make_int4((int)pk[4 * e], (int)pk[4 * e + 1], (int)pk[4 * e + 2],
-                                    (int)pk[4 * e + 3]));
-      }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&bars->o_empty);
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<TMEM_COLS>(tmem);
-  }
-}
-
-}  // namespace tc3
-
-// =====================================================================================
-// tcgen05 kernel, two independent tile pipelines per CTA (TCB_CARVE_V2=4 while under test).
-// One CTA per SM; tile a in {0,1} owns producer warp a, MMA warp 2+a, softmax warps
-// 4+4a .. 7+4a, Q slot a, a 2-slot K/V ring and TMEM columns [256a, 256a+256): S [0,128)
-// (a full 128-key block -> QK^T at N = 128, full tensor rate) and O [128,256).  Two MMA
-// issuers keep the tensor pipe fed (a single issuer stalls on its own waits).  PV(j) is
-// split in key halves so PV over keys 0..63 runs while the softmax finishes keys 64..127.
-// Optional (TCB_CARVE_DEBUG bit 4): the two tiles' exp2 phases strictly alternate (MUFU
-// token), so one tile's softmax overlaps the other tile's MMAs instead of its softmax.
-// =====================================================================================
-namespace tc4 {
-
-using tc::BM;
-using tc::BK;
-using tc::HN;
-constexpr int NUM_THREADS = 384;
-constexpr int TMEM_COLS = 512;
-constexpr int MAX_SMEM = 232448;
-constexpr float RESCALE_THRESHOLD = 8.0f;
-
-template <int D>
-struct Smem {
-  static constexpr int Q_BYTES = BM * D * 2;
-  static constexpr int TILE_BYTES = BK * D * 2;
-  static constexpr int CHUNKS = D / 64;
-  static constexpr int CHUNK = BM * 128;
-  static constexpr int BAR_BYTES = 1024;
-  static constexpr int R0 = (MAX_SMEM - BAR_BYTES - 2 * Q_BYTES) / (2 * TILE_BYTES);
-  static constexpr int RING = R0 > 8 ? 8 : R0;  // K/V tiles in flight per tile (2 at d = 128)
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_RING = 2 * Q_BYTES;
-  static constexpr int OFF_BAR = OFF_RING + 2 * RING * TILE_BYTES;
-  static constexpr int BYTES = OFF_BAR + BAR_BYTES;
-};
-
-struct TileBars {
-  uint64_t q_full, q_empty, s_full, o_full, o_empty, exp_done;
-  uint64_t p_half[2];
-  uint64_t sched_full[2], sched_empty[2];
-  uint64_t r_full[8], r_empty[8];
-  int sched_item[2];
-  volatile int finished;
-  uint32_t pad;
-};
-struct Bars {
-  TileBars t[2];
-  uint32_t tmem_base;
-};
-static_assert(sizeof(Bars) <= 1024, "barrier block must fit the reserved smem");
-
-template <int D, typename E = __nv_bfloat16>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    k_carve_tc4(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                const __grid_constant__ CUtensorMap tm_v, E* __restrict__ o, CarveShape s,
-                const int32_t* __restrict__ kv_idx, const int32_t* __restrict__ kv_cnt,
-                int* __restrict__ counter, int total_items, float scale_log2, float beta_log2,
-                int dbg) {
-  using L = Smem<D>;
-  constexpr int RING = L::RING;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  Bars* bars = reinterpret_cast<Bars*>(smem + L::OFF_BAR);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int a = warp < 4 ? (warp & 1) : (warp - 4) >> 2;  // tile of this warp
-  TileBars* tb = &bars->t[a];
-  uint8_t* sQ = smem + L::OFF_Q + a * L::Q_BYTES;
-  uint8_t* sR = smem + L::OFF_RING + a * RING * L::TILE_BYTES;
-
-  if (threadIdx.x == 0) {
-    if (ptx::smem_u32(smem) & 1023u) __trap();
-    for (int i = 0; i < 2; ++i) {
-      TileBars* b = &bars->t[i];
-      ptx::mbar_init(&b->q_full, 1);
-      ptx::mbar_init(&b->q_empty, 1);
-      ptx::mbar_init(&b->s_full, 1);
-      ptx::mbar_init(&b->o_full, 1);
-      ptx::mbar_init(&b->o_empty, 128);
-      ptx::mbar_init(&b->exp_done, 128);
-      ptx::mbar_init(&b->p_half[0], 128);
-      ptx::mbar_init(&b->p_half[1], 128);
-      for (int k = 0; k < 2; ++k) {
-        ptx::mbar_init(&b->sched_full[k], 1);
-        ptx::mbar_init(&b->sched_empty[k], 2);
-      }
-      for (int k = 0; k < RING; ++k) {
-        ptx::mbar_init(&b->r_full[k], 1);
-        ptx::mbar_init(&b->r_empty[k], 1);
-      }
-      b->finished = 0;
-    }
-    ptx::fence_mbar_init();
-    ptx::tma_prefetch_desc(&tm_q);
-    ptx::tma_prefetch_desc(&tm_k);
-    ptx::tma_prefetch_desc(&tm_v);
-  }
-  if (warp == 2) ptx::tmem_alloc<TMEM_COLS>(&bars->tmem_base);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = bars->tmem_base + a * 256;
-
-  if (warp < 2) {
-    // ============================ TMA producer + scheduler (tile a) ============================
-    const uint64_t pol_kv = ptx::policy_evict_last();
-    const uint64_t pol_q = ptx::policy_evict_first();
-    uint32_t it = 0, gr = 0, qloads = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      int item = 0;
-      if (lane == 0) {
-        ptx::mbar_wait(&tb->sched_empty[slot], ((it >> 1) & 1) ^ 1);
-        item = atomicAdd(counter, 1);
-        if (item >= total_items) item = -1;
-        tb->sched_item[slot] = item;
-        ptx::mbar_arrive(&tb->sched_full[slot]);
-      }
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-      if (n == 0) continue;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      const uint64_t pol = vis ? pol_kv : pol_q;
-      if (lane == 0) {
-        ptx::mbar_wait(&tb->q_empty, (qloads & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&tb->q_full, L::Q_BYTES);
-#pragma unroll
-        for (int c = 0; c < L::CHUNKS; ++c)
-          ptx::tma_load_3d(sQ + c * L::CHUNK, &tm_q, &tb->q_full, c * 64, qb * BM, h, pol_q);
-      }
-      ++qloads;
-      for (int j = 0; j < n; ++j) {  // ring order = consumption order: K(j), V(j)
-        const int b = kl.block(j);
-#pragma unroll
-        for (int kv = 0; kv < 2; ++kv) {
-          if (lane == 0) {
-            const int sl = gr % RING;
-            ptx::mbar_wait(&tb->r_empty[sl], ((gr / RING) & 1) ^ 1);
-            if ((dbg & 1) && gr >= (uint32_t)RING) {  // timing experiment: no operand traffic
-              ptx::mbar_arrive(&tb->r_full[sl]);
-            } else {
-              ptx::mbar_arrive_expect_tx(&tb->r_full[sl], L::TILE_BYTES);
-#pragma unroll
-              for (int c = 0; c < L::CHUNKS; ++c)
-                ptx::tma_load_3d(sR + sl * L::TILE_BYTES + c * L::CHUNK, kv ? &tm_v : &tm_k,
-                                 &tb->r_full[sl], c * 64, b * BK, h, pol);
-            }
-          }
-          ++gr;
-        }
-      }
-    }
-  } else if (warp < 4) {
-    // ============================ MMA issuer (tile a) ============================
-    constexpr uint32_t IDESC_S = tc::make_idesc(BM, BK, 0, tc::Elem<E>::kBf16);
-    constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, 1, tc::Elem<E>::kBf16);
-    const uint32_t aQ = ptx::smem_u32(sQ), aR = ptx::smem_u32(sR);
-    const uint32_t s_col = tmem, o_col = tmem + 128;
-    uint32_t it = 0, gr = 0, gs = 0, qloads = 0;
-    auto take = [&]() {
-      const int sl = gr % RING;
-      ptx::mbar_wait(&tb->r_full[sl], (gr / RING) & 1);
-      ++gr;
-      return sl;
-    };
-    for (;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&tb->sched_full[slot], (it >> 1) & 1);
-      const int item = __shfl_sync(0xffffffffu, tb->sched_item[slot], 0);
-      if (lane == 0) ptx::mbar_arrive(&tb->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = __shfl_sync(0xffffffffu, vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total, 0);
-      if (n == 0) {  // cannot come from build_block_mask; keep the epilogue in step
-        if (it > 0) ptx::mbar_wait(&tb->o_empty, (it - 1) & 1);
-        if (ptx::elect_one()) ptx::mma_commit(&tb->o_full);
-        __syncwarp();
-        continue;
-      }
-      ptx::mbar_wait(&tb->q_full, qloads & 1);
-      ++qloads;
-      for (int j = 0; j < n; ++j, ++gs) {
-        const int kt = take();
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) {  // S = Q K(j)^T, M = N = 128 (after PV(j-1): in order)
-          const uint32_t kb = aR + kt * L::TILE_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * L::CHUNK + (kk & 3) * 32;
-            ptx::mma_ss(s_col, tc::make_sdesc(aQ + off, 16, 1024), tc::make_sdesc(kb + off, 16, 1024),
-                        IDESC_S, kk > 0 ? 1u : 0u);
-          }
-          ptx::mma_commit(&tb->r_empty[kt]);
-          ptx::mma_commit(&tb->s_full);
-          if (j + 1 == n) ptx::mma_commit(&tb->q_empty);
-        }
-        __syncwarp();
-        const int vt = take();
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {  // O (+)= P V over keys [64 half, 64 half + 64)
-          ptx::mbar_wait(&tb->p_half[half], gs & 1);
-          if (half == 0 && j == 0 && it > 0) ptx::mbar_wait(&tb->o_empty, (it - 1) & 1);
-          ptx::tc_fence_after();
-          if (ptx::elect_one()) {
-#pragma unroll
-            for (int kk = 4 * half; kk < 4 * half + 4; ++kk) {
-              const uint32_t vb = aR + vt * L::TILE_BYTES + kk * 16 * 128;
-              ptx::mma_ts(o_col, s_col + kk * 8, tc::make_sdesc(vb, L::CHUNK, 1024), IDESC_O,
-                          (j > 0 || kk > 0) ? 1u : 0u);
-            }
-            if (half == 1) {
-              ptx::mma_commit(&tb->r_empty[vt]);
-              if (j + 1 == n) ptx::mma_commit(&tb->o_full);
-            }
-          }
-          __syncwarp();
-        }
-      }
-    }
-  } else {
-    // ============================ softmax / correction / epilogue (tile a) ============================
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
-    constexpr uint32_t s_col = 0, o_col = 128;
-    const bool token = (dbg & 16) != 0;
-    TileBars* other = &bars->t[a ^ 1];
-    uint32_t it = 0, g = 0;
-    for (;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&tb->sched_full[slot], (it >> 1) & 1);
-      const int item = tb->sched_item[slot];
-      ptx::named_bar_sync(1 + a, 128);
-      if (threadIdx.x == 128 + 128 * a) ptx::mbar_arrive(&tb->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      float m_run = -INFINITY, l_run = 0.f;
-      for (int j = 0; j < n; ++j, ++g) {
-        const int b = kl.block(j);
-        const int kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond);
-        const float bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
-        ptx::mbar_wait(&tb->s_full, g & 1);
-        ptx::tc_fence_after();
-        uint32_t sr[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          ptx::tmem_ld32(t_row + s_col + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
-        ptx::tmem_wait_ld();
-        if (dbg & 2) {  // timing experiment: no softmax work
-          l_run = 1.f;
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&tb->p_half[0]);
-          ptx::mbar_arrive(&tb->p_half[1]);
-          continue;
-        }
-        if (kvalid < BK) {  // padding keys of a partial block -> -inf (attention.py:193)
-#pragma unroll
-          for (int e = 0; e < 128; ++e)
-            if (e >= kvalid) sr[e] = __float_as_uint(-INFINITY);
-        }
-        float mx8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
-#pragma unroll
-        for (int e = 8; e < 120; e += 16)
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            mx8[q] = tc::fmax3(mx8[q], __uint_as_float(sr[e + q]), __uint_as_float(sr[e + 8 + q]));
-#pragma unroll
-        for (int q = 0; q < 8; ++q) mx8[q] = fmaxf(mx8[q], __uint_as_float(sr[120 + q]));
-        const float mraw = tc::fmax3(tc::fmax3(mx8[0], mx8[1], mx8[2]),
-                                     tc::fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-        const float m_blk = (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
-        const float m_new = fmaxf(m_run, m_blk);
-        const bool first = (j == 0);
-        const bool need = !first && (m_new > m_run + RESCALE_THRESHOLD);
-        const float m_use = (first || need) ? m_new : m_run;
-        const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
-        if (__any_sync(0xffffffffu, need)) {
-          // PV(j-1) retired before S(j) was committed; PV(j) waits for p_half[0] below
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            ptx::tmem_ld32(t_row + o_col + c * 32, ov);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            ptx::tmem_st32(t_row + o_col + c * 32, ov);
-          }
-        }
-        if (token && !(a == 0 && g == 0)) {  // MUFU token: tiles' exp2 phases alternate
-          const uint32_t k = a == 0 ? g - 1 : g;
-          while (!ptx::mbar_try_wait(&other->exp_done, k & 1))
-            if (other->finished) break;
-        }
-        const float c0 = bias - m_use;
-        const uint64_t sc2 = tc::f2_pack(scale_log2, scale_log2), c02 = tc::f2_pack(c0, c0);
-        uint64_t acc2[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {  // 32 keys -> 16 packed columns per store
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int k = 32 * c + 2 * e;
-            const uint64_t x = tc::ffma2(
-                tc::f2_pack(__uint_as_float(sr[k]), __uint_as_float(sr[k + 1])), sc2, c02);
-            const float p0 = ptx::ex2(tc::f2_lo(x)), p1 = ptx::ex2(tc::f2_hi(x));
-            acc2[e & 3] = tc::fadd2(acc2[e & 3], tc::f2_pack(p0, p1));
-            pk[e] = tc::Elem<E>::pack(p0, p1);
-          }
-          ptx::tmem_st16(t_row + s_col + 16 * c, pk);
-          if (c & 1) {  // keys [0,64) then [64,128) published for PV
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&tb->p_half[c >> 1]);
-          }
-        }
-        if (token) ptx::mbar_arrive(&tb->exp_done);
-        const uint64_t sum2 = tc::fadd2(tc::fadd2(acc2[0], acc2[1]), tc::fadd2(acc2[2], acc2[3]));
-        l_run = l_run * alpha + (tc::f2_lo(sum2) + tc::f2_hi(sum2));
-        m_run = m_use;
-      }
-      // ---- epilogue: O / l -> row, padding rows zero (attention.py:203-206)
-      ptx::mbar_wait(&tb->o_full, it & 1);
-      ptx::tc_fence_after();
-      const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
-      const float inv_l = (row < qvalid && n > 0) ? 1.f / l_run : 0.f;
-      E* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t ov[32];
-        ptx::tmem_ld32(t_row + o_col + c * 32, ov);
-        ptx::tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pk[e] = n > 0 ? tc::Elem<E>::pack(__uint_as_float(ov[2 * e]) * inv_l,
-                                            __uint_as_float(ov[2 * e + 1]) * inv_l)
-                        : 0u;
-        int4* dst = reinterpret_cast<int4*>(orow + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          __stcs(dst + e, make_int4((int)pk[4 * e], (int)pk[4 * e + 1], (int)pk[4 * e + 2],
-                                    (int)pk[4 * e + 3]));
-      }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&tb->o_empty);
-    }
-    if (token) {  // release the other tile for good
-      ptx::named_bar_sync(1 + a, 128);
-      if (threadIdx.x == 128 + 128 * a) tb->finished = 1;
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<TMEM_COLS>(bars->tmem_base);
-  }
-}
-
-}  // namespace tc4
-
-// =====================================================================================
-// tcgen05 kernel, full-block steps with a triple-buffered S (TCB_CARVE_V2=5 while under test).
-// One CTA per SM, one query tile at a time.  TMEM (512 columns): S0 S1 S2 (fp32 128 x 128,
-// P(j) written as bf16 over the first 64 columns of its S buffer) and O [384, 512).  Every
-// QK^T is M = N = 128 (full tensor rate).  Two MMA warps issue independently: the QK warp
-// runs up to two blocks ahead of the softmax (S(j+2) while P(j) is being computed), the PV
-// warp follows the softmax -- so the tensor pipe always has a queued stream while the
-// softmax warps (one per SMSP, alone on its MUFU) run back to back.  Q is double-buffered so
-// the next item's QK^T starts while the current item's PV drains.
-// =====================================================================================
-namespace tc5 {
-
-using tc::BM;
-using tc::BK;
-constexpr int NUM_THREADS = 224;  // w0 TMA, w1 QK MMA + TMEM owner, w2 PV MMA, w3..6 softmax
-constexpr int TMEM_COLS = 512;
-constexpr int O_COL = 384;
-constexpr int NS = 3;             // S buffers
-constexpr int QS = 2;             // Q buffers
-constexpr int SCHED = 4;          // scheduler ring entries
-constexpr int MAX_SMEM = 232448;
-constexpr float RESCALE_THRESHOLD = 8.0f;
-
-template <int D>
-struct Smem {
-  static constexpr int Q_BYTES = BM * D * 2;
-  static constexpr int TILE_BYTES = BK * D * 2;
-  static constexpr int CHUNKS = D / 64;
-  static constexpr int CHUNK = BM * 128;
-  static constexpr int BAR_BYTES = 1024;
-  static constexpr int TILES = (MAX_SMEM - BAR_BYTES - QS * Q_BYTES) / TILE_BYTES;
-  static constexpr int KS = TILES >= 6 ? 4 : (TILES + 1) / 2;  // K ring (5 tiles at d = 128: 3 + 2)
-  static constexpr int VS0 = TILES - KS;
-  static constexpr int VS = VS0 > 4 ? 4 : VS0;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = QS * Q_BYTES;
-  static constexpr int OFF_V = OFF_K + KS * TILE_BYTES;
-  static constexpr int OFF_BAR = OFF_V + VS * TILE_BYTES;
-  static constexpr int BYTES = OFF_BAR + BAR_BYTES;
-};
-
-struct Bars {
-  uint64_t q_full[QS], q_empty[QS];
-  uint64_t s_full[NS], p_full[NS], s_free[NS];
-  uint64_t o_done, o_full, o_empty;
-  uint64_t k_full[4], k_empty[4], v_full[4], v_empty[4];
-  uint64_t sched_full[SCHED], sched_empty[SCHED];
-  int sched_item[SCHED];
-  uint32_t tmem_base;
-};
-static_assert(sizeof(Bars) <= 1024, "barrier block must fit the reserved smem");
-
-template <int D, typename E = __nv_bfloat16>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    k_carve_tc5(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                const __grid_constant__ CUtensorMap tm_v, E* __restrict__ o, CarveShape s,
-                const int32_t* __restrict__ kv_idx, const int32_t* __restrict__ kv_cnt,
-                int* __restrict__ counter, int total_items, float scale_log2, float beta_log2,
-                int dbg) {
-  using L = Smem<D>;
-  constexpr int KS = L::KS, VS = L::VS;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sQ = smem + L::OFF_Q;
-  uint8_t* sK = smem + L::OFF_K;
-  uint8_t* sV = smem + L::OFF_V;
-  Bars* bars = reinterpret_cast<Bars*>(smem + L::OFF_BAR);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    if (ptx::smem_u32(smem) & 1023u) __trap();
-    for (int i = 0; i < QS; ++i) {
-      ptx::mbar_init(&bars->q_full[i], 1);
-      ptx::mbar_init(&bars->q_empty[i], 1);
-    }
-    for (int i = 0; i < NS; ++i) {
-      ptx::mbar_init(&bars->s_full[i], 1);
-      ptx::mbar_init(&bars->p_full[i], 128);
-      ptx::mbar_init(&bars->s_free[i], 1);
-    }
-    ptx::mbar_init(&bars->o_done, 1);
-    ptx::mbar_init(&bars->o_full, 1);
-    ptx::mbar_init(&bars->o_empty, 128);
-    for (int i = 0; i < KS; ++i) {
-      ptx::mbar_init(&bars->k_full[i], 1);
-      ptx::mbar_init(&bars->k_empty[i], 1);
-    }
-    for (int i = 0; i < VS; ++i) {
-      ptx::mbar_init(&bars->v_full[i], 1);
-      ptx::mbar_init(&bars->v_empty[i], 1);
-    }
-    for (int i = 0; i < SCHED; ++i) {
-      ptx::mbar_init(&bars->sched_full[i], 1);
-      ptx::mbar_init(&bars->sched_empty[i], 3);  // QK warp, PV warp, softmax group
-    }
-    ptx::fence_mbar_init();
-    ptx::tma_prefetch_desc(&tm_q);
-    ptx::tma_prefetch_desc(&tm_k);
-    ptx::tma_prefetch_desc(&tm_v);
-  }
-  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(&bars->tmem_base);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
-
-  // every role walks the same item sequence from the scheduler ring
-  auto next_item = [&](uint32_t it, int& h, int& qb, bool& vis, int& n) -> bool {
-    const int slot = it % SCHED;
-    ptx::mbar_wait(&bars->sched_full[slot], (it / SCHED) & 1);
-    const int item = __shfl_sync(0xffffffffu, bars->sched_item[slot], 0);
-    if (item < 0) return false;
-    decode_item(item, s, h, qb);
-    vis = qb < s.M_v;
-    n = __shfl_sync(0xffffffffu, vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total, 0);
-    return true;
-  };
-
-  if (warp == 0) {
-    // ============================ TMA producer + scheduler ============================
-    // Issue order K(0) K(1) [V(0) K(2)] [V(1) K(3)] ...: the QK warp runs ahead of the PV warp.
-    const uint64_t pol_kv = ptx::policy_evict_last();
-    const uint64_t pol_q = ptx::policy_evict_first();
-    uint32_t gk = 0, gv = 0, qn = 0;
-    for (uint32_t it = 0;; ++it) {
-      const int slot = it % SCHED;
-      int item = 0;
-      if (lane == 0) {
-        ptx::mbar_wait(&bars->sched_empty[slot], ((it / SCHED) & 1) ^ 1);
-        item = atomicAdd(counter, 1);
-        if (item >= total_items) item = -1;
-        bars->sched_item[slot] = item;
-        ptx::mbar_arrive(&bars->sched_full[slot]);
-      }
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-      if (n == 0) continue;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      const uint64_t pol = vis ? pol_kv : pol_q;
-      if (lane == 0) {
-        const int qs = qn % QS;
-        ptx::mbar_wait(&bars->q_empty[qs], ((qn / QS) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&bars->q_full[qs], L::Q_BYTES);
-#pragma unroll
-        for (int c = 0; c < L::CHUNKS; ++c)
-          ptx::tma_load_3d(sQ + qs * L::Q_BYTES + c * L::CHUNK, &tm_q, &bars->q_full[qs], c * 64,
-                           qb * BM, h, pol_q);
-      }
-      ++qn;
-      auto load = [&](bool is_v, int b) {
-        uint32_t& cnt = is_v ? gv : gk;
-        const int slots = is_v ? VS : KS;
-        if (lane == 0) {
-          const int sl = cnt % slots;
-          uint64_t* full = is_v ? bars->v_full : bars->k_full;
-          uint64_t* empty = is_v ? bars->v_empty : bars->k_empty;
-          ptx::mbar_wait(&empty[sl], ((cnt / slots) & 1) ^ 1);
-          if ((dbg & 1) && cnt >= (uint32_t)slots) {  // timing experiment: no operand traffic
-            ptx::mbar_arrive(&full[sl]);
-          } else {
-            ptx::mbar_arrive_expect_tx(&full[sl], L::TILE_BYTES);
-            uint8_t* base = (is_v ? sV : sK) + sl * L::TILE_BYTES;
-#pragma unroll
-            for (int c = 0; c < L::CHUNKS; ++c)
-              ptx::tma_load_3d(base + c * L::CHUNK, is_v ? &tm_v : &tm_k, &full[sl], c * 64, b * BK,
-                               h, pol);
-          }
-        }
-        ++cnt;
-      };
-      load(false, kl.block(0));
-      if (n > 1) load(false, kl.block(1));
-      for (int j = 0; j < n; ++j) {
-        load(true, kl.block(j));
-        if (j + 2 < n) load(false, kl.block(j + 2));
-      }
-    }
-  } else if (warp == 1) {
-    // ============================ QK^T issuer ============================
-    constexpr uint32_t IDESC_S = tc::make_idesc(BM, BK, 0, tc::Elem<E>::kBf16);
-    const uint32_t aQ = ptx::smem_u32(sQ), aK = ptx::smem_u32(sK);
-    uint32_t gk = 0, gs = 0, qn = 0;
-    for (uint32_t it = 0;; ++it) {
-      int h, qb, n;
-      bool vis;
-      const bool ok = next_item(it, h, qb, vis, n);
-      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[it % SCHED]);
-      if (!ok) break;
-      if (n == 0) continue;
-      const int qs = qn % QS;
-      ptx::mbar_wait(&bars->q_full[qs], (qn / QS) & 1);
-      ++qn;
-      const uint32_t qa = aQ + qs * L::Q_BYTES;
-      for (int j = 0; j < n; ++j, ++gs, ++gk) {
-        const int b = gs % NS;
-        if (gs >= (uint32_t)NS) ptx::mbar_wait(&bars->s_free[b], ((gs / NS) - 1) & 1);
-        const int sl = gk % KS;
-        ptx::mbar_wait(&bars->k_full[sl], (gk / KS) & 1);
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          const uint32_t kb = aK + sl * L::TILE_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * L::CHUNK + (kk & 3) * 32;
-            ptx::mma_ss(tmem + b * 128, tc::make_sdesc(qa + off, 16, 1024),
-                        tc::make_sdesc(kb + off, 16, 1024), IDESC_S, kk > 0 ? 1u : 0u);
-          }
-          ptx::mma_commit(&bars->k_empty[sl]);
-          ptx::mma_commit(&bars->s_full[b]);
-          if (j + 1 == n) ptx::mma_commit(&bars->q_empty[qs]);
-        }
-        __syncwarp();
-      }
-    }
-  } else if (warp == 2) {
-    // ============================ PV issuer ============================
-    constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, 1, tc::Elem<E>::kBf16);
-    const uint32_t aV = ptx::smem_u32(sV);
-    uint32_t gv = 0, gs = 0, items = 0;
-    for (uint32_t it = 0;; ++it) {
-      int h, qb, n;
-      bool vis;
-      const bool ok = next_item(it, h, qb, vis, n);
-      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[it % SCHED]);
-      if (!ok) break;
-      // O still holds the previous item until its epilogue has read it
-      if (items > 0) ptx::mbar_wait(&bars->o_empty, (items - 1) & 1);
-      ++items;
-      if (n == 0) {  // cannot come from build_block_mask; keep the epilogue in step
-        if (ptx::elect_one()) ptx::mma_commit(&bars->o_full);
-        __syncwarp();
-        continue;
-      }
-      for (int j = 0; j < n; ++j, ++gs, ++gv) {
-        const int b = gs % NS;
-        ptx::mbar_wait(&bars->p_full[b], (gs / NS) & 1);
-        const int sl = gv % VS;
-        ptx::mbar_wait(&bars->v_full[sl], (gv / VS) & 1);
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          const uint32_t vb = aV + sl * L::TILE_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            ptx::mma_ts(tmem + O_COL, tmem + b * 128 + kk * 8,
-                        tc::make_sdesc(vb + kk * 16 * 128, L::CHUNK, 1024),
-                        IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
-          ptx::mma_commit(&bars->v_empty[sl]);
-          ptx::mma_commit(&bars->s_free[b]);
-          ptx::mma_commit(&bars->o_done);
-          if (j + 1 == n) ptx::mma_commit(&bars->o_full);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    // ============================ softmax / correction / epilogue ============================
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
-    uint32_t g = 0;
-    for (uint32_t it = 0;; ++it) {
-      int h, qb, n;
-      bool vis;
-      const bool ok = next_item(it, h, qb, vis, n);
-      ptx::named_bar_sync(1, 128);
-      if (threadIdx.x == 96) ptx::mbar_arrive(&bars->sched_empty[it % SCHED]);
-      if (!ok) break;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      float m_run = -INFINITY, l_run = 0.f;
-      for (int j = 0; j < n; ++j, ++g) {
-        const int bb = g % NS;
-        const uint32_t scol = t_row + bb * 128;
-        const int blk = kl.block(j);
-        const int kvalid = block_valid(blk, BK, s.M_v, s.n_valid, s.n_cond);
-        const float bias = (vis && blk >= s.M_v) ? beta_log2 : 0.f;
-        ptx::mbar_wait(&bars->s_full[bb], (g / NS) & 1);
-        ptx::tc_fence_after();
-        uint32_t sr[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          ptx::tmem_ld32(scol + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
-        ptx::tmem_wait_ld();
-        if (dbg & 2) {  // timing experiment: no softmax work
-          l_run = 1.f;
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(&bars->p_full[bb]);
-          continue;
-        }
-        if (kvalid < BK) {  // padding keys of a partial block -> -inf (attention.py:193)
-#pragma unroll
-          for (int e = 0; e < 128; ++e)
-            if (e >= kvalid) sr[e] = __float_as_uint(-INFINITY);
-        }
-        float mx8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
-#pragma unroll
-        for (int e = 8; e < 120; e += 16)
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            mx8[q] = tc::fmax3(mx8[q], __uint_as_float(sr[e + q]), __uint_as_float(sr[e + 8 + q]));
-#pragma unroll
-        for (int q = 0; q < 8; ++q) mx8[q] = fmaxf(mx8[q], __uint_as_float(sr[120 + q]));
-        const float mraw = tc::fmax3(tc::fmax3(mx8[0], mx8[1], mx8[2]),
-                                     tc::fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-        const float m_blk = (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
-        const float m_new = fmaxf(m_run, m_blk);
-        const bool first = (j == 0);
-        const bool need = !first && (m_new > m_run + RESCALE_THRESHOLD);
-        const float m_use = (first || need) ? m_new : m_run;
-        const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
-        if (__any_sync(0xffffffffu, need)) {
-          // O is final only once PV(j-1) retired: o_done completes once per PV
-          ptx::mbar_wait(&bars->o_done, (g - 1) & 1);
-          ptx::tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            ptx::tmem_ld32(t_row + O_COL + c * 32, ov);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            ptx::tmem_st32(t_row + O_COL + c * 32, ov);
-          }
-        }
-        const float c0 = bias - m_use;
-        const uint64_t sc2 = tc::f2_pack(scale_log2, scale_log2), c02 = tc::f2_pack(c0, c0);
-        uint64_t acc2[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {  // 64 keys -> 32 packed columns per store
-          uint32_t pk[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int k = 64 * c + 2 * e;
-            const uint64_t x = tc::ffma2(
-                tc::f2_pack(__uint_as_float(sr[k]), __uint_as_float(sr[k + 1])), sc2, c02);
-            const float p0 = ptx::ex2(tc::f2_lo(x)), p1 = ptx::ex2(tc::f2_hi(x));
-            acc2[e & 3] = tc::fadd2(acc2[e & 3], tc::f2_pack(p0, p1));
-            pk[e] = tc::Elem<E>::pack(p0, p1);
-          }
-          ptx::tmem_st32(scol + 32 * c, pk);
-        }
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars->p_full[bb]);
-        const uint64_t sum2 = tc::fadd2(tc::fadd2(acc2[0], acc2[1]), tc::fadd2(acc2[2], acc2[3]));
-        l_run = l_run * alpha + (tc::f2_lo(sum2) + tc::f2_hi(sum2));
-        m_run = m_use;
-      }
-      // ---- epilogue: O / l -> row, padding rows zero (attention.py:203-206)
-      ptx::mbar_wait(&bars->o_full, it & 1);
-      ptx::tc_fence_after();
-      const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
-      const float inv_l = (row < qvalid && n > 0) ? 1.f / l_run : 0.f;
-      E* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
-#pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t ov[32];
-        ptx::tmem_ld32(t_row + O_COL + c * 32, ov);
-        ptx::tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          pk[e] = n > 0 ? tc::Elem<E>::pack(__uint_as_float(ov[2 * e]) * inv_l,
-                                            __uint_as_float(ov[2 * e + 1]) * inv_l)
-                        : 0u;
-        int4* dst = reinterpret_cast<int4*>(orow + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          __stcs(dst + e, make_int4((int)pk[4 * e], (int)pk[4 * e + 1], (int)pk[4 * e + 2],
-                                    (int)pk[4 * e + 3]));
-      }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&bars->o_empty);
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<TMEM_COLS>(tmem);
-  }
-}
-
-}  // namespace tc5
 
 
 
@@ -2547,146 +942,6 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
 
 
 
-template <int D, int NT, typename E = __nv_bfloat16>
-static int launch_tc2(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                      const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
-                      cudaStream_t st) {
-  CUtensorMap tq, tk, tv;
-  const int64_t n_pad = (int64_t)s.M_total * s.m;
-  constexpr bool f16 = !tc::Elem<E>::kBf16;
-  int rc;
-  if ((rc = make_tmap(&tq, q, D, n_pad, s.H, s.sh, s.sn, tc::BM, f16))) return rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::BK, f16))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::BK, f16))) return rc;
-  const int smem = tc2::Smem<D, NT>::BYTES;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc2::k_carve_tc2<D, NT, E>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
-    attr_set = true;
-  }
-  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
-  if (e != cudaSuccess) return set_error(TCB_ECUDA, "memset counter: %s", cudaGetErrorString(e));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int total = s.H * s.M_total;
-  int grid = (3 - NT) * sms;  // NT = 1: two CTAs per SM
-  if (grid > (total + NT - 1) / NT) grid = (total + NT - 1) / NT;
-  const float LOG2E = 1.4426950408889634f;
-  const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  tc2::k_carve_tc2<D, NT, E><<<grid, tc2::Cfg<NT>::NUM_THREADS, smem, st>>>(tq, tk, tv, (E*)o, s, kv_idx, kv_cnt,
-                                                              work, total, scale_log2, beta * LOG2E,
-                                                              dbg_flags());
-  return check_launch("k_carve_tc2");
-}
-
-template <int D, typename E = __nv_bfloat16>
-static int launch_tc3(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                      const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
-                      cudaStream_t st) {
-  CUtensorMap tq, tk, tv;
-  const int64_t n_pad = (int64_t)s.M_total * s.m;
-  constexpr bool f16 = !tc::Elem<E>::kBf16;
-  int rc;
-  if ((rc = make_tmap(&tq, q, D, n_pad, s.H, s.sh, s.sn, tc::BM, f16))) return rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::BK, f16))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::BK, f16))) return rc;
-  const int smem = tc3::Smem<D>::BYTES;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc3::k_carve_tc3<D, E>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
-    attr_set = true;
-  }
-  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
-  if (e != cudaSuccess) return set_error(TCB_ECUDA, "memset counter: %s", cudaGetErrorString(e));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int total = s.H * s.M_total;
-  int grid = 2 * sms;
-  if (grid > total) grid = total;
-  const float LOG2E = 1.4426950408889634f;
-  const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  tc3::k_carve_tc3<D, E><<<grid, tc3::NUM_THREADS, smem, st>>>(tq, tk, tv, (E*)o, s, kv_idx, kv_cnt,
-                                                              work, total, scale_log2, beta * LOG2E,
-                                                              dbg_flags());
-  return check_launch("k_carve_tc3");
-}
-
-template <int D, typename E = __nv_bfloat16>
-static int launch_tc4(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                      const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
-                      cudaStream_t st) {
-  CUtensorMap tq, tk, tv;
-  const int64_t n_pad = (int64_t)s.M_total * s.m;
-  constexpr bool f16 = !tc::Elem<E>::kBf16;
-  int rc;
-  if ((rc = make_tmap(&tq, q, D, n_pad, s.H, s.sh, s.sn, tc::BM, f16))) return rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::BK, f16))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::BK, f16))) return rc;
-  const int smem = tc4::Smem<D>::BYTES;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc4::k_carve_tc4<D, E>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
-    attr_set = true;
-  }
-  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
-  if (e != cudaSuccess) return set_error(TCB_ECUDA, "memset counter: %s", cudaGetErrorString(e));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int total = s.H * s.M_total;
-  int grid = sms;
-  if (grid > (total + 1) / 2) grid = (total + 1) / 2;
-  const float LOG2E = 1.4426950408889634f;
-  const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  tc4::k_carve_tc4<D, E><<<grid, tc4::NUM_THREADS, smem, st>>>(tq, tk, tv, (E*)o, s, kv_idx, kv_cnt,
-                                                              work, total, scale_log2, beta * LOG2E,
-                                                              dbg_flags());
-  return check_launch("k_carve_tc4");
-}
-
-template <int D, typename E = __nv_bfloat16>
-static int launch_tc5(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                      const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
-                      cudaStream_t st) {
-  CUtensorMap tq, tk, tv;
-  const int64_t n_pad = (int64_t)s.M_total * s.m;
-  constexpr bool f16 = !tc::Elem<E>::kBf16;
-  int rc;
-  if ((rc = make_tmap(&tq, q, D, n_pad, s.H, s.sh, s.sn, tc::BM, f16))) return rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::BK, f16))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::BK, f16))) return rc;
-  const int smem = tc5::Smem<D>::BYTES;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tc5::k_carve_tc5<D, E>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
-    attr_set = true;
-  }
-  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
-  if (e != cudaSuccess) return set_error(TCB_ECUDA, "memset counter: %s", cudaGetErrorString(e));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int total = s.H * s.M_total;
-  int grid = sms;
-  if (grid > total) grid = total;
-  const float LOG2E = 1.4426950408889634f;
-  const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  tc5::k_carve_tc5<D, E><<<grid, tc5::NUM_THREADS, smem, st>>>(tq, tk, tv, (E*)o, s, kv_idx, kv_cnt,
-                                                              work, total, scale_log2, beta * LOG2E,
-                                                              dbg_flags());
-  return check_launch("k_carve_tc5");
-}
-
 extern "C" int tcb_carve_fwd_simt(const void* q, const void* k, const void* v, void* o, int dtype,
                                   int64_t stride_h, int64_t stride_n, const int32_t* kv_idx,
                                   const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
@@ -2719,43 +974,6 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
     if (emu != 0 && emu != 2 && emu != 3 && emu != 4) emu = 0;
   }
   cudaStream_t st = as_stream(stream);
-  static int v2 = -1;
-  if (v2 < 0) {
-    const char* env = getenv("TCB_CARVE_V2");
-    v2 = env ? atoi(env) : 0;
-  }
-  if (v2 == 1) {
-    if (dtype == TCB_F16)
-      return d == 128 ? launch_tc2<128, 1, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
-                      : launch_tc2<64, 1, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-    return d == 128 ? launch_tc2<128, 1>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
-                    : launch_tc2<64, 1>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-  }
-  if (v2 == 3) {
-    if (dtype == TCB_F16)
-      return d == 128 ? launch_tc3<128, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
-                      : launch_tc3<64, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-    return d == 128 ? launch_tc3<128>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
-                    : launch_tc3<64>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-  }
-  if (v2 == 4) {
-    if (dtype == TCB_F16)
-      return d == 128 ? launch_tc4<128, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
-                      : launch_tc4<64, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-    return d == 128 ? launch_tc4<128>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
-                    : launch_tc4<64>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-  }
-  if (v2 == 5) {
-    if (dtype == TCB_F16)
-      return d == 128 ? launch_tc5<128, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
-                      : launch_tc5<64, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-    return d == 128 ? launch_tc5<128>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
-                    : launch_tc5<64>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-  }
-  if (v2 == 2) {
-    return d == 128 ? launch_tc2<128, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
-                    : launch_tc2<64, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-  }
   if (dtype == TCB_F16)  // fp16 operands and P (kind::f16 with f16 inputs), f32 accumulation
     return d == 128 ? launch_tc<128, 0, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
                     : launch_tc<64, 0, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
@@ -2768,15 +986,4 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
     }
   }
   return launch_tc<64, 0>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-}
-
-// Debug only (not part of include/tokencarve_b200.h): copy out and clear the CTA-0 timeline
-// (TRACE_EV x TRACE_STEPS clocks, 0 = not reached).
-extern "C" int tcb_debug_trace_read(unsigned long long* host, int cap) {
-  const int n = tcb::tc2::TRACE_EV * tcb::tc2::TRACE_STEPS;
-  if (cap < n) return -1;
-  cudaMemcpyFromSymbol(host, tcb::tc2::g_trace, sizeof(unsigned long long) * n);
-  static unsigned long long zero[tcb::tc2::TRACE_EV * tcb::tc2::TRACE_STEPS];
-  cudaMemcpyToSymbol(tcb::tc2::g_trace, zero, sizeof(zero));
-  return n;
 }
