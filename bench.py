@@ -260,6 +260,22 @@ def run_gpu(args):
     hbm, tf_burst, tf_sust, peak_src = peaks()
     carve_tflops = flops_local / (k_carve * 1e-3) / 1e12
 
+    # the same layer replayed as one CUDA graph (tcb.CarveLayerGraph): launch overhead gone
+    graph_ms = None
+    if world == 1:
+        lg = tcb.CarveLayerGraph(q, k, v, layout, statics, params)
+        for _ in range(2):
+            lg.replay()
+        barrier()
+        a, b = ev(), ev()
+        a.record()
+        for _ in range(args.steps):
+            lg.replay()
+        b.record()
+        barrier()
+        graph_ms = round(a.elapsed_time(b) / args.steps, 4)
+        del lg
+
     # e2e through the public API with host buffers (pinned H2D in, O D2H out)
     e2e = None
     if not args.no_e2e:
@@ -338,6 +354,7 @@ def run_gpu(args):
                    if world > 1 else "single",
                    "l2": "no flush: Q/K/V/O = 2.9 GB per layer > 126 MB L2"},
         "kept_block_tflops": round(carve_tflops, 1),
+        "cuda_graph_ms_per_step": graph_ms,
         "kernels_ms": None if chunked else {
             "block_pool": round(float(k_pool), 4), "block_scores": round(float(k_rel), 4),
             "block_softmax_select": round(float(k_sel), 4), "carve_fwd": round(float(k_carve), 4)},

@@ -27,7 +27,7 @@ from .errors import ShapeError
 from .masks import BlockMask, SelectionParams
 from .partition import BlockLayout, StaticMasks, mask_words
 
-__all__ = ["carve_layer"]
+__all__ = ["carve_layer", "CarveLayerGraph"]
 
 _streams: dict = {}
 
@@ -133,3 +133,58 @@ def carve_layer(q, k, v, layout: BlockLayout, statics: StaticMasks, params: Sele
     mask = BlockMask(words=bits, kv_idx=kv_idx, kv_cnt=kv_cnt, M_total=Mt, nonempty=True)
     comp.synchronize()  # a host result is complete on return, like the reference's arrays
     return (out.numpy() if numpy_in else out), mask
+
+
+class CarveLayerGraph:
+    """One carved-attention layer captured as a CUDA graph on fixed device buffers.
+
+    A DiT runs the same layer geometry every step, so the four launches
+    (pool -> scores -> select/union -> carve) and the carve kernel's work-counter reset are
+    recorded once and replayed with one ``cudaGraphLaunch``.  Like ``torch.cuda.CUDAGraph``
+    the buffers are static: write the step's Q/K/V into ``q``/``k``/``v`` (or pass the
+    tensors the caller already fills in place), call :meth:`replay`, read ``out`` and
+    ``mask``.  The replay is bitwise the eager ``carve_layer`` (same kernels, same order).
+    """
+
+    def __init__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, layout: BlockLayout,
+                 statics: StaticMasks, params: SelectionParams,
+                 beta: AmplifierBias = AmplifierBias(0.0)):
+        if not (isinstance(q, torch.Tensor) and q.is_cuda and k.is_cuda and v.is_cuda):
+            raise ShapeError("CarveLayerGraph takes device Q/K/V (the static replay buffers)")
+        if not (q.shape == k.shape == v.shape) or q.ndim != 3:
+            raise ShapeError(f"Q/K/V must share one (heads, N, d_k) shape, got {tuple(q.shape)}/"
+                             f"{tuple(k.shape)}/{tuple(v.shape)}")
+        if q.shape[1] != layout.padded_total:
+            raise ShapeError(f"token axis {q.shape[1]} != padded token count {layout.padded_total}")
+        if k.stride() != q.stride() or v.stride() != q.stride() or q.stride(2) != 1:
+            raise ShapeError("Q/K/V must share strides with a contiguous innermost axis")
+        H, N, d = q.shape
+        dev = q.device
+        Mv, Mt = layout.M_v, layout.M_total
+        self.q, self.k, self.v = q, k, v
+        self.out = torch.empty_like(q)
+        self._pq = torch.empty((H, Mt, d), dtype=torch.float64, device=dev)
+        self._pk = torch.empty_like(self._pq)
+        self._R = torch.empty((H, Mv, Mt), dtype=torch.float64, device=dev)
+        self._bits = torch.empty((H, Mv, mask_words(Mt)), dtype=torch.int32, device=dev)
+        self._kv_idx = torch.empty((H, Mv, Mt), dtype=torch.int32, device=dev)
+        self._kv_cnt = torch.empty((H, Mv), dtype=torch.int32, device=dev)
+        self._adja = statics.packed(layout)
+        self._work = torch.zeros(16, dtype=torch.int32, device=dev)  # private: replays may overlap
+        self.mask = BlockMask(words=self._bits, kv_idx=self._kv_idx, kv_cnt=self._kv_cnt, M_total=Mt,
+                              nonempty=True)
+        args = (self.q, self.k, self.v, self.out, self._pq, self._pk, self._R, self._bits,
+                self._kv_idx, self._kv_cnt, self._adja, layout, params, beta.beta, self._work)
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # eager warm-up: kernel attributes, tensor-map driver entry
+            _launch_chunk(*args, side.cuda_stream)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            _launch_chunk(*args, torch.cuda.current_stream(dev).cuda_stream)
+
+    def replay(self) -> torch.Tensor:
+        """Run the captured layer on the current stream; returns ``out``."""
+        self.graph.replay()
+        return self.out

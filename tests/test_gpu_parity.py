@@ -306,6 +306,29 @@ def test_carve_layer_host_pipeline_bitwise(hpc):
     np.testing.assert_allclose(o32, ref32, rtol=1e-5, atol=1e-5)
 
 
+def test_carve_layer_cuda_graph_replay_bitwise():
+    # the captured layer == the eager two-call path, bitwise, and replays track new inputs
+    # written into the static buffers (cutoff selection p > 0 included: two select passes)
+    dims = tcb.GridDims(4, 16, 32)
+    lay = tcb.build_layout(dims, 128, 100)
+    st = tcb.StaticMasks.build(lay, dims, tcb.build_curve(dims))
+    for params in (tcb.SelectionParams(k=0.25, p=0.0), tcb.SelectionParams(k=0.1, p=0.3)):
+        g = torch.Generator(device="cuda").manual_seed(11)
+        q, k, v = (torch.randn((4, lay.padded_total, 128), generator=g, device="cuda")
+                   .to(torch.bfloat16) for _ in range(3))
+        lg = tcb.CarveLayerGraph(q, k, v, lay, st, params, tcb.AmplifierBias(0.2))
+        for step in range(3):
+            if step:
+                for t in (q, k, v):
+                    t.copy_(torch.randn(t.shape, generator=g, device="cuda").to(torch.bfloat16))
+            out = lg.replay()
+            ref, ref_mask = tcb.carve_layer(q, k, v, lay, st, params, tcb.AmplifierBias(0.2))
+            torch.cuda.synchronize()
+            assert torch.equal(out, ref), step
+            assert torch.equal(lg.mask.words, ref_mask.words)
+            assert torch.equal(lg.mask.kv_cnt, ref_mask.kv_cnt)
+
+
 # ----------------------------------------------------------------- Ulysses layout (§8e)
 def test_token_major_head_shard_layout_bitwise():
     # after the all-to-all each rank holds a token-major (N, H/G, d) head shard; every
