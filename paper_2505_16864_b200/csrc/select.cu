@@ -4,6 +4,8 @@
 // K4  tcb_block_relevance  <- relevance         masks.py:119-134  (fp64 FMA bound)
 // K5  tcb_block_select     <- importance_mask   masks.py:137-159
 //     (+ union)            <- union_mask        masks.py:162-175
+#include <algorithm>
+
 #include "common.cuh"
 
 #include <cuda_bf16.h>
@@ -718,7 +720,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
     s_nops = pw_program(M_total, s_nl, fold_ops);
   }
   __syncthreads();
-  const int64_t row = (int64_t)blockIdx.x * SW_WARPS + warp;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (row >= n_rows) return;
   if (MODE == 2 && kv_cnt[row] != -1) return;
   unsigned char* base = smem + (size_t)warp * per_warp_bytes;
@@ -1053,23 +1055,28 @@ static int launch_select(double* R, bool raw, int H, int M_v, int M_total, const
   // (np2 >= 544: the register-sort path stages 512 slots + one pad per 16 in skey/scol)
   if (sort) per_warp += (size_t)(np2 > 544 ? np2 : 544) * 12;
   per_warp = (per_warp + 15) & ~size_t(15);
-  const size_t smem = per_warp * SW_WARPS;
-  const unsigned grid = (unsigned)ceil_div(n_rows, SW_WARPS);
-  auto go = [&](auto kern, size_t sm) -> int {
+  // rows (warps) per CTA: SW_WARPS while their shared memory fits, fewer for long rows
+  // (M_total = 8192 with the sort buffers needs 163 KB for one warp)
+  constexpr size_t SMEM_CAP = 232448 - 8192;  // opt-in limit minus the static leaf tables
+  auto go = [&](auto kern, size_t pw) -> int {
+    const int wpc = (int)std::min<size_t>(SW_WARPS, SMEM_CAP / pw);
+    if (wpc < 1) return set_error(TCB_ESIZE, "k_select: %zu B of shared memory per row", pw);
+    const size_t sm = pw * wpc;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "k_select smem: %s", cudaGetErrorString(e));
-    kern<<<grid, SW_WARPS * 32, sm, s>>>(R, n_rows, M_v, M_total, np2, adja, words, n_floor, p,
-                                         with_union, bits, kv_idx, kv_cnt, (int)(sm / SW_WARPS), nslots);
+    kern<<<(unsigned)ceil_div(n_rows, wpc), wpc * 32, sm, s>>>(
+        R, n_rows, M_v, M_total, np2, adja, words, n_floor, p, with_union, bits, kv_idx, kv_cnt,
+        (int)pw, nslots);
     return check_launch("k_select");
   };
-  if (raw && !sort) return go(k_select<true, false>, smem);
+  if (raw && !sort) return go(k_select<true, false>, per_warp);
   // cutoff path: slim pass (register sort of the top-512 window, ~35 % less shared memory
   // per warp -> 1.5x the resident warps), then the full-sort pass over the rows it left
   size_t slim = (size_t)M_pad * 8 + 256 * 4 + (size_t)words_pad * 4 + (size_t)nslots * 8 + 544 * 12;
-  slim = ((slim + 15) & ~size_t(15)) * SW_WARPS;
+  slim = (slim + 15) & ~size_t(15);
   int rc = raw ? go(k_select<true, true, 1>, slim) : go(k_select<false, true, 1>, slim);
   if (rc) return rc;
-  return go(k_select<false, true, 2>, smem);
+  return go(k_select<false, true, 2>, per_warp);
 }
 
 extern "C" int tcb_block_select(const double* R, int H, int M_v, int M_total,

@@ -106,3 +106,40 @@ def test_c2_padding_rows_zero_and_determinism(c2):
     again = tcb.carve_attention(tcb.AttentionInputs(q=c2["q"], k=c2["k"], v=c2["v"], layout=lay),
                                 c2["mask"])
     assert torch.equal(again, out)  # bitwise run to run (fixed kv order, no atomics in the math)
+
+
+@pytest.mark.parametrize("p", [0.0, 0.3])
+def test_large_grid_beyond_c2_masks_and_carve(p):
+    # 64x90x160 + 77 text tokens (921,677 tokens, M_total = 7,201 blocks, one head, d = 64):
+    # rows this long select with one warp per CTA (the sort buffers need ~150 KB), and at
+    # p = 0.3 nearly every row falls through the slim top-512 pass to the full sort
+    dims, m, nc, d = (64, 90, 160), 128, 77, 64
+    g = tcb.GridDims(*dims)
+    lay = tcb.build_layout(g, m, nc)
+    perm = tcb.build_curve(g)
+    st = tcb.StaticMasks.build(lay, g, perm)
+    gen = torch.Generator(device="cuda").manual_seed(7202)
+    q, k, v = (torch.randn((1, lay.padded_total, d), generator=gen, device="cuda").to(torch.bfloat16)
+               for _ in range(3))
+    mask, R = tcb.build_block_mask(q, k, lay, st, tcb.SelectionParams(k=0.02, p=p))
+    out = tcb.carve_attention(tcb.AttentionInputs(q=q, k=k, v=v, layout=lay), mask)
+    torch.cuda.synchronize()
+    L = oracle.layout_scalars(dims, m, nc)
+    assert L["M_total"] == lay.M_total == 7201
+    qn, kn, vn = (t.float().cpu().numpy() for t in (q, k, v))
+    adja = oracle.adjacency(dims, oracle.curve_inverse(perm.forward_np), m, L["M_v"])
+    rows = np.r_[0:64, L["M_v"] - 64:L["M_v"]]  # oracle selection on sampled rows
+    pq, _ = oracle.pool_blocks(qn, L)
+    pk, _ = oracle.pool_blocks(kn, L)
+    Rs = oracle.relevance_f64(pq[:, rows], pk, d)
+    bits = oracle.union_bits(oracle.select_topk(Rs, 0.02, p, L["M_v"]), adja[rows], L["M_v"])
+    got = mask.bits[0].cpu().numpy()[rows]
+    assert np.array_equal(got, bits[0])
+    np.testing.assert_allclose(R[0, rows].cpu().numpy(), Rs[0], rtol=1e-12, atol=0)
+    items = [(0, 0), (0, 3000), (0, L["M_v"] - 1), (0, L["M_v"])]  # last = condition row
+    ref = oracle.carve(qn, kn, vn, mask.bits.cpu().numpy(), L, 0.0, workers=4, items=items)
+    got = out.float().cpu().numpy()
+    for _, b in items:
+        sl = slice(b * m, (b + 1) * m)
+        err = np.abs(got[0, sl] - ref[0, sl]).max() / max(np.abs(ref[0, sl]).max(), 1e-30)
+        assert err <= 2e-2, (b, err)

@@ -278,6 +278,22 @@ def test_select_general_rows_vs_oracle():
             assert np.array_equal(got, oracle.select_topk(R, k, p, n_cols)), (n_cols, k, p)
 
 
+def test_select_maximum_columns_vs_oracle():
+    # the selection kernels' largest supported row (8,192 blocks = 1M tokens at m = 128),
+    # both the quota-only and the cutoff path, then the documented SizeError just beyond
+    rng = np.random.default_rng(81)
+    n_cols = 8192
+    R = rng.dirichlet(np.full(n_cols, 0.3), size=(1, 3))
+    R[0, 2, :100] = R[0, 2, 100]  # ties straddling the cut
+    for k, p in ((0.01, 0.0), (0.02, 0.3), (0.3, 0.9)):
+        got = tcb.importance_mask(R, tcb.SelectionParams(k=k, p=p), n_cols)
+        assert np.array_equal(got, oracle.select_topk(R, k, p, n_cols)), (k, p)
+    from paper_2505_16864_b200.errors import SizeError
+    with pytest.raises(SizeError):
+        tcb.importance_mask(np.full((1, 1, n_cols + 1), 1.0 / (n_cols + 1)),
+                            tcb.SelectionParams(k=0.1, p=0.0), n_cols + 1)
+
+
 # ----------------------------------------------------------------- host-streamed layer
 @pytest.mark.parametrize("hpc", [1, 2, None])
 def test_carve_layer_host_pipeline_bitwise(hpc):
