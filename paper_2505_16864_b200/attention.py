@@ -79,10 +79,13 @@ _work: dict = {}
 
 
 def _workspace(dev: torch.device) -> torch.Tensor:
-    w = _work.get(dev)
+    """The carve kernel's work counter (reset by the launch itself), one per (device,
+    stream): launches on different streams may run concurrently and must not share it."""
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    w = _work.get(key)
     if w is None:
         w = torch.zeros(16, dtype=torch.int32, device=dev)
-        _work[dev] = w
+        _work[key] = w
     return w
 
 

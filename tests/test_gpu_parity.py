@@ -345,6 +345,32 @@ def test_carve_layer_cuda_graph_replay_bitwise():
             assert torch.equal(lg.mask.kv_cnt, ref_mask.kv_cnt)
 
 
+def test_carve_concurrent_streams():
+    # each stream has its own work counter: two layers in flight on two streams stay exact
+    dims = tcb.GridDims(4, 16, 32)
+    lay = tcb.build_layout(dims, 128, 100)
+    st = tcb.StaticMasks.build(lay, dims, tcb.build_curve(dims))
+    params = tcb.SelectionParams(k=0.25, p=0.0)
+    g = torch.Generator(device="cuda").manual_seed(21)
+    ins = [[torch.randn((6, lay.padded_total, 128), generator=g, device="cuda").to(torch.bfloat16)
+            for _ in range(3)] for _ in range(2)]
+    refs = []
+    for q, k, v in ins:
+        o, _ = tcb.carve_layer(q, k, v, lay, st, params)
+        refs.append(o.clone())
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [None, None]
+    for rep in range(3):
+        for i, s in enumerate(streams):
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                outs[i], _ = tcb.carve_layer(*ins[i], lay, st, params)
+        torch.cuda.synchronize()
+        for i in range(2):
+            assert torch.equal(outs[i], refs[i]), (rep, i)
+
+
 # ----------------------------------------------------------------- Ulysses layout (§8e)
 def test_token_major_head_shard_layout_bitwise():
     # after the all-to-all each rank holds a token-major (N, H/G, d) head shard; every
