@@ -288,6 +288,49 @@ def c2_fp32_record():
             "fp32_tflops": round(4.0 * 128 ** 3 * pairs / (t_carve * 1e-3) / 1e12, 1)}
 
 
+def dense_library_record():
+    """Dense attention over the whole C2 sequence (931^2 x 24 block pairs) with the vendor
+    kernels on the same box: torch SDPA (cuDNN / flash backends) and flash_attn if present.
+    The kept-block TFLOP/s of k_carve_tc is judged against what a production dense kernel
+    reaches under the same power cap."""
+    import torch.nn.functional as F
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+
+    N, H, d = 931 * 128, 24, 128
+    flops = 4.0 * N * N * d * H
+    g = torch.Generator(device="cuda").manual_seed(0)
+    q, k, v = (torch.randn((1, H, N, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
+    out = []
+
+    def timed(name, fn, reps=3):
+        try:
+            fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / reps
+            out.append({"kernel": name, "ms": round(ms, 2), "tflops": round(flops / (ms * 1e-3) / 1e12, 1)})
+        except Exception as e:  # backend not available for this shape / build
+            out.append({"kernel": name, "unavailable": str(e).splitlines()[0][:120]})
+
+    for name, be in (("sdpa cudnn", SDPBackend.CUDNN_ATTENTION), ("sdpa flash", SDPBackend.FLASH_ATTENTION)):
+        def run(be=be):
+            with sdpa_kernel([be]):
+                F.scaled_dot_product_attention(q, k, v)
+        timed(name, run)
+    try:
+        from flash_attn import flash_attn_func
+        qt, kt, vt = (t.transpose(1, 2).contiguous() for t in (q, k, v))
+        timed("flash_attn 2.8 (library)", lambda: flash_attn_func(qt, kt, vt))
+    except ImportError:
+        out.append({"kernel": "flash_attn", "unavailable": "not importable"})
+    return {"shape": f"(1, {H}, {N}, {d}) bf16, no mask", "flops": flops, "results": out}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
@@ -316,6 +359,7 @@ def main():
     _, tf = peaks()
     dense = 4.0 * 128 ** 3 * 931 ** 2 * 24
     res["c5_dense_roofline_ms"] = round(dense / (tf * 1e12) * 1e3, 3)
+    res["c2_dense_library"] = dense_library_record()
     text = json.dumps(res, indent=1)
     print(text)
     if a.out:
