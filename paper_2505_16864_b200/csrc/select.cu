@@ -638,6 +638,77 @@ __device__ __forceinline__ void reg_bitonic512(KC (&x)[16]) {
   reg_bitonic_level<2>(x, threadIdx.x & 31);
 }
 
+// The same network on packed 64-bit (key, col) words: when every key of the window shares
+// its top `colbits` bits (one binade of probabilities does: sign + exponent), the column
+// fits below the key's remaining bits and one unsigned compare orders (key, col) exactly.
+template <int KK, int JJ>
+__device__ __forceinline__ void reg_bitonic_stage_u(uint64_t (&y)[16], int lane) {
+  if constexpr (JJ >= 16) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int e = lane * 16 + r;
+      const uint64_t o = __shfl_xor_sync(FULL, y[r], JJ >> 4);
+      const bool up = (e & KK) == 0, lower = (e & JJ) == 0;
+      const bool take_o = (up == lower) ? (o < y[r]) : (y[r] < o);
+      if (take_o) y[r] = o;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      if (r & JJ) continue;
+      const bool up = ((lane * 16 + r) & KK) == 0;
+      if ((y[r | JJ] < y[r]) == up) {
+        const uint64_t t = y[r];
+        y[r] = y[r | JJ];
+        y[r | JJ] = t;
+      }
+    }
+  }
+  if constexpr (JJ > 1) reg_bitonic_stage_u<KK, JJ / 2>(y, lane);
+}
+
+template <int KK>
+__device__ __forceinline__ void reg_bitonic_level_u(uint64_t (&y)[16], int lane) {
+  reg_bitonic_stage_u<KK, KK / 2>(y, lane);
+  if constexpr (KK < 512) reg_bitonic_level_u<KK * 2>(y, lane);
+}
+
+// Sort the window x[16] (cnt real entries, the rest padding ~0 / INT_MAX) by (key, col);
+// packed single-word compares when the keys leave room for the column, KC compares otherwise.
+__device__ __forceinline__ void reg_sort_window(KC (&x)[16], int cnt, int M_total) {
+  const int lane = threadIdx.x & 31;
+  uint64_t kand = ~0ull, kor = 0ull;
+#pragma unroll
+  for (int r = 0; r < 16; ++r)
+    if (lane * 16 + r < cnt) {
+      kand &= x[r].k;
+      kor |= x[r].k;
+    }
+  const uint32_t al = __reduce_and_sync(FULL, (uint32_t)kand), ah = __reduce_and_sync(FULL, (uint32_t)(kand >> 32));
+  const uint32_t ol = __reduce_or_sync(FULL, (uint32_t)kor), oh = __reduce_or_sync(FULL, (uint32_t)(kor >> 32));
+  kand = ((uint64_t)ah << 32) | al;
+  kor = ((uint64_t)oh << 32) | ol;
+  const int colbits = M_total > 1 ? 32 - __clz(M_total - 1) : 0;
+  const uint64_t diff = kand ^ kor;
+  const int lead = diff ? __clzll((long long)diff) : 64;
+  if (lead < colbits) {
+    reg_bitonic512(x);
+    return;
+  }
+  const uint64_t cmask = colbits ? (~0ull >> (64 - colbits)) : 0ull;
+  const uint64_t top = colbits ? (kand & ~(~0ull >> colbits)) : 0ull;
+  uint64_t y[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r)
+    y[r] = (lane * 16 + r < cnt) ? ((x[r].k << colbits) | (uint64_t)x[r].c) : ~0ull;
+  reg_bitonic_level_u<2>(y, lane);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    x[r].k = top | (y[r] >> colbits);
+    x[r].c = (int)(y[r] & cmask);
+  }
+}
+
 // Exact np.cumsum scan of the sorted values: the sorted keys go back to the (padded)
 // staging buffer and lane 0 runs the dependent float64 add chain over them (loads
 // software-pipelined by the unrolled loop); returns 1 + #(prefix <= p), stopping at the
@@ -822,7 +893,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
         x[r].k = stage_k[lane * 17 + r];
         x[r].c = stage_c[lane * 17 + r];
       }
-      reg_bitonic512(x);
+      reg_sort_window(x, k_ub, M_total);
       bool crossed;
       __syncwarp();
       n_cut = reg_sorted_cut(x, stage_k, k_ub, p, &crossed);
