@@ -159,7 +159,7 @@ __device__ __forceinline__ double pw_leaf(const double* p, int len) {
 }
 
 // Leaves of the pairwise tree of n in left-to-right order; returns their count.
-__device__ int pw_leaves(int n, int* off, int* len) {
+__host__ __device__ int pw_leaves(int n, int* off, int* len) {
   int st_off[32], st_len[32], sp = 0, nl = 0;
   st_off[sp] = 0; st_len[sp] = n; ++sp;
   while (sp) {
@@ -217,7 +217,7 @@ __device__ double pw_fold(int n, const double* leaf) {
 // internal node i (post-order, the order pw_fold evaluates them) writes slot nl + i =
 // slot a_i + slot b_i.  Built once per CTA (the tree depends only on n), executed per
 // row by one lane with no stack -- bitwise the pw_fold result.
-__device__ int pw_program(int n, int nl, int2* ops) {
+__host__ __device__ int pw_program(int n, int nl, int2* ops) {
   int st_len[32], st_state[32], st_left[32], sp = 1, ret = -1, leafc = 0, nops = 0;
   st_len[0] = n;
   st_state[0] = 0;
@@ -457,6 +457,14 @@ __device__ void emit_row(uint32_t* sbits, int words, int M_total, uint32_t* __re
     }
   }
 }
+
+// The pairwise-sum tree of a row depends only on M_total: built once on the host per launch
+// and passed by value (it used to be built by thread 0 of every CTA while the CTA waited).
+struct PwProg {
+  int nl, nops;
+  int off[SEL_MAX_LEAVES], len[SEL_MAX_LEAVES];
+  int2 ops[SEL_MAX_LEAVES];
+};
 
 // ---- warp-per-row selection ------------------------------------------------------
 constexpr int SW_WARPS = 4;  // rows (one warp each) per CTA
@@ -780,17 +788,21 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
                                                           uint32_t* __restrict__ bits,
                                                           int32_t* __restrict__ kv_idx,
                                                           int32_t* __restrict__ kv_cnt,
-                                                          int per_warp_bytes, int nslots) {
+                                                          int per_warp_bytes, int nslots,
+                                                          const __grid_constant__ PwProg prog) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int leaf_off[SEL_MAX_LEAVES], leaf_len[SEL_MAX_LEAVES];
   __shared__ int2 fold_ops[SEL_MAX_LEAVES];
-  __shared__ int s_nl, s_nops;
+  const int s_nl = prog.nl, s_nops = prog.nops;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (RAW && threadIdx.x == 0) {
-    s_nl = pw_leaves(M_total, leaf_off, leaf_len);
-    s_nops = pw_program(M_total, s_nl, fold_ops);
+  if (RAW) {
+    for (int i = threadIdx.x; i < s_nl; i += blockDim.x) {
+      leaf_off[i] = prog.off[i];
+      leaf_len[i] = prog.len[i];
+    }
+    for (int i = threadIdx.x; i < s_nops; i += blockDim.x) fold_ops[i] = prog.ops[i];
+    __syncthreads();
   }
-  __syncthreads();
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   if (row >= n_rows) return;
   if (MODE == 2 && kv_cnt[row] != -1) return;
@@ -1115,6 +1127,9 @@ static int launch_select(double* R, bool raw, int H, int M_v, int M_total, const
     }
   }
   const int nslots = (2 * nl + 1) & ~1;
+  PwProg prog;
+  prog.nl = pw_leaves(M_total, prog.off, prog.len);
+  prog.nops = pw_program(M_total, prog.nl, prog.ops);
   TCB_CHECK_ARG(n_floor >= 1, TCB_EDOMAIN, "n_floor must be >= 1");
   const int64_t n_rows = (int64_t)H * M_v;
   if (n_rows == 0) return TCB_OK;
@@ -1137,7 +1152,7 @@ static int launch_select(double* R, bool raw, int H, int M_v, int M_total, const
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "k_select smem: %s", cudaGetErrorString(e));
     kern<<<(unsigned)ceil_div(n_rows, wpc), wpc * 32, sm, s>>>(
         R, n_rows, M_v, M_total, np2, adja, words, n_floor, p, with_union, bits, kv_idx, kv_cnt,
-        (int)pw, nslots);
+        (int)pw, nslots, prog);
     return check_launch("k_select");
   };
   if (raw && !sort) return go(k_select<true, false>, per_warp);
