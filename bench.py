@@ -354,6 +354,7 @@ def run_gpu(args):
                    if world > 1 else "single",
                    "l2": "no flush: Q/K/V/O = 2.9 GB per layer > 126 MB L2"},
         "kept_block_tflops": round(carve_tflops, 1),
+        "layer_tflops": round(flops / (ms_step * 1e-3) / 1e12, 1),
         "cuda_graph_ms_per_step": graph_ms,
         "kernels_ms": None if chunked else {
             "block_pool": round(float(k_pool), 4), "block_scores": round(float(k_rel), 4),
