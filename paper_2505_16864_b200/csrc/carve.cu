@@ -17,6 +17,7 @@
 //                    the common (m, d): fp32 inputs and shapes the tcgen05 kernel does
 //                    not take; mirrors the reference's per-block streaming order (1e-5).
 //  * k_carve_simt -- fp32 math, one warp per query row, any (m, d): the fallback.
+#include <atomic>
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -809,6 +810,14 @@ static int make_tmap(CUtensorMap* tm, const void* base, int d, int64_t n_pad, in
   return TCB_OK;
 }
 
+// Kernel attributes are per device: remember, thread-safely, which devices already have them.
+static bool first_on_device(std::atomic<uint64_t>& seen) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  return !(seen.fetch_or(bit) & bit);
+}
+
 static int validate(const void* q, const void* k, const void* v, void* o, int dtype,
                     const int32_t* kv_idx, const int32_t* kv_cnt, const CarveShape& s) {
   TCB_CHECK_ARG(q && k && v && o, TCB_ESHAPE, "null q/k/v/o");
@@ -832,12 +841,11 @@ static int launch_f32t(const void* q, const void* k, const void* v, void* o, con
   constexpr int M = 16 * MT, D = 16 * DT;
   size_t smem = (size_t)3 * M * (D + 1) * sizeof(float);
   if (M * (M + 1) > M * (D + 1)) smem += (size_t)M * (M + 1) * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(k_carve_f32t<T, MT, DT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "f32t smem: %s", cudaGetErrorString(e));
-    attr = true;
   }
   const float scale = (float)(1.0 / sqrt((double)s.d));
   k_carve_f32t<T, MT, DT><<<(unsigned)((int64_t)s.H * s.M_total), 256, smem, st>>>(
@@ -916,12 +924,11 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
   if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::HN, !tc::Elem<E>::kBf16))) return rc;
   if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::HN, !tc::Elem<E>::kBf16))) return rc;
   const int smem = tc::Smem<D>::BYTES;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(tc::k_carve_tc<D, EMU, E>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
-    attr_set = true;
   }
   cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
   if (e != cudaSuccess) return set_error(TCB_ECUDA, "memset counter: %s", cudaGetErrorString(e));
