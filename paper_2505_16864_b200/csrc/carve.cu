@@ -770,397 +770,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
 
 }  // namespace tc
 
-// =====================================================================================
-// tcgen05 kernel, split-key variant (TCB_CARVE_V6=1 while under test).  One CTA per SM,
-// one query tile at a time, full 128-key blocks: QK^T at M = N = 128 (full tensor rate).
-// TMEM (512 columns): S0 [0,128), S1 [128,256) -- S double-buffered so QK(j+2) overlaps the
-// softmax of block j+1 -- and two output accumulators O_A [256,384), O_B [384,512).
-// The softmax runs in two independent warp groups: group A owns keys 0..63 of every block,
-// group B keys 64..127, each with its own running max / sum and its own accumulator
-// (PV_A over keys 0..63 into O_A, PV_B over keys 64..127 into O_B).  So each SMSP hosts two
-// softmax warps that never wait for each other (no row-max exchange per block); the two
-// halves are merged once per item in the epilogue:
-//   O = (O_A 2^(m_A - m) + O_B 2^(m_B - m)) / (l_A 2^(m_A - m) + l_B 2^(m_B - m)).
-// =====================================================================================
-namespace tc6 {
-
-using tc::BM;
-using tc::BK;
-using tc::HN;
-constexpr int NUM_THREADS = 352;  // w0 TMA, w1 QK MMA + TMEM owner, w2..5 group A, w6..9 group B,
-                                  // w10 PV MMA
-constexpr int TMEM_COLS = 512;
-constexpr int OA_COL = 256, OB_COL = 384;
-constexpr int QS = 2, KS = 2, VS = 3;
-constexpr float RESCALE_THRESHOLD = 8.0f;
-
-template <int D>
-struct Smem {
-  static constexpr int TILE = BM * D * 2;  // Q, K or V block
-  static constexpr int CHUNKS = D / 64;
-  static constexpr int CHUNK = BM * 128;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = QS * TILE;
-  static constexpr int OFF_V = OFF_K + KS * TILE;
-  static constexpr int OFF_BAR = OFF_V + VS * TILE;
-  static constexpr int BYTES = OFF_BAR + 3072;
-};
-
-struct Bars {
-  uint64_t q_full[QS], q_empty[QS];
-  uint64_t k_full[KS], k_empty[KS], v_full[VS], v_empty[VS];
-  uint64_t s_full[2], s_free[2], p_full[2][2];  // p_full[group][S buffer]
-  uint64_t o_done[2], o_full, o_empty;
-  uint64_t sched_full[2], sched_empty[2];
-  int sched_item[2];
-  uint32_t tmem_base;
-  float2 ml[2][128];  // per group, per row: (m, l) for the epilogue merge
-};
-static_assert(sizeof(Bars) <= 3072, "barrier block must fit the reserved smem");
-
-template <int D, typename E = __nv_bfloat16>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    k_carve_tc6(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                const __grid_constant__ CUtensorMap tm_v, E* __restrict__ o, CarveShape s,
-                const int32_t* __restrict__ kv_idx, const int32_t* __restrict__ kv_cnt,
-                int* __restrict__ counter, int total_items, float scale_log2, float beta_log2,
-                int dbg) {
-  using L = Smem<D>;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sQ = smem + L::OFF_Q;
-  uint8_t* sK = smem + L::OFF_K;
-  uint8_t* sV = smem + L::OFF_V;
-  Bars* bars = reinterpret_cast<Bars*>(smem + L::OFF_BAR);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-
-  if (threadIdx.x == 0) {
-    if (ptx::smem_u32(smem) & 1023u) __trap();
-    for (int i = 0; i < QS; ++i) {
-      ptx::mbar_init(&bars->q_full[i], 1);
-      ptx::mbar_init(&bars->q_empty[i], 1);
-    }
-    for (int i = 0; i < KS; ++i) {
-      ptx::mbar_init(&bars->k_full[i], 1);
-      ptx::mbar_init(&bars->k_empty[i], 1);
-    }
-    for (int i = 0; i < VS; ++i) {
-      ptx::mbar_init(&bars->v_full[i], 1);
-      ptx::mbar_init(&bars->v_empty[i], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&bars->s_full[b], 1);
-      ptx::mbar_init(&bars->s_free[b], 1);
-      ptx::mbar_init(&bars->p_full[0][b], 128);
-      ptx::mbar_init(&bars->p_full[1][b], 128);
-      ptx::mbar_init(&bars->o_done[b], 1);
-      ptx::mbar_init(&bars->sched_full[b], 1);
-      ptx::mbar_init(&bars->sched_empty[b], 3);  // QK warp, PV warp, softmax groups
-    }
-    ptx::mbar_init(&bars->o_full, 1);
-    ptx::mbar_init(&bars->o_empty, 256);
-    ptx::fence_mbar_init();
-    ptx::tma_prefetch_desc(&tm_q);
-    ptx::tma_prefetch_desc(&tm_k);
-    ptx::tma_prefetch_desc(&tm_v);
-  }
-  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(&bars->tmem_base);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
-
-  if (warp == 0) {
-    // ============================ TMA producer + scheduler ============================
-    // ring order = MMA consumption: K(0) K(1) | V(0) K(2) | V(1) K(3) | ...
-    const uint64_t pol_kv = ptx::policy_evict_last();
-    const uint64_t pol_q = ptx::policy_evict_first();
-    uint32_t gk = 0, gv = 0, qn = 0;
-    for (uint32_t it = 0;; ++it) {
-      const int slot = it & 1;
-      int item = 0;
-      if (lane == 0) {
-        ptx::mbar_wait(&bars->sched_empty[slot], ((it >> 1) & 1) ^ 1);
-        item = atomicAdd(counter, 1);
-        if (item >= total_items) item = -1;
-        bars->sched_item[slot] = item;
-        ptx::mbar_arrive(&bars->sched_full[slot]);
-      }
-      item = __shfl_sync(0xffffffffu, item, 0);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-      if (n == 0) continue;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      const uint64_t pol = vis ? pol_kv : pol_q;
-      if (lane == 0) {
-        const int qs = qn % QS;
-        ptx::mbar_wait(&bars->q_empty[qs], ((qn / QS) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&bars->q_full[qs], L::TILE);
-#pragma unroll
-        for (int c = 0; c < L::CHUNKS; ++c)
-          ptx::tma_load_3d(sQ + qs * L::TILE + c * L::CHUNK, &tm_q, &bars->q_full[qs], c * 64,
-                           qb * BM, h, pol_q);
-      }
-      ++qn;
-      auto load = [&](bool is_v, int b) {
-        uint32_t& cnt = is_v ? gv : gk;
-        const int slots = is_v ? VS : KS;
-        if (lane == 0) {
-          const int sl = cnt % slots;
-          uint64_t* full = is_v ? bars->v_full : bars->k_full;
-          uint64_t* empty = is_v ? bars->v_empty : bars->k_empty;
-          ptx::mbar_wait(&empty[sl], ((cnt / slots) & 1) ^ 1);
-          if ((dbg & 1) && cnt >= (uint32_t)slots) {  // timing experiment: no operand traffic
-            ptx::mbar_arrive(&full[sl]);
-          } else {
-            ptx::mbar_arrive_expect_tx(&full[sl], L::TILE);
-            uint8_t* base = (is_v ? sV : sK) + sl * L::TILE;
-#pragma unroll
-            for (int c = 0; c < L::CHUNKS; ++c)
-              ptx::tma_load_3d(base + c * L::CHUNK, is_v ? &tm_v : &tm_k, &full[sl], c * 64, b * BK,
-                               h, pol);
-          }
-        }
-        ++cnt;
-      };
-      load(false, kl.block(0));
-      if (n > 1) load(false, kl.block(1));
-      for (int j = 0; j < n; ++j) {
-        load(true, kl.block(j));
-        if (j + 2 < n) load(false, kl.block(j + 2));
-      }
-    }
-  } else if (warp == 1 || warp == 10) {
-    // ============================ MMA issuers ============================
-    // warp 1: S(j) = Q K(j)^T into S[j & 1] as soon as PV(j-2) released the buffer;
-    // warp 10: O_g (+)= P_g(j) V(j) as the softmax groups publish P.  Two independent
-    // issue streams keep the tcgen05 queue fed while either one waits on a barrier.
-    constexpr uint32_t IDESC_S = tc::make_idesc(BM, BK, 0, tc::Elem<E>::kBf16);
-    constexpr uint32_t IDESC_O = tc::make_idesc(BM, D, 1, tc::Elem<E>::kBf16);
-    const bool is_qk = warp == 1;
-    const uint32_t aQ = ptx::smem_u32(sQ), aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
-    uint32_t gk = 0, gv = 0, gb = 0, qn = 0, items = 0;
-    for (uint32_t it = 0;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
-      const int item = __shfl_sync(0xffffffffu, bars->sched_item[slot], 0);
-      if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = __shfl_sync(0xffffffffu, vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total, 0);
-      const uint32_t prev_items = items++;
-      if (is_qk) {
-        if (n == 0) continue;
-        const int qs = qn % QS;
-        ptx::mbar_wait(&bars->q_full[qs], (qn / QS) & 1);
-        ++qn;
-        const uint32_t qa = aQ + qs * L::TILE;
-        for (int j = 0; j < n; ++j, ++gb, ++gk) {
-          const uint32_t b = gb & 1;
-          if (gb >= 2) ptx::mbar_wait(&bars->s_free[b], ((gb >> 1) - 1) & 1);
-          const int sl = gk % KS;
-          ptx::mbar_wait(&bars->k_full[sl], (gk / KS) & 1);
-          ptx::tc_fence_after();
-          if (ptx::elect_one()) {
-            const uint32_t kb = aK + sl * L::TILE;
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint32_t off = (kk >> 2) * L::CHUNK + (kk & 3) * 32;
-              ptx::mma_ss(tmem + b * 128, tc::make_sdesc(qa + off, 16, 1024),
-                          tc::make_sdesc(kb + off, 16, 1024), IDESC_S, kk > 0 ? 1u : 0u);
-            }
-            ptx::mma_commit(&bars->k_empty[sl]);
-            ptx::mma_commit(&bars->s_full[b]);
-            if (j + 1 == n) ptx::mma_commit(&bars->q_empty[qs]);
-          }
-          __syncwarp();
-        }
-      } else {
-        if (n == 0) {  // cannot come from build_block_mask; keep the epilogue in step
-          if (prev_items > 0) ptx::mbar_wait(&bars->o_empty, (prev_items - 1) & 1);
-          if (ptx::elect_one()) ptx::mma_commit(&bars->o_full);
-          __syncwarp();
-          continue;
-        }
-        for (int j = 0; j < n; ++j, ++gb) {
-          const uint32_t b = gb & 1;
-          const int vs = gv % VS;
-          ptx::mbar_wait(&bars->v_full[vs], (gv / VS) & 1);
-          ++gv;
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {  // O_g (+)= P_g V over keys [64 g, 64 g + 64)
-            ptx::mbar_wait(&bars->p_full[g][b], (gb >> 1) & 1);
-            if (g == 0 && j == 0 && prev_items > 0)  // the previous item's epilogue read O
-              ptx::mbar_wait(&bars->o_empty, (prev_items - 1) & 1);
-            ptx::tc_fence_after();
-            if (ptx::elect_one()) {
-#pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                const uint32_t vb = aV + vs * L::TILE + (64 * g + 16 * kk) * 128;
-                ptx::mma_ts(tmem + (g ? OB_COL : OA_COL), tmem + b * 128 + 64 * g + kk * 8,
-                            tc::make_sdesc(vb, L::CHUNK, 1024), IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
-              }
-              ptx::mma_commit(&bars->o_done[g]);
-              if (g == 1) {
-                ptx::mma_commit(&bars->v_empty[vs]);
-                ptx::mma_commit(&bars->s_free[b]);
-                if (j + 1 == n) ptx::mma_commit(&bars->o_full);
-              }
-            }
-            __syncwarp();
-          }
-        }
-      }
-    }
-  } else {
-    // ============================ softmax groups / epilogue ============================
-    const int g = (warp - 2) >> 2;  // 0: keys 0..63 of each block, 1: keys 64..127
-    const int quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t t_row = tmem + ((uint32_t)(quarter * 32) << 16);
-    const uint32_t o_col = g ? OB_COL : OA_COL;
-    uint32_t G = 0;  // global block counter (S buffer G & 1, phase (G >> 1) & 1)
-    for (uint32_t it = 0;; ++it) {
-      const int slot = it & 1;
-      ptx::mbar_wait(&bars->sched_full[slot], (it >> 1) & 1);
-      const int item = bars->sched_item[slot];
-      ptx::named_bar_sync(1, 256);
-      if (threadIdx.x == 64) ptx::mbar_arrive(&bars->sched_empty[slot]);
-      if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
-      const bool vis = qb < s.M_v;
-      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      tc::KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
-      float m_run = -INFINITY, l_run = 0.f;
-      for (int j = 0; j < n; ++j, ++G) {
-        const uint32_t b = G & 1;
-        const int blk = kl.block(j);
-        const int hvalid = block_valid(blk, BK, s.M_v, s.n_valid, s.n_cond) - 64 * g;
-        const float bias = (vis && blk >= s.M_v) ? beta_log2 : 0.f;
-        ptx::mbar_wait(&bars->s_full[b], (G >> 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t scol = t_row + b * 128 + 64 * g;
-        if (dbg & 2) {  // timing experiment: no softmax work
-          l_run = 1.f;
-          m_run = 0.f;
-          ptx::mbar_arrive(&bars->p_full[g][b]);
-          continue;
-        }
-        uint32_t sr[64];
-        ptx::tmem_ld32(scol, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-        ptx::tmem_ld32(scol + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-        ptx::tmem_wait_ld();
-        if (hvalid < HN) {  // padding keys of a partial block -> -inf (attention.py:193)
-#pragma unroll
-          for (int e = 0; e < 64; ++e)
-            if (e >= hvalid) sr[e] = __float_as_uint(-INFINITY);
-        }
-        float mx8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
-#pragma unroll
-        for (int e = 8; e < 64; e += 16)
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            mx8[q] = tc::fmax3(mx8[q], __uint_as_float(sr[e + q]), __uint_as_float(sr[e + 8 + q]));
-        const float mraw = tc::fmax3(tc::fmax3(mx8[0], mx8[1], mx8[2]),
-                                     tc::fmax3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-        const float m_blk = (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
-        const float m_new = fmaxf(m_run, m_blk);
-        // nothing accumulated yet (O_g is exactly 0): adopt the block max, no rescale
-        const bool first = (m_run == -INFINITY);
-        const bool need = !first && (m_new > m_run + RESCALE_THRESHOLD);
-        const float m_use = (first || need) ? m_new : m_run;
-        const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
-        if (__any_sync(0xffffffffu, need)) {
-          // O_g is final only once PV_g(j-1) retired: o_done[g] completes once per PV_g
-          ptx::mbar_wait(&bars->o_done[g], (G - 1) & 1);
-          ptx::tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            ptx::tmem_ld32(t_row + o_col + c * 32, ov);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            ptx::tmem_st32(t_row + o_col + c * 32, ov);
-          }
-        }
-        const float c0 = (m_use == -INFINITY) ? 0.f : bias - m_use;
-        const uint64_t sc2 = tc::f2_pack(scale_log2, scale_log2), c02 = tc::f2_pack(c0, c0);
-        uint64_t acc2[4] = {0, 0, 0, 0};
-        uint32_t pk[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const uint64_t x = tc::ffma2(
-              tc::f2_pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sc2, c02);
-          const float p0 = ptx::ex2(tc::f2_lo(x)), p1 = ptx::ex2(tc::f2_hi(x));
-          acc2[e & 3] = tc::fadd2(acc2[e & 3], tc::f2_pack(p0, p1));
-          pk[e] = tc::Elem<E>::pack(p0, p1);
-        }
-        ptx::tmem_st32(scol, pk);
-        const uint64_t sum2 = tc::fadd2(tc::fadd2(acc2[0], acc2[1]), tc::fadd2(acc2[2], acc2[3]));
-        l_run = l_run * alpha + (tc::f2_lo(sum2) + tc::f2_hi(sum2));
-        m_run = m_use;
-        ptx::tmem_wait_st();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&bars->p_full[g][b]);
-      }
-      // ---- epilogue: merge the two key halves, O / l -> row, padding rows zero ----
-      bars->ml[g][row] = make_float2(m_run, l_run);
-      ptx::mbar_wait(&bars->o_full, it & 1);
-      ptx::tc_fence_after();
-      ptx::named_bar_sync(1, 256);
-      const float2 mine = bars->ml[g][row], other = bars->ml[g ^ 1][row];
-      const float2 mA = g ? other : mine, mB = g ? mine : other;
-      const float mm = fmaxf(mA.x, mB.x);
-      const float sA = (mA.x == -INFINITY) ? 0.f : ptx::ex2(mA.x - mm);
-      const float sB = (mB.x == -INFINITY) ? 0.f : ptx::ex2(mB.x - mm);
-      const float lsum = mA.y * sA + mB.y * sB;
-      const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
-      const bool live = row < qvalid && n > 0 && lsum > 0.f;
-      const float fA = live ? sA / lsum : 0.f, fB = live ? sB / lsum : 0.f;
-      constexpr int HD = D / 2;  // this group writes output columns [HD g, HD g + HD)
-      E* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn + HD * g;
-#pragma unroll 1
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t oa[32], ob[32];
-        ptx::tmem_ld32(t_row + OA_COL + HD * g + 32 * c, oa);
-        ptx::tmem_ld32(t_row + OB_COL + HD * g + 32 * c, ob);
-        ptx::tmem_wait_ld();
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float v0 = fA * __uint_as_float(oa[2 * e]) + fB * __uint_as_float(ob[2 * e]);
-          const float v1 = fA * __uint_as_float(oa[2 * e + 1]) + fB * __uint_as_float(ob[2 * e + 1]);
-          pk[e] = live ? tc::Elem<E>::pack(v0, v1) : 0u;
-        }
-        int4* dst = reinterpret_cast<int4*>(orow + 32 * c);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          __stcs(dst + e, make_int4((int)pk[4 * e], (int)pk[4 * e + 1], (int)pk[4 * e + 2],
-                                    (int)pk[4 * e + 3]));
-      }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&bars->o_empty);
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<TMEM_COLS>(tmem);
-  }
-}
-
-}  // namespace tc6
-
 
 
 
@@ -1340,40 +949,6 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
 
 
 
-template <int D, typename E = __nv_bfloat16>
-static int launch_tc6(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                      const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
-                      cudaStream_t st) {
-  CUtensorMap tq, tk, tv;
-  const int64_t n_pad = (int64_t)s.M_total * s.m;
-  constexpr bool f16 = !tc::Elem<E>::kBf16;
-  int rc;
-  if ((rc = make_tmap(&tq, q, D, n_pad, s.H, s.sh, s.sn, tc::BM, f16))) return rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::BK, f16))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::BK, f16))) return rc;
-  const int smem = tc6::Smem<D>::BYTES;
-  static std::atomic<uint64_t> attr{0};
-  if (first_on_device(attr)) {
-    cudaError_t e = cudaFuncSetAttribute(tc6::k_carve_tc6<D, E>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
-  }
-  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
-  if (e != cudaSuccess) return set_error(TCB_ECUDA, "memset counter: %s", cudaGetErrorString(e));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int total = s.H * s.M_total;
-  int grid = sms;
-  if (grid > total) grid = total;
-  const float LOG2E = 1.4426950408889634f;
-  const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  tc6::k_carve_tc6<D, E><<<grid, tc6::NUM_THREADS, smem, st>>>(tq, tk, tv, (E*)o, s, kv_idx, kv_cnt,
-                                                              work, total, scale_log2, beta * LOG2E,
-                                                              dbg_flags());
-  return check_launch("k_carve_tc6");
-}
-
 extern "C" int tcb_carve_fwd_simt(const void* q, const void* k, const void* v, void* o, int dtype,
                                   int64_t stride_h, int64_t stride_n, const int32_t* kv_idx,
                                   const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
@@ -1406,18 +981,6 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
     if (emu != 0 && emu != 2 && emu != 3 && emu != 4) emu = 0;
   }
   cudaStream_t st = as_stream(stream);
-  static int v6 = -1;
-  if (v6 < 0) {
-    const char* env = getenv("TCB_CARVE_V6");
-    v6 = env ? atoi(env) : 0;
-  }
-  if (v6) {
-    if (dtype == TCB_F16)
-      return d == 128 ? launch_tc6<128, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
-                      : launch_tc6<64, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-    return d == 128 ? launch_tc6<128>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
-                    : launch_tc6<64>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-  }
   if (dtype == TCB_F16)  // fp16 operands and P (kind::f16 with f16 inputs), f32 accumulation
     return d == 128 ? launch_tc<128, 0, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
                     : launch_tc<64, 0, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);

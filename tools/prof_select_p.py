@@ -10,7 +10,7 @@ st = tcb.StaticMasks.build(lay, g, tcb.build_curve(g))
 gen = torch.Generator(device="cuda").manual_seed(0)
 q, k = (torch.randn((24, lay.padded_total, 128), generator=gen, device="cuda").to(torch.bfloat16) for _ in range(2))
 p = float(sys.argv[1]) if len(sys.argv) > 1 else 0.3
-for _ in range(4):
+for _ in range(3):
     m, _ = tcb.build_block_mask(q, k, lay, st, tcb.SelectionParams(k=0.2, p=p))
 torch.cuda.synchronize()
 print("kept", m.selected_fraction)
