@@ -681,6 +681,40 @@ __device__ __forceinline__ void reg_bitonic_level_u(uint64_t (&y)[16], int lane)
   if constexpr (KK < 512) reg_bitonic_level_u<KK * 2>(y, lane);
 }
 
+// Keys only, R per lane (element e = R * lane + r): ascending 64-bit keys -- what the exact
+// prefix scan needs (equal keys are equal values, so their order cannot change a sum).
+template <int R, int KK, int JJ>
+__device__ __forceinline__ void keys_bitonic_stage(uint64_t (&y)[R], int lane) {
+  if constexpr (JJ >= R) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int e = lane * R + r;
+      const uint64_t o = __shfl_xor_sync(FULL, y[r], JJ / R);
+      const bool up = (e & KK) == 0, lower = (e & JJ) == 0;
+      const bool take_o = (up == lower) ? (o < y[r]) : (y[r] < o);
+      if (take_o) y[r] = o;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r & JJ) continue;
+      const bool up = ((lane * R + r) & KK) == 0;
+      if ((y[r | JJ] < y[r]) == up) {
+        const uint64_t t = y[r];
+        y[r] = y[r | JJ];
+        y[r | JJ] = t;
+      }
+    }
+  }
+  if constexpr (JJ > 1) keys_bitonic_stage<R, KK, JJ / 2>(y, lane);
+}
+
+template <int R, int KK>
+__device__ __forceinline__ void keys_bitonic_level(uint64_t (&y)[R], int lane) {
+  keys_bitonic_stage<R, KK, KK / 2>(y, lane);
+  if constexpr (KK < 32 * R) keys_bitonic_level<R, KK * 2>(y, lane);
+}
+
 // Sort the window x[16] (cnt real entries, the rest padding ~0 / INT_MAX) by (key, col);
 // packed single-word compares when the keys leave room for the column, KC compares otherwise.
 __device__ __forceinline__ void reg_sort_window(KC (&x)[16], int cnt, int M_total) {
@@ -878,8 +912,9 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
     // from an external R) the smem path below sorts as much as needed.
     const int k_ub = min(512, M_total);
     bool done = false;
-    if (!neg && k_ub <= 512) {
+    if (MODE != 2 && !neg && k_ub <= 512) {
       // common case: the crossing lies in the top <= 512 -> register sort + shuffle scan
+      // (MODE 2 only sees the rows where this already failed)
       const RadixState t = warp_radix(keys, M_total, k_ub, hist);
       uint64_t* stage_k = skey;  // staging with one pad slot per 16 (conflict-free lane reads)
       int* stage_c = scol;
@@ -925,6 +960,33 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
     if (MODE == 1 && !done) {  // decided by the MODE 2 pass
       if (lane == 0) kv_cnt[row] = -1;
       return;
+    }
+    if (!done && !neg && M_total <= 1024) {
+      // whole row in registers (32 keys per lane), keys only; then the exact sequential
+      // scan by lane 0 over the sorted keys staged with one pad slot per 32 (the staging
+      // may run 32 slots past skey's np2 into scol, which this path does not use)
+      uint64_t y[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int j = lane * 32 + r;
+        y[r] = j < M_total ? keys[j] : ~0ull;
+      }
+      keys_bitonic_level<32, 2>(y, lane);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) skey[lane * 33 + r] = y[r];
+      __syncwarp();
+      int c = 0;
+      if (lane == 0) {
+        double pre = 0.0;
+#pragma unroll 8
+        for (int t = 0; t < M_total; ++t) {
+          pre = __dadd_rn(pre, key_value(skey[t + (t >> 5)]));  // np.cumsum order (masks.py:152)
+          if (pre > p) break;
+          ++c;
+        }
+      }
+      n_cut = __shfl_sync(FULL, c, 0) + 1;
+      done = true;
     }
     if (!done) {  // full sort of the row in shared memory, exact scan
       for (int j = lane; j < M_total; j += 32) { skey[j] = keys[j]; scol[j] = j; }
