@@ -779,6 +779,55 @@ __device__ int reg_sorted_cut(const KC (&x)[16], uint64_t* stage, int cnt, doubl
   return __shfl_sync(FULL, c, 0) + 1;
 }
 
+// The crossing rank of the exact sequential prefix (np.cumsum, masks.py:152) without the
+// dependent fp64 chain when possible.  Sorted keys are held R per lane (element e = R lane + r);
+// a warp-parallel prefix (in-lane sums + a shuffle scan) differs from the sequential one by
+// at most ~(e + R + 5) u S_e for non-negative values (u = 2^-53), far below a 1e-12
+// relative margin, so every prefix outside that margin around p compares exactly as the
+// sequential one does.  Returns 1 + #(prefix <= p) (and *crossed), or -1 when some prefix
+// lies inside the margin -- the caller then replays the sequential chain.
+template <int R, typename KeyOf>
+__device__ __forceinline__ int par_cut(KeyOf key_of, int cnt, double p, bool* crossed) {
+  const int lane = threadIdx.x & 31;
+  double tot = 0.0;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (lane * R + r < cnt) tot += key_value(key_of(r));
+  double inc = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(FULL, inc, o);
+    if (lane >= o) inc += y;
+  }
+  double pre = __shfl_up_sync(FULL, inc, 1);
+  if (lane == 0) pre = 0.0;
+  int first = 0x7fffffff;
+  bool amb = false;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = lane * R + r;
+    if (e < cnt && first == 0x7fffffff) {
+      pre += key_value(key_of(r));
+      const double m = 1e-12 * pre;
+      if (pre > p - m) {
+        first = e;
+        amb = !(pre - m > p);
+      }
+    }
+  }
+  int f = first;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) f = min(f, __shfl_xor_sync(FULL, f, o));
+  if (f == 0x7fffffff) {  // every prefix certainly <= p
+    *crossed = false;
+    return cnt + 1;
+  }
+  const int src = __ffs(__ballot_sync(FULL, first == f)) - 1;
+  if (__shfl_sync(FULL, (int)amb, src)) return -1;
+  *crossed = true;
+  return f + 1;
+}
+
 // Sort (key, col) pairs [0, cnt) of skey/scol (padded to np2) and return
 // 1 + #(sequential prefix <= p) over the sorted values; *crossed reports whether the
 // monotone prefix exceeded p inside the sorted window.
@@ -943,7 +992,8 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
       reg_sort_window(x, k_ub, M_total);
       bool crossed;
       __syncwarp();
-      n_cut = reg_sorted_cut(x, stage_k, k_ub, p, &crossed);
+      n_cut = par_cut<16>([&](int r) { return x[r].k; }, k_ub, p, &crossed);
+      if (n_cut < 0) n_cut = reg_sorted_cut(x, stage_k, k_ub, p, &crossed);
       if (crossed || k_ub == M_total) {
         done = true;
         reg_keep = max(n_cut, n_floor);
@@ -972,20 +1022,24 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
         y[r] = j < M_total ? keys[j] : ~0ull;
       }
       keys_bitonic_level<32, 2>(y, lane);
+      bool crossed;
+      n_cut = par_cut<32>([&](int r) { return y[r]; }, M_total, p, &crossed);
+      if (n_cut < 0) {
 #pragma unroll
-      for (int r = 0; r < 32; ++r) skey[lane * 33 + r] = y[r];
-      __syncwarp();
-      int c = 0;
-      if (lane == 0) {
-        double pre = 0.0;
+        for (int r = 0; r < 32; ++r) skey[lane * 33 + r] = y[r];
+        __syncwarp();
+        int c = 0;
+        if (lane == 0) {
+          double pre = 0.0;
 #pragma unroll 8
-        for (int t = 0; t < M_total; ++t) {
-          pre = __dadd_rn(pre, key_value(skey[t + (t >> 5)]));  // np.cumsum order (masks.py:152)
-          if (pre > p) break;
-          ++c;
+          for (int t = 0; t < M_total; ++t) {
+            pre = __dadd_rn(pre, key_value(skey[t + (t >> 5)]));  // np.cumsum order (masks.py:152)
+            if (pre > p) break;
+            ++c;
+          }
         }
+        n_cut = __shfl_sync(FULL, c, 0) + 1;
       }
-      n_cut = __shfl_sync(FULL, c, 0) + 1;
       done = true;
     }
     if (!done) {  // full sort of the row in shared memory, exact scan

@@ -278,6 +278,22 @@ def test_select_general_rows_vs_oracle():
             assert np.array_equal(got, oracle.select_topk(R, k, p, n_cols)), (n_cols, k, p)
 
 
+def test_select_cutoff_prefix_on_the_boundary_vs_oracle():
+    # prefixes landing within rounding of p (0.1 + 0.1 + 0.1 = 0.30000000000000004, ...):
+    # the warp-parallel prefix cannot decide these and must replay np.cumsum's chain
+    for n_cols in (10, 40, 900):
+        R = np.zeros((1, 4, n_cols))
+        R[0, :, :10] = 0.1
+        R[0, 1, 10:] = 1e-9
+        R[0, 2, :10] = np.arange(10, 0, -1) * 0.01
+        R[0, 3, :] = np.linspace(1.0, 0.5, n_cols) / n_cols
+        for p in (0.3, 0.7, 0.8, 0.9, 0.1 + 0.2, 0.55, 0.45):
+            for k in (0.01, 0.2):
+                got = tcb.importance_mask(R, tcb.SelectionParams(k=k, p=min(p, 0.95)), n_cols)
+                want = oracle.select_topk(R, k, min(p, 0.95), n_cols)
+                assert np.array_equal(got, want), (n_cols, p, k)
+
+
 def test_select_maximum_columns_vs_oracle():
     # the selection kernels' largest supported row (8,192 blocks = 1M tokens at m = 128),
     # both the quota-only and the cutoff path, then the documented SizeError just beyond
