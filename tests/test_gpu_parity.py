@@ -452,13 +452,14 @@ def test_carve_bf16_fuzz_random_layouts():
     # tcgen05 (bf16, m=128) vs the fp32 oracle on the same mask (2e-2), plus the fp32 SIMT
     # kernel (1e-5) -- exercises 1-block rows, condition-only tails, partial blocks
     rng = np.random.default_rng(2024)
-    for trial in range(10):
+    for trial in range(14):
         dims = tcb.GridDims(int(rng.integers(1, 5)), int(rng.integers(3, 20)), int(rng.integers(3, 24)))
         n_cond = int(rng.choice([0, 1, 77, 128, 300]))
         lay = tcb.build_layout(dims, 128, n_cond)
         H = int(rng.integers(1, 4))
+        d = 64 if trial % 2 else 128  # both head sizes of the tcgen05 kernel
         st = tcb.StaticMasks.build(lay, dims, tcb.build_curve(dims))
-        q, k, v = (rng.standard_normal((H, lay.padded_total, 128)).astype(np.float32)
+        q, k, v = (rng.standard_normal((H, lay.padded_total, d)).astype(np.float32)
                    for _ in range(3))
         qb, kb, vb = (_bf16(a) for a in (q, k, v))
         params = tcb.SelectionParams(k=float(rng.choice([0.05, 0.3, 1.0])),
