@@ -191,13 +191,17 @@ __global__ void __launch_bounds__(256, 1) k_carve_f32t(const T* __restrict__ q, 
                                                        const int32_t* __restrict__ kv_cnt, float beta,
                                                        float scale) {
   constexpr int M = 16 * MT, D = 16 * DT;
-  constexpr int QP = D + 1;   // padded row pitch (floats) of Q / K / V tiles
-  constexpr int PP = M + 1;   // padded row pitch of P
-  extern __shared__ float sm_f32t[];
+  // Q and K stay row-major, V is stored transposed and P row-major, so both inner loops read
+  // their operands as float4 along the reduction axis (4 LDS.128 per 64 FMAs per thread);
+  // the FMA order (c, then key) is the scalar kernel's, so results are unchanged.
+  constexpr int QP = D + 4;   // row pitch (floats) of Q / K: 16-byte rows
+  constexpr int VP = M + 4;   // row pitch of V^T
+  constexpr int PP = M + 4;   // row pitch of P
+  extern __shared__ __align__(16) float sm_f32t[];
   float* sQ = sm_f32t;
   float* sK = sQ + M * QP;
-  float* sV = sK + M * QP;
-  float* sP = (M * PP <= M * QP) ? sK : sV + M * QP;  // P reuses K's tile when it fits
+  float* sVt = sK + M * QP;
+  float* sP = (M * PP <= M * QP) ? sK : sVt + D * VP;  // P reuses K's tile when it fits
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   const int h = blockIdx.x / s.M_total;
   const int qb = blockIdx.x - h * s.M_total;
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(256, 1) k_carve_f32t(const T* __restrict__ q, 
       const int r = e / D, c = e - r * D;
       const int64_t g = ((int64_t)b * M + r) * s.sn + c;
       sK[r * QP + c] = ldf(kh + g);
-      sV[r * QP + c] = ldf(vh + g);
+      sVt[c * VP + r] = ldf(vh + g);
     }
     __syncthreads();
     float sc[MT][MT];
@@ -237,17 +241,22 @@ __global__ void __launch_bounds__(256, 1) k_carve_f32t(const T* __restrict__ q, 
     for (int i = 0; i < MT; ++i)
 #pragma unroll
       for (int j = 0; j < MT; ++j) sc[i][j] = 0.f;
-#pragma unroll 4
-    for (int c = 0; c < D; ++c) {
-      float a[MT], bk[MT];
+#pragma unroll 2
+    for (int c = 0; c < D; c += 4) {
+      float4 a[MT], bk[MT];
 #pragma unroll
-      for (int i = 0; i < MT; ++i) a[i] = sQ[(ty + 16 * i) * QP + c];
+      for (int i = 0; i < MT; ++i) a[i] = *reinterpret_cast<const float4*>(sQ + (ty + 16 * i) * QP + c);
 #pragma unroll
-      for (int j = 0; j < MT; ++j) bk[j] = sK[(tx + 16 * j) * QP + c];
+      for (int j = 0; j < MT; ++j) bk[j] = *reinterpret_cast<const float4*>(sK + (tx + 16 * j) * QP + c);
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < MT; ++j) sc[i][j] = fmaf(a[i], bk[j], sc[i][j]);
+        for (int j = 0; j < MT; ++j) {
+          float x = fmaf(a[i].x, bk[j].x, sc[i][j]);
+          x = fmaf(a[i].y, bk[j].y, x);
+          x = fmaf(a[i].z, bk[j].z, x);
+          sc[i][j] = fmaf(a[i].w, bk[j].w, x);
+        }
     }
     __syncthreads();  // K tile consumed (P may overwrite it)
     float alpha[MT];
@@ -282,17 +291,22 @@ __global__ void __launch_bounds__(256, 1) k_carve_f32t(const T* __restrict__ q, 
     for (int i = 0; i < MT; ++i)
 #pragma unroll
       for (int j = 0; j < DT; ++j) acc[i][j] *= alpha[i];
-#pragma unroll 4
-    for (int jk = 0; jk < M; ++jk) {
-      float pr[MT], vv[DT];
+#pragma unroll 2
+    for (int jk = 0; jk < M; jk += 4) {
+      float4 pr[MT], vv[DT];
 #pragma unroll
-      for (int i = 0; i < MT; ++i) pr[i] = sP[(ty + 16 * i) * PP + jk];
+      for (int i = 0; i < MT; ++i) pr[i] = *reinterpret_cast<const float4*>(sP + (ty + 16 * i) * PP + jk);
 #pragma unroll
-      for (int j = 0; j < DT; ++j) vv[j] = sV[jk * QP + tx + 16 * j];
+      for (int j = 0; j < DT; ++j) vv[j] = *reinterpret_cast<const float4*>(sVt + (tx + 16 * j) * VP + jk);
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < DT; ++j) acc[i][j] = fmaf(pr[i], vv[j], acc[i][j]);
+        for (int j = 0; j < DT; ++j) {
+          float x = fmaf(pr[i].x, vv[j].x, acc[i][j]);
+          x = fmaf(pr[i].y, vv[j].y, x);
+          x = fmaf(pr[i].z, vv[j].z, x);
+          acc[i][j] = fmaf(pr[i].w, vv[j].w, x);
+        }
     }
   }
   T* oh = o + (int64_t)h * s.sh;
@@ -839,8 +853,9 @@ template <typename T, int MT, int DT>
 static int launch_f32t(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
                        const int32_t* kv_idx, const int32_t* kv_cnt, float beta, cudaStream_t st) {
   constexpr int M = 16 * MT, D = 16 * DT;
-  size_t smem = (size_t)3 * M * (D + 1) * sizeof(float);
-  if (M * (M + 1) > M * (D + 1)) smem += (size_t)M * (M + 1) * sizeof(float);
+  // Q, K (M x (D+4)), V^T (D x (M+4)), and P (M x (M+4)) unless it fits in K's tile
+  size_t smem = ((size_t)2 * M * (D + 4) + (size_t)D * (M + 4)) * sizeof(float);
+  if (M + 4 > D + 4) smem += (size_t)M * (M + 4) * sizeof(float);
   static std::atomic<uint64_t> attr{0};
   if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(k_carve_f32t<T, MT, DT>,
