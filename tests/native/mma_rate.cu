@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(128) k_rate(int iters, unsigned long long* cyc
   uint8_t* sK = smem + QB;
   uint8_t* sV = smem + 2 * QB;
   __shared__ uint64_t bar[4];
+  __shared__ uint64_t donebar;  // a barrier whose phase 0 has completed (MODE >= 10 waits)
   __shared__ uint64_t cfull[8], cempty[8];  // copy ring (RS slots of 16 KB)
   uint8_t* ring = FREE ? smem + 3 * QB : sK;  // coupled mode aliases the K/V operands
   __shared__ uint32_t tbase;
@@ -52,11 +53,13 @@ __global__ void __launch_bounds__(128) k_rate(int iters, unsigned long long* cyc
     reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u ^ (i * 2654435761u & 0x00ff00ffu);
   if (threadIdx.x == 0) {
     for (int i = 0; i < 4; ++i) ptx::mbar_init(&bar[i], 1);
+    ptx::mbar_init(&donebar, 1);
     for (int i = 0; i < 8; ++i) {
       ptx::mbar_init(&cfull[i], 1);
       ptx::mbar_init(&cempty[i], 1);
     }
     ptx::fence_mbar_init();
+    ptx::mbar_arrive(&donebar);
   }
   if (threadIdx.x < 32) ptx::tmem_alloc<TCOLS>(&tbase);
   ptx::tc_fence_before();
@@ -112,6 +115,37 @@ __global__ void __launch_bounds__(128) k_rate(int iters, unsigned long long* cyc
         ptx::mbar_wait(&cfull[c % RS], (c / RS) & 1);
       }
       ptx::tc_fence_after();
+      if constexpr (MODE >= 10) {  // single-tile split-key block: PV_A, PV_B, QK with NW
+        constexpr int NW = MODE - 10;  // already-satisfied barrier waits per block
+        auto wt = [&](int i) { if (i < NW) ptx::mbar_wait(&donebar, 0); };
+        wt(0);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            ptx::mma_ts(tmem + 256, tmem + kk * 8, make_sdesc(aV + kk * 16 * 128, N * 128, 1024), IO, 1);
+        }
+        __syncwarp();
+        wt(1);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 4; kk < 8; ++kk)
+            ptx::mma_ts(tmem + 384, tmem + 64 + (kk - 4) * 8, make_sdesc(aV + kk * 16 * 128, N * 128, 1024), IO, 1);
+        }
+        __syncwarp();
+        wt(2);
+        wt(3);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+            ptx::mma_ss(tmem, make_sdesc(aQ + off, 16, 1024), make_sdesc(aK + off, 16, 1024), IS, kk > 0);
+          }
+          ptx::mma_commit(&bar[it & 3]);
+        }
+        __syncwarp();
+        if (it >= 3) ptx::mbar_wait(&bar[(it - 3) & 3], ((it - 3) >> 2) & 1);
+        continue;
+      }
       if (!WARP || elect_one()) {
       if (MODE == 0 || MODE == 3) {
 #pragma unroll
@@ -215,6 +249,7 @@ void run(const char* name, int occ) {
   if (MODE >= 2 && MODE != 5 && MODE < 6) macs += 128.0 * N * D;
   if (MODE == 6 || MODE == 9) macs = 2 * 128.0 * N * D;
   if (MODE == 7 || MODE == 8) macs = 4 * 128.0 * N * D;
+  if (MODE >= 10) macs = 2 * 128.0 * N * D;
   const double per_sm_cyc = (double)mx / iters / occ;  // cycles per iteration per SM
   const double tflops = 2.0 * macs * iters * grid / (ms * 1e-3) / 1e12;
   if (FREE) {
@@ -233,10 +268,10 @@ int main() {
   setvbuf(stdout, nullptr, _IONBF, 0);
   cudaMalloc(&g_src, SRC_BYTES);
   cudaMemset(g_src, 0x3c, SRC_BYTES);
-  run<128, 3, 256, 0, 1, 0, 1>("SS QK + TS PV (indep.)", 1);
   run<128, 9, 512, 0, 1, 0, 1>("1 tile QK->PV (RAW on S)", 1);
-  run<128, 6, 512, 0, 1, 0, 1>("1 tile PV->QK (WAR on S)", 1);
-  run<128, 7, 512, 0, 1, 0, 1>("2 tiles PV0 QK0 PV1 QK1", 1);
-  run<128, 8, 512, 0, 1, 0, 1>("2 tiles PV0 PV1 QK0 QK1", 1);
+  run<128, 10, 512, 0, 1, 0, 1>("split-key block, 0 waits", 1);
+  run<128, 12, 512, 0, 1, 0, 1>("split-key block, 2 waits", 1);
+  run<128, 14, 512, 0, 1, 0, 1>("split-key block, 4 waits", 1);
+  run<128, 10, 512, 0, 1, 0, 1>("split-key block, 0 waits", 1);
   return 0;
 }
