@@ -1,4 +1,6 @@
-"""CTA-0 timeline of the split-key carve kernel (TCB_CARVE_V6=1, TCB_CARVE_DEBUG bit 3)."""
+"""CTA-0 timeline of the split-key carve kernel -- needs the experiment build (csrc/carve.cu of
+commit b881966 plus the trace stamps described in profiles/r01_carve_structure_variants.log),
+run with TCB_CARVE_V6=1 TCB_CARVE_DEBUG=8 (or 10 without the softmax)."""
 import ctypes as C, os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
