@@ -1,3 +1,6 @@
+"""CTA-0 timeline of the shipped carve kernel -- needs a build with the trace stamps described in
+profiles/r01_carve_structure_variants.log (g_trace + tcb_debug_trace_read); run with
+TCB_CARVE_DEBUG=8."""
 import ctypes as C, os, sys
 import numpy as np, torch
 sys.path.insert(0, os.getcwd())
