@@ -370,7 +370,7 @@ def run_gpu(args):
                      "hbm_peak_gbs": hbm},
         "e2e": e2e,
         "cpu_baseline": cpu,
-        "gpu_launches": 4 * args.steps,
+        "gpu_launches": 4 * args.steps * (min(args.a2a_chunks, Hl) if chunked else 1),
         "clocks": clk.result,
     }
     print(json.dumps(line))
