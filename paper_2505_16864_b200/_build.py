@@ -23,7 +23,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
     "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"),
-]
+] + os.environ.get("TCB_NVCC_EXTRA", "").split()  # e.g. -DTCB_CARVE_TRACE for timeline builds
 
 
 def nvcc() -> str:
@@ -38,9 +38,17 @@ def _deps_mtime() -> float:
     return max(os.path.getmtime(f) for f in files)
 
 
-def _compile(src: str, verbose: bool) -> str:
+def _flags_changed() -> bool:
+    stamp = os.path.join(OBJ_DIR, "flags.txt")
+    cur = " ".join(NVCC_FLAGS)
+    old = open(stamp).read() if os.path.exists(stamp) else None
+    return old != cur
+
+
+def _compile(src: str, verbose: bool, force: bool = False) -> str:
     obj = os.path.join(OBJ_DIR, os.path.basename(src).replace(".cu", ".o"))
-    if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), _deps_mtime()):
+    if (not force and os.path.exists(obj)
+            and os.path.getmtime(obj) >= max(os.path.getmtime(src), _deps_mtime())):
         return obj
     cmd = [nvcc(), *NVCC_FLAGS, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -57,8 +65,13 @@ def _compile(src: str, verbose: bool) -> str:
 def build(verbose: bool = False) -> str:
     os.makedirs(OBJ_DIR, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    force = _flags_changed()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
+        objs = list(ex.map(lambda s: _compile(s, verbose, force), srcs))
+    with open(os.path.join(OBJ_DIR, "flags.txt"), "w") as fh:
+        fh.write(" ".join(NVCC_FLAGS))
+    if force and os.path.exists(LIB):
+        os.remove(LIB)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcuda" if False else "-lcudart_static"]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -456,6 +456,23 @@ struct KvList {
   }
 };
 
+// Timeline stamps for tools/carve_trace1.py: compiled only into trace builds
+// (TCB_NVCC_EXTRA=-DTCB_CARVE_TRACE python -m paper_2505_16864_b200._build), enabled at run
+// time by TCB_CARVE_DEBUG bit 3; CTA 0 writes clock64() per (event, half-step).
+#ifdef TCB_CARVE_TRACE
+constexpr int TRACE_EV = 24, TRACE_STEPS = 8192;
+__device__ unsigned long long g_trace[TRACE_EV][TRACE_STEPS];
+#define TRACE(ev, step)                                                                 \
+  do {                                                                                  \
+    if ((dbg & 8) && blockIdx.x == 0 && (step) < (uint32_t)TRACE_STEPS)                 \
+      g_trace[(ev)][(step)] = clock64();                                                \
+  } while (0)
+#else
+#define TRACE(ev, step) \
+  do {                  \
+  } while (0)
+#endif
+
 template <int D, int EMU, typename E = __nv_bfloat16>
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     k_carve_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -572,7 +589,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     uint32_t it = 0, gk = 0, gv = 0, gs = 0, gp = 0;
     auto issue_s = [&]() {  // S(gs) = Q K(gs)^T into buffer gs & 1
       const int sl = gk % K_SLOTS;
+      if (lane == 0) TRACE(7, gs);
       ptx::mbar_wait(&bars->k_full[sl], (gk / K_SLOTS) & 1);
+      if (lane == 0) TRACE(8, gs);
       ptx::tc_fence_after();
       const uint32_t kbase = aK + sl * L::HALF_BYTES;
       if (ptx::elect_one()) {
@@ -587,6 +606,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         ptx::mma_commit(&bars->s_full[gs & 1]);
       }
       __syncwarp();
+      if (lane == 0) TRACE(9, gs);
       ++gk;
       ++gs;
     };
@@ -621,7 +641,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
           }
         }
         // ---- O += P(t) V(t): A = P from TMEM (32 packed columns), K = 64 keys
+        if (lane == 0) TRACE(1, gp);
         ptx::mbar_wait(&bars->p_full[gp & 1], (gp >> 1) & 1);
+        if (lane == 0) TRACE(3, gp);
         const int vs = gv % V_SLOTS;
         ptx::mbar_wait(&bars->v_full[vs], (gv / V_SLOTS) & 1);
         ptx::tc_fence_after();
@@ -638,6 +660,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
           ptx::mma_commit(&bars->o_done);
         }
         __syncwarp();
+        if (lane == 0) TRACE(5, gp);
         ++gv;
         ++gp;
       }
@@ -673,7 +696,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
           bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
         }
         const int hvalid = kvalid - (t & 1) * HN;  // valid keys in this half (may be <= 0)
+        if (lane == 0 && (warp & 3) == 2) TRACE(14, g);
         ptx::mbar_wait(&bars->s_full[g & 1], (g >> 1) & 1);
+        if (lane == 0 && (warp & 3) == 2) TRACE(10, g);
         ptx::tc_fence_after();
         if (dbg & 2) {  // timing experiment: no softmax work
           l_run = 1.f;
@@ -748,6 +773,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&bars->p_full[g & 1]);
+        if (lane == 0 && (warp & 3) == 2) TRACE(12, g);
       }
       // ---- epilogue: O / l -> bf16 row, padding rows zero (attention.py:203-206)
       ptx::mbar_wait(&bars->o_full, it & 1);
@@ -782,6 +808,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
   }
 }
 
+#undef TRACE
 }  // namespace tc
 
 
@@ -1009,3 +1036,16 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
   }
   return launch_tc<64, 0>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
 }
+
+#ifdef TCB_CARVE_TRACE
+// Trace builds only (not part of include/tokencarve_b200.h): copy out and clear CTA 0's
+// timeline, TRACE_EV x TRACE_STEPS clocks (0 = not reached).
+extern "C" int tcb_debug_trace_read(unsigned long long* host, int cap) {
+  const int n = tcb::tc::TRACE_EV * tcb::tc::TRACE_STEPS;
+  if (cap < n) return -1;
+  cudaMemcpyFromSymbol(host, tcb::tc::g_trace, sizeof(unsigned long long) * n);
+  static unsigned long long zero[tcb::tc::TRACE_EV * tcb::tc::TRACE_STEPS];
+  cudaMemcpyToSymbol(tcb::tc::g_trace, zero, sizeof(zero));
+  return n;
+}
+#endif

@@ -1,6 +1,9 @@
-"""CTA-0 timeline of the shipped carve kernel -- needs a build with the trace stamps described in
-profiles/r01_carve_structure_variants.log (g_trace + tcb_debug_trace_read); run with
-TCB_CARVE_DEBUG=8."""
+"""CTA-0 timeline of the shipped carve kernel.  Needs a trace build:
+
+    TCB_NVCC_EXTRA=-DTCB_CARVE_TRACE python -m paper_2505_16864_b200._build
+    TCB_CARVE_DEBUG=8 python tools/carve_trace1.py     # 10 = also skip the softmax
+
+(rebuild without TCB_NVCC_EXTRA afterwards; the stamps cost ~3 % when compiled in)."""
 import ctypes as C, os, sys
 import numpy as np, torch
 sys.path.insert(0, os.getcwd())
