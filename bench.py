@@ -6,9 +6,11 @@ K3 block pool (Q,K) -> K4 pooled relevance -> K5 select/union -> K7/K8 carve.
 With --gpus N>1 (torchrun) the layer is head-parallel: all-to-all (seq -> head
 shard), the local layer on H/N heads, all-to-all back; value = max over ranks.
 
-Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle port of
-the reference (the reference is pure numpy; oracle/port.py restates it) on a
-bounded sample and prints the same metric.
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference itself
+(tokencarve 0.1.0, pure numpy, installed unmodified into baseline/_ref) on the
+box's host cores -- its build_block_mask over all heads plus its carve body on
+consecutive slices of the layer's (head, q-block) jobs -- and prints the same
+metric (the oracle port stands in only when baseline/_ref is absent).
 """
 
 from __future__ import annotations
@@ -379,89 +381,166 @@ def run_gpu(args):
 
 
 # ------------------------------------------------------------------------------ CPU arm
-def cpu_sample(budget_s: float):
-    """Time the oracle port of the reference on a bounded C2 sample and extrapolate to
-    one full layer (ms).  Sample: build_block_mask on 1 head + carve of as many head-0
-    q-blocks as fit the budget (cond rows excluded), per-pair cost scaled to all pairs."""
-    import oracle
-
-    from threadpoolctl import threadpool_limits
-
-    threads = len(os.sched_getaffinity(0))
-    with threadpool_limits(limits=1, user_api="blas"):  # workers x 1 BLAS thread (SURVEY §8d)
-        return _cpu_sample(budget_s, threads)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
-def _cpu_sample(budget_s, threads):
-    import oracle
+def reference_module():
+    """The unmodified reference package installed into baseline/_ref (pip --target, see
+    DESIGN.md §7), or None when it is absent (then the oracle port stands in)."""
+    if not os.path.isdir(os.path.join(REF_DIR, "tokencarve")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import tokencarve
 
-    L = oracle.layout_scalars(DIMS, M, N_COND)
-    rng = np.random.default_rng(0)
-    shape = (1, L["padded_total"], D)
-    q, k, v = (rng.standard_normal(shape, dtype=np.float32) for _ in range(3))
-    inv = oracle.curve_inverse(oracle.curve_forward(DIMS))
-    adja = oracle.adjacency(DIMS, inv, M, L["M_v"])
-    t0 = time.perf_counter()
-    bits, _ = oracle.block_mask(q, k, L, adja, K_RATE, P_CUT)
-    t_mask = time.perf_counter() - t0
-    order = np.random.default_rng(1).permutation(L["M_v"])
-    # pick the faster of serial / threaded workers on a calibration chunk (the reference's
-    # ThreadPoolExecutor path, attention.py:233-242, only helps on some hosts)
-    best_w, best_rate = 1, None
-    pos = 0
-    for w in sorted({1, threads}):
-        sel = [(0, int(b)) for b in order[pos:pos + max(24, 3 * w)]]
-        pos += len(sel)
+    if not os.path.abspath(tokencarve.__file__).startswith(REF_DIR):
+        return None
+    return tokencarve
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class CpuLayer:
+    """The C2 layer on the host: the reference's own build_block_mask over all 24 heads
+    (timed once) and its per-(head, q-block) carve body, timed on consecutive slices of the
+    reference's job list (attention.py:236-239), so successive steps cover whole heads.
+
+    Q/K/V are the same bf16-representable values the GPU arm computes on (default_rng(0)
+    normals rounded to bf16, held as fp32 -- the reference's only precision)."""
+
+    def __init__(self):
+        from threadpoolctl import threadpool_limits
+
+        self.tc = reference_module()
+        self.kind = "reference" if self.tc is not None else "port"
+        self.threads = len(os.sched_getaffinity(0))
+        self._limits = threadpool_limits(limits=1, user_api="blas")  # workers x 1 BLAS thread
+        rng = np.random.default_rng(0)
+        import torch
+
+        Np = math.ceil(DIMS[0] * DIMS[1] * DIMS[2] / M) * M + math.ceil(N_COND / M) * M
+        shape = (H, Np, D)
+        self.q, self.k, self.v = (
+            torch.from_numpy(rng.standard_normal(shape, dtype=np.float32)).to(torch.bfloat16)
+            .to(torch.float32).numpy() for _ in range(3))
         t0 = time.perf_counter()
-        oracle.carve(q, k, v, bits, L, 0.0, workers=w, items=sel)
-        rate = (time.perf_counter() - t0) / sum(int(bits[0, b].sum()) for _, b in sel)
-        if best_rate is None or rate < best_rate:
-            best_w, best_rate = w, rate
-    items, pairs, t_carve = 0, 0, 0.0
-    chunk = max(best_w * 4, 16)
-    while t_carve < budget_s and pos + items < L["M_v"]:
-        sel = [(0, int(b)) for b in order[pos + items:pos + items + chunk]]
-        t0 = time.perf_counter()
-        oracle.carve(q, k, v, bits, L, 0.0, workers=best_w, items=sel)
-        t_carve += time.perf_counter() - t0
-        pairs += int(sum(bits[0, b].sum() for _, b in sel))
-        items += len(sel)
-    kept_per_head = int(bits[0].sum()) + L["M_c"] * L["M_total"]
-    total_pairs = kept_per_head * H  # head 0's kept count stands in for every head
-    ms = (t_carve / pairs * total_pairs + t_mask * H) * 1e3
-    sample = (f"oracle port (numpy, {best_w} worker threads x 1 BLAS thread, {threads} cores): "
-              f"build_block_mask on 1 of "
-              f"{H} heads ({t_mask:.2f} s) + carve of {items} head-0 q-blocks / {pairs} kv pairs "
-              f"({t_carve:.2f} s), extrapolated to {total_pairs} pairs and {H} heads")
-    return ms, best_w, sample
+        if self.tc is not None:
+            tc = self.tc
+            dims = tc.GridDims(*DIMS)
+            self.layout = tc.build_layout(dims, M, N_COND)
+            statics = tc.StaticMasks.build(self.layout, dims, tc.build_curve(dims))
+            t0 = time.perf_counter()
+            mask, _ = tc.build_block_mask(self.q, self.k, self.layout, statics,
+                                          tc.SelectionParams(k=K_RATE, p=P_CUT))
+            self.t_mask = time.perf_counter() - t0
+            self.bits = mask.bits
+            self.inputs = tc.AttentionInputs(q=self.q, k=self.k, v=self.v, layout=self.layout)
+            from tokencarve.attention import _carve_rows
+
+            self._rows = _carve_rows
+            M_v, M_total = self.layout.M_v, self.layout.M_total
+        else:
+            import oracle
+
+            self.L = oracle.layout_scalars(DIMS, M, N_COND)
+            adja = oracle.adjacency(DIMS, oracle.curve_inverse(oracle.curve_forward(DIMS)), M,
+                                    self.L["M_v"])
+            t0 = time.perf_counter()
+            self.bits, _ = oracle.block_mask(self.q, self.k, self.L, adja, K_RATE, P_CUT)
+            self.t_mask = time.perf_counter() - t0
+            M_v, M_total = self.L["M_v"], self.L["M_total"]
+        self.out = np.zeros_like(self.q)
+        row = self.bits.sum(axis=-1)
+        self.jobs = [(h, b) for h in range(H) for b in range(M_total)]  # attention.py:236
+        self.job_pairs = [int(row[h, b]) if b < M_v else M_total for h, b in self.jobs]
+        self.total_pairs = int(sum(self.job_pairs))
+        self.pos = 0
+        self.covered = 0  # jobs timed so far (consecutive from job 0)
+
+    def _run(self, jobs):
+        from concurrent.futures import ThreadPoolExecutor
+
+        if self.tc is not None:
+            f = lambda hb: self._rows(self.inputs, self.bits, 0.0, *hb, self.out)  # noqa: E731
+            with ThreadPoolExecutor(max_workers=self.threads) as pool:  # attention.py:237-239
+                list(pool.map(f, jobs))
+        else:
+            import oracle
+
+            oracle.carve(self.q, self.k, self.v, self.bits, self.L, 0.0, workers=self.threads,
+                         items=jobs)
+
+    def step(self, budget_s: float) -> float:
+        """Carve the next jobs for about budget_s; returns the extrapolated ms per layer
+        (measured s/pair x all kept pairs + the 24-head mask build)."""
+        t, pairs = 0.0, 0
+        chunk = 4 * self.threads
+        while t < budget_s:
+            if self.pos >= len(self.jobs):
+                self.pos = 0
+            sel = self.jobs[self.pos:self.pos + chunk]
+            t0 = time.perf_counter()
+            self._run(sel)
+            t += time.perf_counter() - t0
+            pairs += sum(self.job_pairs[self.pos:self.pos + len(sel)])
+            self.pos += len(sel)
+            self.covered = max(self.covered, self.pos)
+        return (t / pairs * self.total_pairs + self.t_mask) * 1e3
+
+    def describe(self) -> str:
+        heads = min(H, self.covered // (len(self.jobs) // H))
+        what = ("reference tokencarve 0.1.0 from baseline/_ref (unmodified; build_block_mask + "
+                "attention._carve_rows, the body carve_attention maps over its ThreadPoolExecutor)"
+                if self.tc is not None else "oracle port of the reference (baseline/_ref absent)")
+        return (f"{what}, fp32, {self.threads} worker threads x 1 BLAS thread on {self.threads} "
+                f"cores ({cpu_model()}): build_block_mask over all {H} heads once "
+                f"({self.t_mask:.2f} s, added to every step) + carve of consecutive "
+                f"(head, q-block) jobs, {self.covered} jobs timed = {heads} whole heads; "
+                f"per-step value = measured s per kept pair x {self.total_pairs} kept pairs "
+                f"(extrapolation factor {self.total_pairs / max(1, self._covered_pairs()):.2f}) "
+                f"+ the mask build")
+
+    def _covered_pairs(self) -> int:
+        return sum(self.job_pairs[: self.covered])
 
 
 def cpu_baseline(budget_s):
-    ms, cores, sample = cpu_sample(budget_s)
-    return {"value": round(ms, 1), "unit": "ms", "cores": cores, "kind": "port", "sample": sample}
+    cl = CpuLayer()
+    ms = cl.step(budget_s)
+    return {"value": round(ms, 1), "unit": "ms", "cores": cl.threads, "kind": cl.kind,
+            "sample": cl.describe()}
 
 
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    budget = max(1.0, args.cpu_seconds / max(1, args.steps + args.warmup))
-    if args.cpu_seconds == 20.0:  # default: keep the whole reference run within minutes
-        budget = max(1.0, 120.0 / max(1, args.steps + args.warmup))
+    cl = CpuLayer()
+    # keep the whole run within a few minutes: ~200 s of carving over all steps
+    budget = max(2.0, 200.0 / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
-        cpu_sample(budget)
-    vals, samples = [], None
-    for _ in range(args.steps):
-        ms, cores, samples = cpu_sample(budget)
-        vals.append(ms)
+        cl.step(budget)
+    vals = [cl.step(budget) for _ in range(args.steps)]
     v = float(np.mean(vals))
     line = {"metric": METRIC, "value": round(v, 1), "unit": "ms", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 1),
-            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (numpy default_rng(0) Q/K/V, fp32)", "impl": "reference",
-            "config": {"workload": WORKLOAD, "k": K_RATE, "p": P_CUT},
-            "cpu_baseline": {"value": round(v, 1), "unit": "ms", "cores": cores, "kind": "port",
-                             "sample": samples},
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 (the reference's only precision; Q/K/V are the bf16-rounded values)",
+            "data": "synthetic (numpy default_rng(0) normals rounded to bf16, held as fp32)",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "tokens": len(cl.q[0]), "heads": H, "d": D,
+                       "block": M, "k": K_RATE, "p": P_CUT, "kept_pairs": cl.total_pairs},
+            "cpu_baseline": {"value": round(v, 1), "unit": "ms", "cores": cl.threads,
+                             "kind": cl.kind, "sample": cl.describe()},
             "e2e": {"value": round(v, 1), "unit": "ms", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))

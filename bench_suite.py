@@ -131,7 +131,7 @@ def hbm_records():
     n = dims.n_cells
     x = torch.randn((n, 3072), device="cuda").to(torch.bfloat16)
     y = torch.empty_like(x)
-    t = timed(lambda: tcb.gather_rows(x, perm.forward, out=y), reps=20)
+    t = timed(lambda: tcb.gather_rows(x, perm.forward_dev, out=y), reps=20)
     byts = 2 * x.numel() * 2 + 4 * n
     out.append({"kernel": "permute_rows (K2)", "shape": "118800 x 3072 bf16", "ms": round(t, 4),
                 "gbs": round(byts / (t * 1e-3) / 1e9, 1), "frac_of_hbm": round(byts / (t * 1e-3) / 1e9 / hbm, 3)})
@@ -186,7 +186,7 @@ def c4_records():
         lay = tcb.build_layout(dst, 128, 256)
         tcb.StaticMasks.build(lay, dst, perm)
         z = tcb.switch_stage(x, vel, 0.899083, dst, 1234)
-        tcb.gather_rows(z.reshape(-1, C), perm.forward)
+        tcb.gather_rows(z.reshape(-1, C), perm.forward_dev)
 
     t = timed(switch, reps=10)
     recs.append({"kernel": "full stage switch (switch + curve + statics + permute)", "ms": round(t, 4),
@@ -221,7 +221,7 @@ def fused_records():
     offs = [0, dims.t * 8, dims.t * 8 + dims.h * 28]
     cs = torch.cat([tab[offs[a] + pos[:, a:a + 1] * (sec[a] // 2) +
                         torch.arange(sec[a] // 2, device="cuda")] for a in range(3)], dim=1)  # (n, 64, 2)
-    fidx = perm.forward.long()
+    fidx = perm.forward_dev.long()
 
     def unfused():
         res = []

@@ -35,6 +35,7 @@ extern "C" {
 #define TCB_F32 0
 #define TCB_BF16 1
 #define TCB_F16 2
+#define TCB_F64 3 /* tcb_block_pool and the stage point ops only (reference float64 callers) */
 
 const char* tcb_last_error(void);
 int tcb_abi_version(void);
@@ -133,9 +134,20 @@ int tcb_upsample_renoise(const float* x, const float* vel, const float* eps, flo
                          int sh, int sw, int dt, int dh, int dw, int C, double sigma, int mode,
                          uint64_t seed, uint64_t offset, void* stream);
 
-/* Euler step x + (sigma_next - sigma) * v (pipeline.py:131-137), float32. */
+/* float64 source latent (a numpy float64 caller of upsample_area_3d / stage_transition):
+ * mode 0 writes float64 U(x) (pipeline.py:173 keeps x.dtype), modes 1/2 write float32
+ * (1-sigma)*float32(U(x)) + sigma*eps (pipeline.py:190-192).  No velocity term. */
+int tcb_upsample_renoise_f64(const double* x, const float* eps, void* out, int st, int sh, int sw,
+                             int dt, int dh, int dw, int C, double sigma, int mode, uint64_t seed,
+                             uint64_t offset, void* stream);
+
+/* Euler step x + (sigma_next - sigma) * v (pipeline.py:131-137), float32; predict_clean
+ * (pipeline.py:124-128) is the same op with dsigma = -sigma. */
 int tcb_euler_step(const float* x, const float* v, float* out, int64_t n, float dsigma,
                    void* stream);
+/* The same in float64 (numpy float64 callers). */
+int tcb_euler_step_f64(const double* x, const double* v, double* out, int64_t n, double dsigma,
+                       void* stream);
 
 /* ---- fused neighbours of the path ---- */
 

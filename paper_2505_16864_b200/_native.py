@@ -15,7 +15,7 @@ from .errors import ContractError, DomainError, ShapeError, SizeError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libtcb200.so")
 
-F32, BF16, F16 = 0, 1, 2
+F32, BF16, F16, F64 = 0, 1, 2, 3
 
 _P = C.c_void_p
 _I = C.c_int
@@ -44,6 +44,8 @@ SIGNATURES = {
                            _I64, _F, _P],
     "tcb_upsample_renoise": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _I, _U64, _U64, _P],
     "tcb_euler_step": [_P, _P, _P, _I64, _F, _P],
+    "tcb_euler_step_f64": [_P, _P, _P, _I64, _D, _P],
+    "tcb_upsample_renoise_f64": [_P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _I, _U64, _U64, _P],
     "tcb_upsample_renoise_curve": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _I, _U64,
                                    _U64, _P],
     "tcb_curve_positions": [_P, _I64, _I, _I, _I, _P, _P],

@@ -92,21 +92,28 @@ def _workspace(dev: torch.device) -> torch.Tensor:
 def carve_raw(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: BlockMask,
               layout: BlockLayout, beta: float = 0.0, out: torch.Tensor | None = None,
               simt: bool = False) -> torch.Tensor:
-    """Device-tensor entry: q/k/v (H, N_pad, d) sharing strides, innermost contiguous."""
+    """Device-tensor entry: q/k/v (H, N_pad, d) of one dtype on one device, innermost axis
+    contiguous (any head / token strides; all three are made contiguous if they differ)."""
+    if not (q.dtype == k.dtype == v.dtype):
+        raise ShapeError(f"q/k/v dtypes differ: {q.dtype}, {k.dtype}, {v.dtype}")
+    if not (q.shape == k.shape == v.shape) or q.ndim != 3:
+        raise ShapeError(f"q/k/v must share one (heads, N, d_k) shape")
+    _dev.same_device(q, k, v, mask.kv_idx, *(() if out is None else (out,)))
     H, N, d = q.shape
     if k.stride() != q.stride() or v.stride() != q.stride() or q.stride(2) != 1:
         q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-    if out is None:
-        out = torch.empty_like(q)
-    if out.stride() != q.stride():
-        raise ShapeError("output must share the input strides")
-    args = (q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), _dev.code_of(q.dtype),
-            q.stride(0), q.stride(1), mask.kv_idx.data_ptr(), mask.kv_cnt.data_ptr(), H, d, layout.m,
-            layout.M_v, layout.M_total, layout.n_valid, layout.n_cond, float(beta))
-    if simt:
-        _native.call("tcb_carve_fwd_simt", *args, _dev.stream())
-    else:
-        _native.call("tcb_carve_fwd", *args, _workspace(q.device).data_ptr(), _dev.stream())
+    with _dev.on(q):
+        if out is None:
+            out = torch.empty_like(q)
+        if out.stride() != q.stride() or out.dtype != q.dtype or out.shape != q.shape:
+            raise ShapeError("output must share the inputs' shape, dtype and strides")
+        args = (q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), _dev.code_of(q.dtype),
+                q.stride(0), q.stride(1), mask.kv_idx.data_ptr(), mask.kv_cnt.data_ptr(), H, d,
+                layout.m, layout.M_v, layout.M_total, layout.n_valid, layout.n_cond, float(beta))
+        if simt:
+            _native.call("tcb_carve_fwd_simt", *args, _dev.stream())
+        else:
+            _native.call("tcb_carve_fwd", *args, _workspace(q.device).data_ptr(), _dev.stream())
     return out
 
 
@@ -124,7 +131,10 @@ def carve_attention(inputs: AttentionInputs, mask: BlockMask,
     if layout.M_v:
         mask.check_nonempty()
     q, k, v = (_dev.as_cuda(x) for x in (inputs.q, inputs.k, inputs.v))
-    if q.dtype not in (torch.float32, torch.bfloat16, torch.float16):
+    _dev.same_device(q, k, v)
+    if not (q.dtype == k.dtype == v.dtype) or q.dtype not in (torch.float32, torch.bfloat16,
+                                                               torch.float16):
+        # mixed or other dtypes compute in float32, as the reference's astype(float32)
         q, k, v = q.float(), k.float(), v.float()
     out = carve_raw(q, k, v, mask, layout, beta.beta)
     return _dev.to_like(out, inputs.q)
@@ -177,11 +187,12 @@ def block_mask_logit_bias(mask: BlockMask, layout: BlockLayout, beta: float = 0.
     (attention.py:145-159): -inf on deselected vision-row blocks, condition rows open,
     +beta on vision-query x condition-key pairs.  Built on the device."""
     m, n = layout.m, layout.padded_total
-    bits = mask.bits if isinstance(mask, BlockMask) else _dev.as_cuda(mask)
+    bits = mask.bits_dev if isinstance(mask, BlockMask) else _dev.as_cuda(mask)
     H = int(bits.shape[0])
     bias = torch.zeros((H, layout.M_total, layout.M_total), dtype=torch.float32, device=bits.device)
     bias[:, : layout.M_v, :] = torch.where(bits.to(torch.bool), 0.0, float("-inf"))
     if beta:
         bias[:, : layout.M_v, layout.M_v:] += np.float32(beta)
     out = bias.repeat_interleave(m, dim=1).repeat_interleave(m, dim=2).reshape(H, n, n)
-    return out.cpu().numpy() if isinstance(mask, np.ndarray) else out
+    host = mask.host if isinstance(mask, BlockMask) else isinstance(mask, np.ndarray)
+    return out.cpu().numpy() if host else out

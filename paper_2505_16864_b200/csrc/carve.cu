@@ -18,6 +18,7 @@
 //                    not take; mirrors the reference's per-block streaming order (1e-5).
 //  * k_carve_simt -- fp32 math, one warp per query row, any (m, d): the fallback.
 #include <atomic>
+#include <mutex>
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -573,8 +574,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         }
         ++cnt;
       };
-      // same order the MMA warp consumes: K0, K1, V0, K2, V1, ..., V(T-1)
-      load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, 0);
+      // same order the MMA warp consumes: K0, K1, V0, K2, V1, ..., V(T-1); an empty row
+      // (T == 0, only reachable through a hand-built mask) loads nothing, like the MMA warp
+      if (T > 0) load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, 0);
       for (int t = 0; t < T; ++t) {
         if (t + 1 < T) load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, t + 1);
         load(&tm_v, sV, bars->v_full, bars->v_empty, V_SLOTS, gv, t);
@@ -779,7 +781,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       ptx::mbar_wait(&bars->o_full, it & 1);
       ptx::tc_fence_after();
       const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
-      const float inv_l = (row < qvalid) ? 1.f / l_run : 0.f;
+      const float inv_l = (row < qvalid && T > 0) ? 1.f / l_run : 0.f;
       E* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
@@ -851,12 +853,20 @@ static int make_tmap(CUtensorMap* tm, const void* base, int d, int64_t n_pad, in
   return TCB_OK;
 }
 
-// Kernel attributes are per device: remember, thread-safely, which devices already have them.
-static bool first_on_device(std::atomic<uint64_t>& seen) {
+// Kernel attributes are per device: set one once per device under a lock, and remember the
+// device only after cudaFuncSetAttribute succeeded (a failure is retried on the next launch).
+template <typename F>
+static cudaError_t once_per_device(std::atomic<uint64_t>& seen, F&& set_attr) {
   int dev = 0;
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
-  return !(seen.fetch_or(bit) & bit);
+  if (seen.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (seen.load(std::memory_order_relaxed) & bit) return cudaSuccess;
+  const cudaError_t e = set_attr();
+  if (e == cudaSuccess) seen.fetch_or(bit, std::memory_order_release);
+  return e;
 }
 
 static int validate(const void* q, const void* k, const void* v, void* o, int dtype,
@@ -884,9 +894,11 @@ static int launch_f32t(const void* q, const void* k, const void* v, void* o, con
   size_t smem = ((size_t)2 * M * (D + 4) + (size_t)D * (M + 4)) * sizeof(float);
   if (M + 4 > D + 4) smem += (size_t)M * (M + 4) * sizeof(float);
   static std::atomic<uint64_t> attr{0};
-  if (first_on_device(attr)) {
-    cudaError_t e = cudaFuncSetAttribute(k_carve_f32t<T, MT, DT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    const cudaError_t e = once_per_device(attr, [&] {
+      return cudaFuncSetAttribute(k_carve_f32t<T, MT, DT>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "f32t smem: %s", cudaGetErrorString(e));
   }
   const float scale = (float)(1.0 / sqrt((double)s.d));
@@ -967,9 +979,11 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
   if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::HN, !tc::Elem<E>::kBf16))) return rc;
   const int smem = tc::Smem<D>::BYTES;
   static std::atomic<uint64_t> attr{0};
-  if (first_on_device(attr)) {
-    cudaError_t e = cudaFuncSetAttribute(tc::k_carve_tc<D, EMU, E>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    const cudaError_t e = once_per_device(attr, [&] {
+      return cudaFuncSetAttribute(tc::k_carve_tc<D, EMU, E>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    });
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
   }
   cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);

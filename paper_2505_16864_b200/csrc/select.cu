@@ -33,6 +33,14 @@ struct Vec16<float> {
   }
 };
 template <>
+struct Vec16<double> {
+  static constexpr int VE = 2;
+  __device__ static void load(const double* p, double* o) {
+    double2 v = __ldcs(reinterpret_cast<const double2*>(p));
+    o[0] = v.x; o[1] = v.y;
+  }
+};
+template <>
 struct Vec16<__nv_bfloat16> {
   static constexpr int VE = 8;
   __device__ static void load(const __nv_bfloat16* p, double* o) {
@@ -61,6 +69,11 @@ struct Vec16<__half> {
     }
   }
 };
+
+template <typename T>
+__device__ __forceinline__ double to_f64(T x) { return (double)(float)x; }
+template <>
+__device__ __forceinline__ double to_f64<double>(double x) { return x; }
 
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(128) k_pool(const T* __restrict__ x0, const T* __restrict__ x1,
@@ -97,7 +110,7 @@ __global__ void __launch_bounds__(128) k_pool(const T* __restrict__ x0, const T*
         if constexpr (VEC) {
           Vec16<T>::load(p + (int64_t)(r + u) * sn, v[u]);
         } else {
-          v[u][0] = (double)(float)p[(int64_t)(r + u) * sn];
+          v[u][0] = to_f64(p[(int64_t)(r + u) * sn]);
         }
       }
 #pragma unroll
@@ -110,7 +123,7 @@ __global__ void __launch_bounds__(128) k_pool(const T* __restrict__ x0, const T*
       if constexpr (VEC) {
         Vec16<T>::load(p + (int64_t)r * sn, v);
       } else {
-        v[0] = (double)(float)p[(int64_t)r * sn];
+        v[0] = to_f64(p[(int64_t)r * sn]);
       }
 #pragma unroll
       for (int e = 0; e < VE; ++e) acc[e] += v[e];
@@ -1151,6 +1164,18 @@ static int launch_scores(const double* pq, int pq_blocks, const double* pk, int 
   return check_launch("k_scores_dmma");
 }
 
+template <typename T>
+static void launch_pool(bool vec, dim3 grid, cudaStream_t s, const void* x0, const void* x1,
+                        int64_t sh, int64_t sn, int H, int d, int m, int M_v, int M_total,
+                        int64_t n_valid, int64_t n_cond, double* o0, double* o1, int G, int chunks) {
+  if (vec)
+    k_pool<T, true><<<grid, 128, 0, s>>>((const T*)x0, (const T*)x1, sh, sn, H, d, m, M_v, M_total,
+                                         n_valid, n_cond, o0, o1, G, chunks);
+  else
+    k_pool<T, false><<<grid, 128, 0, s>>>((const T*)x0, (const T*)x1, sh, sn, H, d, m, M_v,
+                                          M_total, n_valid, n_cond, o0, o1, G, chunks);
+}
+
 extern "C" int tcb_block_pool(const void* x0, const void* x1, int dtype, int64_t stride_h,
                               int64_t stride_n, int H, int d, int m, int M_v, int M_total,
                               int64_t n_valid, int64_t n_cond, double* out0, double* out1,
@@ -1159,10 +1184,10 @@ extern "C" int tcb_block_pool(const void* x0, const void* x1, int dtype, int64_t
   TCB_CHECK_ARG((x1 == nullptr) == (out1 == nullptr), TCB_ESHAPE, "x1/out1 must both be set");
   TCB_CHECK_ARG(H >= 1 && d >= 1 && m >= 1 && M_total >= M_v && M_v >= 0, TCB_ESHAPE,
                 "bad pool shape");
-  TCB_CHECK_ARG(dtype == TCB_F32 || dtype == TCB_BF16 || dtype == TCB_F16, TCB_EDOMAIN,
-                "unsupported dtype %d", dtype);
+  TCB_CHECK_ARG(dtype == TCB_F32 || dtype == TCB_BF16 || dtype == TCB_F16 || dtype == TCB_F64,
+                TCB_EDOMAIN, "unsupported dtype %d", dtype);
   if ((int64_t)H * M_total == 0) return TCB_OK;
-  const int esz = dtype == TCB_F32 ? 4 : 2;
+  const int esz = dtype == TCB_F64 ? 8 : dtype == TCB_F32 ? 4 : 2;
   const int VE = 16 / esz;
   const bool vec = (d % VE == 0) && (stride_n % VE == 0) && (stride_h % VE == 0) &&
                    ((uintptr_t)x0 % 16 == 0) && ((uintptr_t)x1 % 16 == 0);
@@ -1173,36 +1198,18 @@ extern "C" int tcb_block_pool(const void* x0, const void* x1, int dtype, int64_t
   const int64_t items = (int64_t)H * M_total;
   dim3 grid((unsigned)ceil_div(items, per_cta), x1 ? 2 : 1);
   cudaStream_t s = as_stream(stream);
-  if (dtype == TCB_F32) {
-    if (vec)
-      k_pool<float, true><<<grid, 128, 0, s>>>((const float*)x0, (const float*)x1, stride_h,
-                                               stride_n, H, d, m, M_v, M_total, n_valid, n_cond,
-                                               out0, out1, G, chunks);
-    else
-      k_pool<float, false><<<grid, 128, 0, s>>>((const float*)x0, (const float*)x1, stride_h,
-                                                stride_n, H, d, m, M_v, M_total, n_valid, n_cond,
-                                                out0, out1, G, chunks);
-  } else if (dtype == TCB_BF16) {
-    using B = __nv_bfloat16;
-    if (vec)
-      k_pool<B, true><<<grid, 128, 0, s>>>((const B*)x0, (const B*)x1, stride_h, stride_n, H, d,
-                                           m, M_v, M_total, n_valid, n_cond, out0, out1, G,
-                                           chunks);
-    else
-      k_pool<B, false><<<grid, 128, 0, s>>>((const B*)x0, (const B*)x1, stride_h, stride_n, H, d,
-                                            m, M_v, M_total, n_valid, n_cond, out0, out1, G,
-                                            chunks);
-  } else {
-    using B = __half;
-    if (vec)
-      k_pool<B, true><<<grid, 128, 0, s>>>((const B*)x0, (const B*)x1, stride_h, stride_n, H, d,
-                                           m, M_v, M_total, n_valid, n_cond, out0, out1, G,
-                                           chunks);
-    else
-      k_pool<B, false><<<grid, 128, 0, s>>>((const B*)x0, (const B*)x1, stride_h, stride_n, H, d,
-                                            m, M_v, M_total, n_valid, n_cond, out0, out1, G,
-                                            chunks);
-  }
+  if (dtype == TCB_F32)
+    launch_pool<float>(vec, grid, s, x0, x1, stride_h, stride_n, H, d, m, M_v, M_total, n_valid,
+                       n_cond, out0, out1, G, chunks);
+  else if (dtype == TCB_BF16)
+    launch_pool<__nv_bfloat16>(vec, grid, s, x0, x1, stride_h, stride_n, H, d, m, M_v, M_total,
+                               n_valid, n_cond, out0, out1, G, chunks);
+  else if (dtype == TCB_F16)
+    launch_pool<__half>(vec, grid, s, x0, x1, stride_h, stride_n, H, d, m, M_v, M_total, n_valid,
+                        n_cond, out0, out1, G, chunks);
+  else
+    launch_pool<double>(vec, grid, s, x0, x1, stride_h, stride_n, H, d, m, M_v, M_total, n_valid,
+                        n_cond, out0, out1, G, chunks);
   return check_launch("k_pool");
 }
 

@@ -65,74 +65,167 @@ __device__ __forceinline__ float philox_normal(uint64_t seed, uint64_t idx) {
   return (idx & 1) ? r * sinf(6.283185307179586f * u2) : r * cosf(6.283185307179586f * u2);
 }
 
+// Output cell -> source taps, computed once per (cell, 4-channel group) thread and reused
+// for every channel of the group.  VEC = channels per thread (4: float4 / 2x double2 loads and
+// stores along C; 1: any C).  Index math is int32 (the host guarantees n_cells * C < 2^31).
+template <typename TI, typename TO, int VEC>
 __global__ void __launch_bounds__(256) k_upsample_renoise(
-    const float* __restrict__ x, const float* __restrict__ vel, const int32_t* __restrict__ inv,
-    const float* __restrict__ eps, float* __restrict__ out, int st, int sh, int sw, int dt, int dh,
+    const TI* __restrict__ x, const float* __restrict__ vel, const int32_t* __restrict__ inv,
+    const float* __restrict__ eps, TO* __restrict__ out, int st, int sh, int sw, int dt, int dh,
     int dw, int C, float sigma_f, int mode, uint64_t seed, uint64_t offset) {
-  const int64_t n = (int64_t)dt * dh * dw * C;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int groups = C / VEC;
+  const int n = dt * dh * dw * groups;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
-  const int c = (int)(e % C);
-  int64_t cell = e / C;
-  const int ow = (int)(cell % dw);
-  cell /= dw;
-  const int oh = (int)(cell % dh);
-  const int ot = (int)(cell / dh);
+  const int cell = e / groups;
+  const int c0 = (e - cell * groups) * VEC;
+  const int ow = cell % dw;
+  const int rest = cell / dw;
+  const int oh = rest % dh;
+  const int ot = rest / dh;
   const Taps tt = axis_taps(ot, st, dt), th = axis_taps(oh, sh, dh), tw = axis_taps(ow, sw, dw);
+  // Always two taps per axis: a missing second tap repeats the first index with weight 0,
+  // and 0 * x adds an exact zero -- as the reference's dense tensordot rows do.
+  const int ti[2] = {tt.i0, tt.n > 1 ? tt.i0 + 1 : tt.i0};
+  const int hi[2] = {th.i0, th.n > 1 ? th.i0 + 1 : th.i0};
+  const int wi[2] = {tw.i0, tw.n > 1 ? tw.i0 + 1 : tw.i0};
+  const double tw_[2] = {tt.w0, tt.w1}, hw_[2] = {th.w0, th.w1}, ww_[2] = {tw.w0, tw.w1};
   // same axis order as the reference's separable tensordots: t, then h, then w
-  double acc_w = 0.0;
-  for (int b = 0; b < tw.n; ++b) {
-    double acc_h = 0.0;
-    for (int a = 0; a < th.n; ++a) {
-      double acc_t = 0.0;
-      for (int z = 0; z < tt.n; ++z) {
-        const int64_t cell = ((int64_t)(tt.i0 + z) * sh + (th.i0 + a)) * sw + (tw.i0 + b);
-        const int64_t src = cell * C + c;
-        float x0 = x[src];
-        if (vel) {  // predict_clean in fp32; a curve-order velocity is read through inv
-          const float v = vel[(inv ? (int64_t)inv[cell] : cell) * C + c];
-          x0 = __fsub_rn(x0, __fmul_rn(sigma_f, v));
+  double acc_w[VEC];
+#pragma unroll
+  for (int u = 0; u < VEC; ++u) acc_w[u] = 0.0;
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    double acc_h[VEC];
+#pragma unroll
+    for (int u = 0; u < VEC; ++u) acc_h[u] = 0.0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      double acc_t[VEC];
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) acc_t[u] = 0.0;
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        const int scell = (ti[z] * sh + hi[a]) * sw + wi[b];
+        double x0[VEC];
+        const TI* xp = x + (int64_t)scell * C + c0;
+        if constexpr (VEC == 4 && sizeof(TI) == 4) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(xp));
+          x0[0] = f.x; x0[1] = f.y; x0[2] = f.z; x0[3] = f.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < VEC; ++u) x0[u] = (double)__ldg(xp + u);
         }
-        acc_t += (z == 0 ? tt.w0 : tt.w1) * (double)x0;
+        if (vel) {  // predict_clean in fp32; a curve-order velocity is read through inv
+          const float* vp = vel + (int64_t)(inv ? inv[scell] : scell) * C + c0;
+#pragma unroll
+          for (int u = 0; u < VEC; ++u)
+            x0[u] = (double)__fsub_rn((float)x0[u], __fmul_rn(sigma_f, __ldg(vp + u)));
+        }
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) acc_t[u] = fma(tw_[z], x0[u], acc_t[u]);
       }
-      acc_h += (a == 0 ? th.w0 : th.w1) * acc_t;
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) acc_h[u] = fma(hw_[a], acc_t[u], acc_h[u]);
     }
-    acc_w += (b == 0 ? tw.w0 : tw.w1) * acc_h;
+#pragma unroll
+    for (int u = 0; u < VEC; ++u) acc_w[u] = fma(ww_[b], acc_h[u], acc_w[u]);
   }
-  const float up = (float)acc_w;
+  const int64_t o = (int64_t)cell * C + c0;
+  TO r[VEC];
   if (mode == 0) {
-    out[e] = up;
-    return;
+#pragma unroll
+    for (int u = 0; u < VEC; ++u) r[u] = (TO)acc_w[u];
+  } else {
+    float nz[VEC];
+    if (mode == 1) {
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) nz[u] = __ldcs(eps + o + u);
+    } else {
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) nz[u] = philox_normal(seed, offset + (uint64_t)(o + u));
+    }
+    // (1 - s) * up + s * noise on the float32-cast upsample, each op rounded like numpy's
+    // float32 arrays (pipeline.py:190-192)
+#pragma unroll
+    for (int u = 0; u < VEC; ++u)
+      r[u] = (TO)__fadd_rn(__fmul_rn(__fsub_rn(1.0f, sigma_f), (float)acc_w[u]),
+                           __fmul_rn(sigma_f, nz[u]));
   }
-  const float nz = (mode == 1) ? eps[e] : philox_normal(seed, offset + (uint64_t)e);
-  // (1 - s) * up + s * noise, each op rounded like numpy's float32 arrays
-  out[e] = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, sigma_f), up), __fmul_rn(sigma_f, nz));
+  if constexpr (VEC == 4 && sizeof(TO) == 4) {
+    __stcs(reinterpret_cast<float4*>(out + o), make_float4(r[0], r[1], r[2], r[3]));
+  } else {
+#pragma unroll
+    for (int u = 0; u < VEC; ++u) out[o + u] = r[u];
+  }
 }
 
-__global__ void k_euler(const float* __restrict__ x, const float* __restrict__ v,
-                        float* __restrict__ out, int64_t n, float ds) {
+template <typename T>
+__global__ void k_euler(const T* __restrict__ x, const T* __restrict__ v, T* __restrict__ out,
+                        int64_t n, T ds) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < n) out[e] = __fadd_rn(x[e], __fmul_rn(ds, v[e]));
+  if (e < n) {
+    if constexpr (sizeof(T) == 4)
+      out[e] = __fadd_rn(x[e], __fmul_rn(ds, v[e]));
+    else
+      out[e] = __dadd_rn(x[e], __dmul_rn(ds, v[e]));
+  }
+}
+
+template <typename TI, typename TO>
+static int launch_switch(const TI* x, const float* vel, const int32_t* inv, const float* eps, TO* out,
+                         int st, int sh, int sw, int dt, int dh, int dw, int C, double sigma,
+                         int mode, uint64_t seed, uint64_t offset, cudaStream_t stream) {
+  TCB_CHECK_ARG((int64_t)dt * dh * dw * C < ((int64_t)1 << 31) &&
+                    (int64_t)st * sh * sw * C < ((int64_t)1 << 31),
+                TCB_ESIZE, "latent too large");
+  const bool vec = (C % 4 == 0) && ((uintptr_t)x % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
+                   (!eps || (uintptr_t)eps % 16 == 0) && (!vel || (uintptr_t)vel % 16 == 0);
+  const int64_t n = (int64_t)dt * dh * dw * (vec ? C / 4 : C);
+  const unsigned grid = (unsigned)ceil_div(n, 256);
+  if (vec)
+    k_upsample_renoise<TI, TO, 4><<<grid, 256, 0, stream>>>(x, vel, inv, eps, out, st, sh, sw, dt, dh,
+                                                           dw, C, (float)sigma, mode, seed, offset);
+  else
+    k_upsample_renoise<TI, TO, 1><<<grid, 256, 0, stream>>>(x, vel, inv, eps, out, st, sh, sw, dt, dh,
+                                                           dw, C, (float)sigma, mode, seed, offset);
+  return check_launch("k_upsample_renoise");
 }
 
 }  // namespace tcb
 
 using namespace tcb;
 
+#define TCB_SWITCH_CHECKS()                                                                 \
+  TCB_CHECK_ARG(st >= 1 && sh >= 1 && sw >= 1 && C >= 1, TCB_ESHAPE, "bad source dims");    \
+  TCB_CHECK_ARG(dt >= st && dh >= sh && dw >= sw, TCB_EDOMAIN, "target shrinks source");    \
+  TCB_CHECK_ARG(mode >= 0 && mode <= 2, TCB_EDOMAIN, "bad mode %d", mode);                  \
+  TCB_CHECK_ARG(mode != 1 || eps, TCB_ESHAPE, "mode 1 needs eps");                          \
+  TCB_CHECK_ARG(sigma >= 0.0 && sigma <= 1.0, TCB_EDOMAIN, "sigma %g outside [0, 1]", sigma)
+
 extern "C" int tcb_upsample_renoise(const float* x, const float* vel, const float* eps, float* out,
                                     int st, int sh, int sw, int dt, int dh, int dw, int C,
                                     double sigma, int mode, uint64_t seed, uint64_t offset,
                                     void* stream) {
   TCB_CHECK_ARG(x && out, TCB_ESHAPE, "null tensor");
-  TCB_CHECK_ARG(st >= 1 && sh >= 1 && sw >= 1 && C >= 1, TCB_ESHAPE, "bad source dims");
-  TCB_CHECK_ARG(dt >= st && dh >= sh && dw >= sw, TCB_EDOMAIN, "target shrinks source");
-  TCB_CHECK_ARG(mode >= 0 && mode <= 2, TCB_EDOMAIN, "bad mode %d", mode);
-  TCB_CHECK_ARG(mode != 1 || eps, TCB_ESHAPE, "mode 1 needs eps");
-  TCB_CHECK_ARG(sigma >= 0.0 && sigma <= 1.0, TCB_EDOMAIN, "sigma %g outside [0, 1]", sigma);
-  const int64_t n = (int64_t)dt * dh * dw * C;
-  k_upsample_renoise<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(
-      x, vel, nullptr, eps, out, st, sh, sw, dt, dh, dw, C, (float)sigma, mode, seed, offset);
-  return check_launch("k_upsample_renoise");
+  TCB_SWITCH_CHECKS();
+  return launch_switch<float, float>(x, vel, nullptr, eps, out, st, sh, sw, dt, dh, dw, C, sigma,
+                                     mode, seed, offset, as_stream(stream));
+}
+
+extern "C" int tcb_upsample_renoise_f64(const double* x, const float* eps, void* out, int st,
+                                        int sh, int sw, int dt, int dh, int dw, int C,
+                                        double sigma, int mode, uint64_t seed, uint64_t offset,
+                                        void* stream) {
+  TCB_CHECK_ARG(x && out, TCB_ESHAPE, "null tensor");
+  TCB_SWITCH_CHECKS();
+  cudaStream_t s = as_stream(stream);
+  if (mode == 0)  // upsample_area_3d keeps the float64 dtype (pipeline.py:173)
+    return launch_switch<double, double>(x, nullptr, nullptr, nullptr, (double*)out, st, sh, sw, dt,
+                                         dh, dw, C, 0.0, 0, seed, offset, s);
+  // stage_transition casts the float64 upsample to float32 before mixing (pipeline.py:190)
+  return launch_switch<double, float>(x, nullptr, nullptr, eps, (float*)out, st, sh, sw, dt, dh, dw,
+                                      C, sigma, mode, seed, offset, s);
 }
 
 extern "C" int tcb_upsample_renoise_curve(const float* x, const float* vel_curve,
@@ -141,21 +234,23 @@ extern "C" int tcb_upsample_renoise_curve(const float* x, const float* vel_curve
                                           double sigma, int mode, uint64_t seed, uint64_t offset,
                                           void* stream) {
   TCB_CHECK_ARG(x && out && vel_curve && inv, TCB_ESHAPE, "null tensor");
-  TCB_CHECK_ARG(st >= 1 && sh >= 1 && sw >= 1 && C >= 1, TCB_ESHAPE, "bad source dims");
-  TCB_CHECK_ARG(dt >= st && dh >= sh && dw >= sw, TCB_EDOMAIN, "target shrinks source");
-  TCB_CHECK_ARG(mode >= 0 && mode <= 2, TCB_EDOMAIN, "bad mode %d", mode);
-  TCB_CHECK_ARG(mode != 1 || eps, TCB_ESHAPE, "mode 1 needs eps");
-  TCB_CHECK_ARG(sigma >= 0.0 && sigma <= 1.0, TCB_EDOMAIN, "sigma %g outside [0, 1]", sigma);
-  const int64_t n = (int64_t)dt * dh * dw * C;
-  k_upsample_renoise<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(
-      x, vel_curve, inv, eps, out, st, sh, sw, dt, dh, dw, C, (float)sigma, mode, seed, offset);
-  return check_launch("k_upsample_renoise");
+  TCB_SWITCH_CHECKS();
+  return launch_switch<float, float>(x, vel_curve, inv, eps, out, st, sh, sw, dt, dh, dw, C, sigma,
+                                     mode, seed, offset, as_stream(stream));
 }
 
 extern "C" int tcb_euler_step(const float* x, const float* v, float* out, int64_t n, float dsigma,
                               void* stream) {
   TCB_CHECK_ARG(x && v && out, TCB_ESHAPE, "null tensor");
   if (n == 0) return TCB_OK;
-  k_euler<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(x, v, out, n, dsigma);
+  k_euler<float><<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(x, v, out, n, dsigma);
+  return check_launch("k_euler");
+}
+
+extern "C" int tcb_euler_step_f64(const double* x, const double* v, double* out, int64_t n,
+                                  double dsigma, void* stream) {
+  TCB_CHECK_ARG(x && v && out, TCB_ESHAPE, "null tensor");
+  if (n == 0) return TCB_OK;
+  k_euler<double><<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(x, v, out, n, dsigma);
   return check_launch("k_euler");
 }

@@ -49,8 +49,8 @@ def curve_positions(perm: Permutation) -> torch.Tensor:
     """(n, 3) int64 (t, h, w) of each curve position (pipeline.py:334-337)."""
     d = perm.dims
     n = d.n_cells
-    pos = torch.empty((n, 3), dtype=torch.int64, device=perm.forward.device)
-    _native.call("tcb_curve_positions", perm.forward.data_ptr(), n, d.t, d.h, d.w, pos.data_ptr(),
+    pos = torch.empty((n, 3), dtype=torch.int64, device=perm.forward_dev.device)
+    _native.call("tcb_curve_positions", perm.forward_dev.data_ptr(), n, d.t, d.h, d.w, pos.data_ptr(),
                  _dev.stream())
     return pos
 
@@ -71,7 +71,7 @@ def patchify_permute(x, perm: Permutation, patch=(1, 1, 1)) -> torch.Tensor:
     dims = perm.dims
     pt, ph, pw, C = _patch_dims(xt, dims, patch)
     tok = torch.empty((dims.n_cells, pt * ph * pw * C), dtype=torch.float32, device=xt.device)
-    _native.call("tcb_patchify_permute", xt.data_ptr(), perm.forward.data_ptr(), dims.t, dims.h,
+    _native.call("tcb_patchify_permute", xt.data_ptr(), perm.forward_dev.data_ptr(), dims.t, dims.h,
                  dims.w, pt, ph, pw, C, tok.data_ptr(), _dev.stream())
     return _dev.to_like(tok, x)
 
@@ -89,7 +89,7 @@ def unpermute_euler(x, vel_curve, perm: Permutation, sigma_t: float, sigma_next:
     if tuple(vt.shape) != (dims.n_cells, pt * ph * pw * C):
         raise ShapeError(f"velocity shape {tuple(vt.shape)} != {(dims.n_cells, pt * ph * pw * C)}")
     out = torch.empty_like(xt)
-    _native.call("tcb_unpermute_euler", xt.data_ptr(), vt.data_ptr(), perm.inverse.data_ptr(),
+    _native.call("tcb_unpermute_euler", xt.data_ptr(), vt.data_ptr(), perm.inverse_dev.data_ptr(),
                  dims.t, dims.h, dims.w, pt, ph, pw, C, float(np.float32(sigma_next - sigma_t)),
                  out.data_ptr(), _dev.stream())
     return _dev.to_like(out, x)
@@ -108,13 +108,13 @@ def switch_stage_curve(x, vel_curve, perm: Permutation, sigma_t: float, target: 
     if sigma_t in (0.0, 1.0):
         from .sfc import gather_rows
 
-        vel = gather_rows(vt, perm.inverse).reshape(xt.shape)
+        vel = gather_rows(vt, perm.inverse_dev).reshape(xt.shape)
         x0 = predict_clean(xt, vel, sigma_t)
         if sigma_t == 0.0:
             return _dev.to_like(upsample_area_3d(x0, target), x)
         return _dev.to_like(eps if eps is not None else stage_transition(x0, 1.0, target, seed), x)
     out = torch.empty((*dst, C), dtype=torch.float32, device=xt.device)
-    _native.call("tcb_upsample_renoise_curve", xt.data_ptr(), vt.data_ptr(), perm.inverse.data_ptr(),
+    _native.call("tcb_upsample_renoise_curve", xt.data_ptr(), vt.data_ptr(), perm.inverse_dev.data_ptr(),
                  _native.ptr(eps), out.data_ptr(), *src, *dst, C, float(sigma_t), mode, seed, 0,
                  _dev.stream())
     return _dev.to_like(out, x)
@@ -175,7 +175,7 @@ def rope_permute(srcs, perm: Permutation, dsts, rotate, sections=(16, 56, 56),
     rot_arr = (C.c_int * len(rotate))(*[1 if r else 0 for r in rotate])
     _native.call("tcb_rope_permute", C.cast(src_arr, C.c_void_p), s0.stride(0), s0.stride(1),
                  C.cast(dst_arr, C.c_void_p), d0.stride(0), d0.stride(1),
-                 C.cast(rot_arr, C.c_void_p), len(srcs), perm.forward.data_ptr(), dims.t, dims.h,
+                 C.cast(rot_arr, C.c_void_p), len(srcs), perm.forward_dev.data_ptr(), dims.t, dims.h,
                  dims.w, H, d, _native.ptr(tab), *(sections if any(rotate) else (0, 0, 0)),
                  _dev.stream())
 

@@ -28,9 +28,10 @@ __all__ = ["PooledBlocks", "SelectionParams", "BlockMask", "block_pool", "releva
 
 @dataclass(frozen=True)
 class PooledBlocks:
-    """Per-head block means (H, blocks, d) float64 (masks.py:31-50)."""
+    """Per-head block means (H, blocks, d) float64 (masks.py:31-50).  ``values`` is a
+    device tensor, or numpy when the caller pooled numpy input (as the reference)."""
 
-    values: torch.Tensor
+    values: object
     valid_counts: np.ndarray
 
     def __post_init__(self):
@@ -76,21 +77,30 @@ class BlockMask:
     """Selection mask (H, M_v, M_total) (masks.py:78-95).
 
     Device form: packed ``words`` (H, M_v, ceil(M_total/32)) and the ascending CSR
-    ``kv_idx`` (H, M_v, M_total capacity) / ``kv_cnt`` (H, M_v).  ``BlockMask(bits=)``
-    accepts a dense bool array/tensor like the reference and packs it on the device;
-    ``.bits`` materialises the dense bool tensor lazily.
+    ``kv_idx`` (H, M_v, M_total capacity) / ``kv_cnt`` (H, M_v).  ``BlockMask(bits)``
+    accepts a dense bool array/tensor like the reference and packs it on the device.
+    ``.bits`` is the dense bool mask: a read-only numpy array when the mask came from
+    numpy (a numpy ``bits`` argument, or ``build_block_mask`` on numpy Q/K), as the
+    reference returns (masks.py:87); otherwise the device tensor (``bits_dev``).
     """
 
     def __init__(self, bits=None, *, words=None, kv_idx=None, kv_cnt=None, M_total=None,
-                 nonempty: bool = False):
+                 nonempty: bool = False, host: bool | None = None):
+        self._np = None
         if bits is not None:
             if bits.ndim != 3 or (bits.dtype not in (np.bool_, torch.bool)):
                 raise ShapeError(f"mask bits must be a rank-3 boolean array, got {tuple(bits.shape)}")
+            if isinstance(bits, np.ndarray):
+                bits.setflags(write=False)  # the reference freezes the caller's array
+                self._np = bits
             dense = _dev.as_cuda(bits)
             M_total = int(dense.shape[-1])
-            words, kv_idx, kv_cnt = pack_rows(dense, M_total)
+            with _dev.on(dense):
+                words, kv_idx, kv_cnt = pack_rows(dense, M_total)
             self._dense = dense
             nonempty = False
+            if host is None:
+                host = isinstance(bits, np.ndarray)
         else:
             if words is None or kv_idx is None or kv_cnt is None or M_total is None:
                 raise ShapeError("BlockMask needs bits= or the packed (words, kv_idx, kv_cnt)")
@@ -100,16 +110,28 @@ class BlockMask:
         self.kv_cnt = kv_cnt
         self.M_total = int(M_total)
         self._nonempty = nonempty
+        self.host = bool(host)
 
     @property
     def shape(self) -> tuple:
         return (*self.kv_cnt.shape, self.M_total)
 
     @property
-    def bits(self) -> torch.Tensor:
+    def bits_dev(self) -> torch.Tensor:
+        """Dense bool (H, M_v, M_total) on the device (unpacked lazily)."""
         if self._dense is None:
             self._dense = unpack_rows(self.words, self.M_total)
         return self._dense
+
+    @property
+    def bits(self):
+        if not self.host:
+            return self.bits_dev
+        if self._np is None:
+            a = self.bits_dev.cpu().numpy()
+            a.setflags(write=False)
+            self._np = a
+        return self._np
 
     @property
     def n_heads(self) -> int:
@@ -144,19 +166,38 @@ def _pool_one_or_two(x0: torch.Tensor, x1: torch.Tensor | None, layout: BlockLay
     H, _, d = x0.shape
     if x0.stride(2) != 1:
         raise ShapeError("innermost (d_k) axis must be contiguous")
-    outs = [torch.empty((H, layout.M_total, d), dtype=torch.float64, device=x0.device)
-            for _ in range(1 if x1 is None else 2)]
-    _native.call("tcb_block_pool", x0.data_ptr(), _native.ptr(x1), _dev.code_of(x0.dtype),
-                 x0.stride(0), x0.stride(1), H, d, layout.m, layout.M_v, layout.M_total,
-                 layout.n_valid, layout.n_cond, outs[0].data_ptr(),
-                 outs[1].data_ptr() if x1 is not None else None, _dev.stream())
+    if x1 is not None:
+        _dev.same_device(x0, x1)
+    with _dev.on(x0):
+        outs = [torch.empty((H, layout.M_total, d), dtype=torch.float64, device=x0.device)
+                for _ in range(1 if x1 is None else 2)]
+        _native.call("tcb_block_pool", x0.data_ptr(), _native.ptr(x1),
+                     _dev.code_of(x0.dtype, allow_f64=True), x0.stride(0), x0.stride(1), H, d,
+                     layout.m, layout.M_v, layout.M_total, layout.n_valid, layout.n_cond,
+                     outs[0].data_ptr(), outs[1].data_ptr() if x1 is not None else None,
+                     _dev.stream())
     counts = layout.block_valid_counts.copy()
     return [PooledBlocks(values=o, valid_counts=counts) for o in outs]
 
 
+def _poolable(x) -> torch.Tensor:
+    """Device view of a pool input: 16/32/64-bit floats are read as they are; anything else
+    (integer arrays) is promoted to float64 first, which is exact below 2^53."""
+    t = _dev.as_cuda(x)
+    if t.dtype not in (torch.float32, torch.bfloat16, torch.float16, torch.float64):
+        t = t.to(torch.float64)
+    return t
+
+
 def block_pool(x, layout: BlockLayout) -> PooledBlocks:
-    """Mean over valid tokens per block, float64 (masks.py:98-116)."""
-    return _pool_one_or_two(_dev.as_cuda(x), None, layout)[0]
+    """Mean over valid tokens per block, float64 (masks.py:98-116).  numpy input (any float
+    width, float64 included) gives numpy values, like the reference."""
+    if x.ndim != 3:
+        raise ShapeError(f"expected (heads, tokens, d_k), got shape {tuple(x.shape)}")
+    pooled = _pool_one_or_two(_poolable(x), None, layout)[0]
+    if _dev.is_numpy(x):
+        return PooledBlocks(values=pooled.values.cpu().numpy(), valid_counts=pooled.valid_counts)
+    return pooled
 
 
 def relevance(pooled_q: PooledBlocks, pooled_k: PooledBlocks, d_k: int) -> torch.Tensor:
@@ -165,25 +206,28 @@ def relevance(pooled_q: PooledBlocks, pooled_k: PooledBlocks, d_k: int) -> torch
         raise ShapeError("pooled Q and K disagree on head count")
     if pooled_q.values.shape[2] != d_k or pooled_k.values.shape[2] != d_k:
         raise ShapeError("pooled Q/K feature size must equal d_k")
-    pq = pooled_q.values.contiguous()
-    pk = pooled_k.values.contiguous()
+    pq = _dev.as_cuda(pooled_q.values, torch.float64).contiguous()
+    pk = _dev.as_cuda(pooled_k.values, torch.float64).contiguous()
+    _dev.same_device(pq, pk)
     H, rows, _ = pq.shape
-    R = torch.empty((H, rows, pk.shape[1]), dtype=torch.float64, device=pq.device)
-    _native.call("tcb_block_relevance", pq.data_ptr(), rows, pk.data_ptr(), H, rows, pk.shape[1],
-                 d_k, R.data_ptr(), _dev.stream())
-    return R
+    with _dev.on(pq):
+        R = torch.empty((H, rows, pk.shape[1]), dtype=torch.float64, device=pq.device)
+        _native.call("tcb_block_relevance", pq.data_ptr(), rows, pk.data_ptr(), H, rows,
+                     pk.shape[1], d_k, R.data_ptr(), _dev.stream())
+    return _dev.to_like(R, pooled_q.values)
 
 
 def _select(R: torch.Tensor, params: SelectionParams, M_v: int, adja_bits, with_union: bool):
     H, rows, n_cols = R.shape
     words = mask_words(n_cols)
     dev = R.device
-    bits = torch.empty((H, rows, words), dtype=torch.int32, device=dev)
-    kv_idx = torch.empty((H, rows, n_cols), dtype=torch.int32, device=dev)
-    kv_cnt = torch.empty((H, rows), dtype=torch.int32, device=dev)
-    _native.call("tcb_block_select", R.data_ptr(), H, rows, n_cols, _native.ptr(adja_bits), words,
-                 params.n_floor(M_v), float(params.p), 1 if with_union else 0, bits.data_ptr(),
-                 kv_idx.data_ptr(), kv_cnt.data_ptr(), _dev.stream())
+    with _dev.on(R):
+        bits = torch.empty((H, rows, words), dtype=torch.int32, device=dev)
+        kv_idx = torch.empty((H, rows, n_cols), dtype=torch.int32, device=dev)
+        kv_cnt = torch.empty((H, rows), dtype=torch.int32, device=dev)
+        _native.call("tcb_block_select", R.data_ptr(), H, rows, n_cols, _native.ptr(adja_bits),
+                     words, params.n_floor(M_v), float(params.p), 1 if with_union else 0,
+                     bits.data_ptr(), kv_idx.data_ptr(), kv_cnt.data_ptr(), _dev.stream())
     return bits, kv_idx, kv_cnt
 
 
@@ -205,9 +249,10 @@ def union_mask(b_top, cond, adja, layout: BlockLayout) -> BlockMask:
         raise ShapeError(f"condition mask shape {tuple(cond.shape)} is inconsistent with the layout")
     if tuple(adja.shape) != (layout.M_v, layout.M_v):
         raise ShapeError(f"adjacency mask shape {tuple(adja.shape)} is inconsistent with the layout")
-    dense = _dev.as_cuda(b_top).clone() | _dev.as_cuda(cond)[None, : layout.M_v, :]
-    dense[:, :, : layout.M_v] |= _dev.as_cuda(adja)[None]
-    return BlockMask(bits=dense)
+    top = _dev.as_cuda(b_top)
+    dense = top.to(torch.bool) | _dev.as_cuda(cond).to(torch.bool)[None, : layout.M_v, :]
+    dense[:, :, : layout.M_v] |= _dev.as_cuda(adja).to(torch.bool)[None]
+    return BlockMask(bits=dense, host=_dev.is_numpy(b_top))
 
 
 def build_block_mask(q, k, layout: BlockLayout, statics: StaticMasks, params: SelectionParams):
@@ -215,7 +260,15 @@ def build_block_mask(q, k, layout: BlockLayout, statics: StaticMasks, params: Se
 
     Three launches: K3 pool (Q and K together), K4a float64 scores, and the fused
     row-softmax + selection + union kernel, which leaves R in the score buffer."""
-    qd, kd = _dev.as_cuda(q), _dev.as_cuda(k)
+    qd, kd = _poolable(q), _poolable(k)
+    if qd.dtype != kd.dtype:
+        qd, kd = qd.to(torch.float64), kd.to(torch.float64)
+    _dev.same_device(qd, kd)
+    with _dev.on(qd):
+        return _build_block_mask(qd, kd, layout, statics, params, host=_dev.is_numpy(q))
+
+
+def _build_block_mask(qd, kd, layout, statics, params, host):
     d_k = qd.shape[-1]
     H = qd.shape[0]
     pq, pk = _pool_one_or_two(qd, kd, layout)
@@ -231,8 +284,8 @@ def build_block_mask(q, k, layout: BlockLayout, statics: StaticMasks, params: Se
                  _native.ptr(adja), words, params.n_floor(layout.M_v), float(params.p), 1,
                  bits.data_ptr(), kv_idx.data_ptr(), kv_cnt.data_ptr(), _dev.stream())
     mask = BlockMask(words=bits, kv_idx=kv_idx, kv_cnt=kv_cnt, M_total=layout.M_total,
-                     nonempty=True)
-    return mask, _dev.to_like(R, q)
+                     nonempty=True, host=host)
+    return mask, (R.cpu().numpy() if host else R)
 
 
 def mask_stats(mask: BlockMask, R=None, p: float | None = None) -> dict:
@@ -241,7 +294,7 @@ def mask_stats(mask: BlockMask, R=None, p: float | None = None) -> dict:
              "selected_fraction": mask.selected_fraction}
     if R is not None and p is not None:
         Rd = _dev.as_cuda(R, torch.float64)
-        covered = (Rd * mask.bits[:, :, : Rd.shape[-1]]).sum(dim=-1) > p
+        covered = (Rd * mask.bits_dev[:, :, : Rd.shape[-1]]).sum(dim=-1) > p
         stats["rows_meeting_cutoff"] = int(covered.sum().item())
         stats["rows_total"] = int(covered.numel())
     return stats

@@ -95,15 +95,17 @@ def build_layout(dims: GridDims, m: int, n_cond_tokens: int = 0) -> BlockLayout:
 
 
 def adjacency_bits(layout: BlockLayout, dims: GridDims, perm: Permutation) -> torch.Tensor:
-    """Packed (M_v, words) uint32 adjacency, one K6 launch."""
+    """Packed (M_v, words) uint32 adjacency on the device, one K6 launch."""
     if perm.dims != dims:
         raise ShapeError("permutation was built for different dims")
     if layout.n_valid != dims.n_cells:
         raise ShapeError("layout was built for different dims")
     words = mask_words(layout.M_total)
-    out = torch.empty((layout.M_v, words), dtype=torch.int32, device=perm.inverse.device)
-    _native.call("tcb_adjacency_build", perm.inverse.data_ptr(), dims.t, dims.h, dims.w, layout.m,
-                 layout.M_v, words, out.data_ptr(), _dev.stream())
+    inv = perm.inverse_dev
+    with _dev.on(inv):
+        out = torch.empty((layout.M_v, words), dtype=torch.int32, device=inv.device)
+        _native.call("tcb_adjacency_build", inv.data_ptr(), dims.t, dims.h, dims.w, layout.m,
+                     layout.M_v, words, out.data_ptr(), _dev.stream())
     return out
 
 
@@ -111,44 +113,116 @@ def unpack_rows(bits: torch.Tensor, n_cols: int) -> torch.Tensor:
     """Packed uint32 rows -> dense bool (..., n_cols) on the device."""
     lead = bits.shape[:-1]
     rows = int(np.prod(lead)) if len(lead) else 1
-    out = torch.empty((*lead, n_cols), dtype=torch.uint8, device=bits.device)
-    _native.call("tcb_mask_unpack", bits.data_ptr(), rows, n_cols, bits.shape[-1], out.data_ptr(),
-                 _dev.stream())
+    with _dev.on(bits):
+        out = torch.empty((*lead, n_cols), dtype=torch.uint8, device=bits.device)
+        _native.call("tcb_mask_unpack", bits.data_ptr(), rows, n_cols, bits.shape[-1],
+                     out.data_ptr(), _dev.stream())
     return out.view(torch.bool)
 
 
-def adjacency_mask(layout: BlockLayout, dims: GridDims, perm: Permutation) -> torch.Tensor:
-    """Dense bool (M_v, M_v) adjacency on the device (partition.py:107-136)."""
-    return unpack_rows(adjacency_bits(layout, dims, perm), layout.M_total)[:, : layout.M_v]
+def _frozen(a: np.ndarray) -> np.ndarray:
+    a.setflags(write=False)
+    return a
 
 
-def condition_mask(layout: BlockLayout) -> torch.Tensor:
-    """``i >= M_v or j >= M_v`` (partition.py:139-143)."""
-    is_cond = torch.arange(layout.M_total, device=_dev.device()) >= layout.M_v
+def adjacency_mask(layout: BlockLayout, dims: GridDims, perm: Permutation) -> np.ndarray:
+    """Dense bool (M_v, M_v) adjacency (partition.py:107-136): built on the device by K6,
+    returned as numpy like the reference."""
+    dense = unpack_rows(adjacency_bits(layout, dims, perm), layout.M_total)[:, : layout.M_v]
+    return dense.cpu().numpy()
+
+
+def condition_mask(layout: BlockLayout) -> np.ndarray:
+    """``i >= M_v or j >= M_v`` (partition.py:139-143); a host array like the reference
+    (the device path never materialises it: the select kernel forces the columns)."""
+    is_cond = np.arange(layout.M_total) >= layout.M_v
     return is_cond[:, None] | is_cond[None, :]
 
 
-@dataclass(frozen=True)
 class StaticMasks:
-    """Per-stage masks (partition.py:146-159).  ``adja_bits`` is the packed form
-    the selection kernel consumes; ``cond``/``adja`` are dense views."""
+    """Per-stage masks (partition.py:146-159).
 
-    cond: torch.Tensor
-    adja: torch.Tensor
-    adja_bits: torch.Tensor | None = None
+    ``adja_bits`` is the packed (M_v, words) device bitset the selection kernel ORs in;
+    ``cond`` / ``adja`` are the reference's read-only dense bool numpy arrays
+    (partition.py:154-155), materialised from the device on first access;
+    ``cond_dev`` / ``adja_dev`` are the dense device views.
+    """
+
+    __slots__ = ("_cond", "_adja", "adja_bits", "_cache")
+
+    def __init__(self, cond=None, adja=None, adja_bits: torch.Tensor | None = None):
+        if adja is None and adja_bits is None:
+            raise ShapeError("StaticMasks needs adja (dense) or adja_bits (packed)")
+        object.__setattr__(self, "_cond", cond)
+        object.__setattr__(self, "_adja", adja)
+        object.__setattr__(self, "adja_bits", adja_bits)
+        object.__setattr__(self, "_cache", {})
+        for a in (cond, adja):
+            if isinstance(a, np.ndarray):
+                a.setflags(write=False)
+
+    def __setattr__(self, name, value):
+        raise AttributeError(f"StaticMasks is immutable (cannot set {name!r})")
+
+    def __repr__(self) -> str:
+        return f"StaticMasks(M_v={self.adja_dev.shape[0]})"
 
     @classmethod
     def build(cls, layout: BlockLayout, dims: GridDims, perm: Permutation) -> "StaticMasks":
         bits = adjacency_bits(layout, dims, perm)
-        adja = unpack_rows(bits, layout.M_total)[:, : layout.M_v]
-        return cls(cond=condition_mask(layout), adja=adja, adja_bits=bits)
+        sm = cls(cond=None, adja=None, adja_bits=bits)
+        sm._cache["M_total"] = layout.M_total
+        sm._cache["M_v"] = layout.M_v
+        return sm
+
+    def _get(self, key, make):
+        v = self._cache.get(key)
+        if v is None:
+            v = make()
+            self._cache[key] = v
+        return v
+
+    @property
+    def adja_dev(self) -> torch.Tensor:
+        if isinstance(self._adja, torch.Tensor):
+            return self._adja
+        if self._adja is not None:
+            return self._get("adja_dev", lambda: _dev.as_cuda(self._adja).to(torch.bool))
+        M_v, M_total = self._cache["M_v"], self._cache["M_total"]
+        return self._get("adja_dev", lambda: unpack_rows(self.adja_bits, M_total)[:, :M_v])
+
+    @property
+    def adja(self) -> np.ndarray:
+        if isinstance(self._adja, np.ndarray):
+            return self._adja
+        return self._get("adja_np", lambda: _frozen(self.adja_dev.cpu().numpy()))
+
+    @property
+    def cond(self) -> np.ndarray:
+        if isinstance(self._cond, np.ndarray):
+            return self._cond
+        if isinstance(self._cond, torch.Tensor):
+            return self._get("cond_np", lambda: _frozen(self._cond.cpu().numpy()))
+        M_v, M_total = self._cache["M_v"], self._cache["M_total"]
+        return self._get("cond_np", lambda: _frozen(condition_mask(
+            BlockLayout(m=1, n_valid=M_v, n_cond=M_total - M_v, M_v=M_v, M_c=M_total - M_v))))
+
+    @property
+    def cond_dev(self) -> torch.Tensor:
+        if isinstance(self._cond, torch.Tensor):
+            return self._cond
+        return self._get("cond_dev", lambda: _dev.as_cuda(self.cond))
 
     def packed(self, layout: BlockLayout) -> torch.Tensor:
+        """The (M_v, words) packed adjacency the selection kernel consumes."""
         if self.adja_bits is not None:
             return self.adja_bits
-        dense = torch.zeros((layout.M_v, layout.M_total), dtype=torch.uint8, device=_dev.device())
-        dense[:, : layout.M_v] = _dev.as_cuda(self.adja).to(torch.uint8)
-        return pack_rows(dense, layout.M_total)[0]
+
+        def make():
+            dense = torch.zeros((layout.M_v, layout.M_total), dtype=torch.uint8, device=_dev.device())
+            dense[:, : layout.M_v] = self.adja_dev.to(torch.uint8)
+            return pack_rows(dense, layout.M_total)[0]
+        return self._get(("packed", layout.M_total), make)
 
 
 def pack_rows(dense: torch.Tensor, n_cols: int):

@@ -154,6 +154,29 @@ def plan_to_dict(plan: StagePlan) -> dict:
 
 
 # ----------------------------------------------------------------------------- point ops
+def _pair(a, b):
+    """Device views of two same-shape latents in their common float dtype (float32, or
+    float64 when either is float64 -- numpy's promotion for the reference's expressions)."""
+    x, y = _dev.as_cuda(a), _dev.as_cuda(b)
+    dt = torch.float64 if torch.float64 in (x.dtype, y.dtype) else torch.float32
+    return x.to(dt).contiguous(), y.to(dt).contiguous()
+
+
+def _axpy(x: torch.Tensor, y: torch.Tensor, coef: float) -> torch.Tensor:
+    """``x + coef * y`` elementwise in x's dtype (coef rounded to it, like
+    np.asarray(coef, dtype=x.dtype)), one K9 Euler launch."""
+    _dev.same_device(x, y)
+    with _dev.on(x):
+        out = torch.empty_like(x)
+        if x.dtype == torch.float64:
+            _native.call("tcb_euler_step_f64", x.data_ptr(), y.data_ptr(), out.data_ptr(),
+                         x.numel(), float(coef), _dev.stream())
+        else:
+            _native.call("tcb_euler_step", x.data_ptr(), y.data_ptr(), out.data_ptr(), x.numel(),
+                         float(np.float32(coef)), _dev.stream())
+    return out
+
+
 def _f32(x) -> torch.Tensor:
     t = _dev.as_cuda(x)
     if t.dtype != torch.float32:
@@ -162,15 +185,12 @@ def _f32(x) -> torch.Tensor:
 
 
 def predict_clean(x_t, eps_t, sigma_t: float):
-    """``x - sigma * eps`` in float32 (pipeline.py:124-128)."""
+    """``x - sigma * eps`` (pipeline.py:124-128), float32 or float64 like the input."""
     if tuple(x_t.shape) != tuple(eps_t.shape):
         raise ShapeError(f"latent and prediction shapes differ: {tuple(x_t.shape)} vs {tuple(eps_t.shape)}")
-    x, e = _f32(x_t), _f32(eps_t)
-    out = torch.empty_like(x)
+    x, e = _pair(x_t, eps_t)
     # x + (-sigma) * e == x - sigma * e bitwise in IEEE arithmetic
-    _native.call("tcb_euler_step", x.data_ptr(), e.data_ptr(), out.data_ptr(), x.numel(),
-                 -float(np.float32(sigma_t)), _dev.stream())
-    return _dev.to_like(out, x_t)
+    return _dev.to_like(_axpy(x, e, -sigma_t), x_t)
 
 
 def denoise_step(x_t, v_t, sigma_t: float, sigma_next: float):
@@ -179,11 +199,8 @@ def denoise_step(x_t, v_t, sigma_t: float, sigma_next: float):
         raise ShapeError(f"latent and velocity shapes differ: {tuple(x_t.shape)} vs {tuple(v_t.shape)}")
     if not sigma_next < sigma_t:
         raise DomainError(f"sigmas must decrease: {sigma_t} -> {sigma_next}")
-    x, v = _f32(x_t), _f32(v_t)
-    out = torch.empty_like(x)
-    _native.call("tcb_euler_step", x.data_ptr(), v.data_ptr(), out.data_ptr(), x.numel(),
-                 float(np.float32(sigma_next - sigma_t)), _dev.stream())
-    return _dev.to_like(out, x_t)
+    x, v = _pair(x_t, v_t)
+    return _dev.to_like(_axpy(x, v, sigma_next - sigma_t), x_t)
 
 
 def _check_up(x, target: GridDims):
@@ -195,22 +212,38 @@ def _check_up(x, target: GridDims):
     return src, dst
 
 
+def _latent(x) -> torch.Tensor:
+    """Device latent in float32, or float64 kept as is (the reference upsamples in float64)."""
+    t = _dev.as_cuda(x)
+    if t.dtype not in (torch.float32, torch.float64):
+        t = t.to(torch.float32)
+    return t.contiguous()
+
+
 def _launch_switch(x: torch.Tensor, vel, eps, sigma: float, dst, mode: int, seed: int = 0,
                    offset: int = 0) -> torch.Tensor:
     C = x.shape[-1]
-    out = torch.empty((*dst, C), dtype=torch.float32, device=x.device)
-    _native.call("tcb_upsample_renoise", x.data_ptr(), _native.ptr(vel), _native.ptr(eps),
-                 out.data_ptr(), *x.shape[:3], *dst, C, float(sigma), mode, seed, offset,
-                 _dev.stream())
+    with _dev.on(x):
+        if x.dtype == torch.float64:
+            odt = torch.float64 if mode == 0 else torch.float32
+            out = torch.empty((*dst, C), dtype=odt, device=x.device)
+            _native.call("tcb_upsample_renoise_f64", x.data_ptr(), _native.ptr(eps), out.data_ptr(),
+                         *x.shape[:3], *dst, C, float(sigma), mode, seed, offset, _dev.stream())
+            return out
+        out = torch.empty((*dst, C), dtype=torch.float32, device=x.device)
+        _native.call("tcb_upsample_renoise", x.data_ptr(), _native.ptr(vel), _native.ptr(eps),
+                     out.data_ptr(), *x.shape[:3], *dst, C, float(sigma), mode, seed, offset,
+                     _dev.stream())
     return out
 
 
 def upsample_area_3d(x, target: GridDims):
-    """Area upsample of a (t, h, w, c) latent (pipeline.py:153-173)."""
+    """Area upsample of a (t, h, w, c) latent (pipeline.py:153-173); float64 input stays
+    float64, like the reference's ``astype(x.dtype)``."""
     src, dst = _check_up(x, target)
-    xt = _f32(x)
+    xt = _latent(x)
     if src == dst:
-        return _dev.to_like(xt.clone(), x)
+        return x.copy() if _dev.is_numpy(x) else xt.clone()
     return _dev.to_like(_launch_switch(xt, None, None, 0.0, dst, 0), x)
 
 
@@ -234,7 +267,7 @@ def stage_transition(x0, sigma_t: float, target: GridDims, rng):
     src, dst = _check_up(x0, target)
     C = int(x0.shape[-1])
     mode, eps, seed = _noise_source(rng, (*dst, C))  # drawn first, like pipeline.py:187
-    xt = _f32(x0)
+    xt = _latent(x0)
     if sigma_t == 0.0:
         return upsample_area_3d(x0, target)
     if sigma_t == 1.0:
@@ -281,12 +314,13 @@ def gaussian_analytic_denoiser(mu: float, s: float) -> "Denoiser":
         sig = ctx.sigma
         a = 1.0 - sig
         denom = a * a * s2 + sig * sig
-        # numpy >= 2 keeps Python scalars weak: every op runs in float32 with the scalar
-        # rounded to float32, as torch does; the divisor is a 0-dim tensor so the division
-        # is a true per-element divide (a CPU-scalar divide would multiply by 1/denom)
-        t = tok.float()
+        # numpy >= 2 keeps Python scalars weak: every op runs in the array's dtype (float32
+        # for latents) with the scalar rounded to it, as torch does; the divisor is a 0-dim
+        # tensor so the division is a true per-element divide (a CPU-scalar divide would
+        # multiply by 1/denom).  numpy callers get numpy back.
+        t = tok if tok.dtype == torch.float64 else tok.float()
         num = sig * (t - mu) - a * s2 * t
-        return num / torch.tensor(denom, dtype=torch.float32, device=t.device)
+        return _dev.to_like(num / torch.tensor(denom, dtype=t.dtype, device=t.device), tokens)
 
     return velocity
 
@@ -347,7 +381,7 @@ def run_pipeline(plan: StagePlan, denoiser: Denoiser, rng=0, channels: int = 1) 
         last = len(stage.step_indices) - 1
         for j, idx in enumerate(stage.step_indices):
             sigma = float(schedule.sigmas[j])
-            z = gather_rows(x.reshape(n, channels), perm.forward)
+            z = gather_rows(x.reshape(n, channels), perm.forward_dev)
             ctx = StepContext(stage=s_idx, step_index=int(idx), sigma=sigma, dims=dims,
                               layout=layout, perm=perm, statics=statics, positions=positions,
                               params=params, beta=beta)

@@ -10,7 +10,7 @@ vectorised, any row payload (sfc.py:213-237).
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -53,37 +53,65 @@ class GridDims:
         return cls(*(int(p) for p in parts))
 
 
-@dataclass(frozen=True)
 class Permutation:
-    """Curve <-> row-major bijection held on the device as int32 (sfc.py:70-95).
+    """Curve <-> row-major bijection (sfc.py:70-95).
 
-    ``forward[i]`` is the row-major cell at curve position i; ``inverse`` its
-    inverse.  ``forward_np``/``inverse_np`` give the reference's int64 numpy view.
+    ``forward[i]`` is the row-major cell at curve position i; ``inverse`` its inverse.
+    As in the reference both are read-only int64 numpy arrays (sfc.py:91-92; copied
+    from the device once, on first access).  The kernels use the device copies
+    ``forward_dev`` / ``inverse_dev`` (int32, resident in HBM).  Immutable like the
+    reference's frozen dataclass.
     """
 
-    dims: GridDims
-    forward: torch.Tensor
-    inverse: torch.Tensor = field(repr=False)
+    __slots__ = ("dims", "forward_dev", "inverse_dev", "_np")
 
-    def __post_init__(self):
-        n = self.dims.n_cells
-        if tuple(self.forward.shape) != (n,) or tuple(self.inverse.shape) != (n,):
-            raise ShapeError(f"permutation arrays must have length {n}")
+    def __init__(self, dims: GridDims, forward, inverse):
+        n = dims.n_cells
+        if tuple(forward.shape) != (n,) or tuple(inverse.shape) != (n,):
+            raise ShapeError(f"permutation arrays must have length {n}, got "
+                             f"{tuple(forward.shape)} / {tuple(inverse.shape)}")
+        fwd = _dev.as_cuda(forward, torch.int32)
+        inv = _dev.as_cuda(inverse, torch.int32)
+        host = {}
+        if not isinstance(forward, torch.Tensor) or not isinstance(inverse, torch.Tensor):
+            # a caller-built permutation is checked like sfc.py:88-89
+            f64 = np.asarray(forward.cpu() if isinstance(forward, torch.Tensor) else forward,
+                             dtype=np.int64)
+            i64 = np.asarray(inverse.cpu() if isinstance(inverse, torch.Tensor) else inverse,
+                             dtype=np.int64)
+            if not np.array_equal(f64[i64], np.arange(n)):
+                raise ShapeError("inverse is not the inverse of forward")
+        for name, val in (("dims", dims), ("forward_dev", fwd), ("inverse_dev", inv), ("_np", host)):
+            object.__setattr__(self, name, val)
+
+    def __setattr__(self, name, value):
+        raise AttributeError(f"Permutation is immutable (cannot set {name!r})")
 
     def __len__(self) -> int:
-        return int(self.forward.shape[0])
+        return int(self.forward_dev.shape[0])
 
-    @property
-    def forward_np(self) -> np.ndarray:
-        a = self.forward.cpu().numpy().astype(np.int64)
-        a.setflags(write=False)
+    def __repr__(self) -> str:
+        return f"Permutation(dims={self.dims!r}, n={len(self)})"
+
+    def _host(self, key: str, dev: torch.Tensor) -> np.ndarray:
+        a = self._np.get(key)
+        if a is None:
+            a = dev.cpu().numpy().astype(np.int64)
+            a.setflags(write=False)
+            self._np[key] = a
         return a
 
     @property
-    def inverse_np(self) -> np.ndarray:
-        a = self.inverse.cpu().numpy().astype(np.int64)
-        a.setflags(write=False)
-        return a
+    def forward(self) -> np.ndarray:
+        return self._host("f", self.forward_dev)
+
+    @property
+    def inverse(self) -> np.ndarray:
+        return self._host("i", self.inverse_dev)
+
+    # round-1 names, kept for callers of this package
+    forward_np = forward
+    inverse_np = inverse
 
 
 def build_curve(dims: GridDims) -> Permutation:
@@ -96,7 +124,10 @@ def build_curve(dims: GridDims) -> Permutation:
     inv = torch.empty(n, dtype=torch.int32, device=dev)
     _native.call("tcb_curve_build", dims.t, dims.h, dims.w, fwd.data_ptr(), inv.data_ptr(),
                  _dev.stream())
-    return Permutation(dims=dims, forward=fwd, inverse=inv)
+    perm = Permutation.__new__(Permutation)
+    for name, val in (("dims", dims), ("forward_dev", fwd), ("inverse_dev", inv), ("_np", {})):
+        object.__setattr__(perm, name, val)
+    return perm
 
 
 def gather_rows(x: torch.Tensor, index: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -127,12 +158,12 @@ def _permute(tokens, index: torch.Tensor):
 
 def apply_permutation(tokens, perm: Permutation):
     """Curve order: ``out[i] = tokens[perm.forward[i]]`` (sfc.py:226-232)."""
-    return _permute(tokens, perm.forward)
+    return _permute(tokens, perm.forward_dev)
 
 
 def invert_permutation(tokens, perm: Permutation):
     """Row-major order: ``out[i] = tokens[perm.inverse[i]]`` (sfc.py:235-237)."""
-    return _permute(tokens, perm.inverse)
+    return _permute(tokens, perm.inverse_dev)
 
 
 def padded_token_count(n_tokens: int, m: int) -> tuple[int, int]:

@@ -57,3 +57,8 @@ def attention_cases():
         k, p, beta = float(meta[8]), float(meta[9]), float(meta[10])
         yield str(name), dict(dims=(t, h, w), m=m, n_cond=nc, H=H, d=d, seed=seed, k=k, p=p,
                               beta=beta), g
+
+
+def host(x):
+    """numpy view of a result that is numpy (numpy callers) or a device tensor."""
+    return x if isinstance(x, np.ndarray) else x.detach().cpu().numpy()

@@ -65,7 +65,7 @@ def test_criterion_06_adjacency_equals_brute_force():
         fw = perm.forward_np
         for m in (4, 8, 16):
             lay = tcb.build_layout(dims, m)
-            got = tcb.adjacency_mask(lay, dims, perm).cpu().numpy()
+            got = tcb.adjacency_mask(lay, dims, perm)
             assert np.array_equal(got, brute_adjacency(dims_t, fw, m)), (dims_t, m)
 
 

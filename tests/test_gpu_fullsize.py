@@ -11,6 +11,8 @@
 """
 
 import numpy as np
+
+from golden_io import host as _host
 import pytest
 import torch
 
@@ -62,8 +64,8 @@ def test_c2_masks_bit_exact_on_sampled_heads(c2, head):
 
 def test_c2_mask_row_properties(c2):
     lay, mask = c2["lay"], c2["mask"]
-    bits = mask.bits.cpu().numpy()  # (H, M_v, M_total)
-    adja = c2["st"].adja.cpu().numpy()
+    bits = _host(mask.bits)  # (H, M_v, M_total)
+    adja = c2["st"].adja
     n_floor = c2["params"].n_floor(lay.M_v)
     assert np.all(bits[:, :, lay.M_v:])  # condition columns (the text sink)
     assert np.all(bits[:, :, : lay.M_v] >= adja[None])  # 3D neighbours incl. the diagonal
@@ -137,7 +139,7 @@ def test_large_grid_beyond_c2_masks_and_carve(p):
     assert np.array_equal(got, bits[0])
     np.testing.assert_allclose(R[0, rows].cpu().numpy(), Rs[0], rtol=1e-12, atol=0)
     items = [(0, 0), (0, 3000), (0, L["M_v"] - 1), (0, L["M_v"])]  # last = condition row
-    ref = oracle.carve(qn, kn, vn, mask.bits.cpu().numpy(), L, 0.0, workers=4, items=items)
+    ref = oracle.carve(qn, kn, vn, _host(mask.bits), L, 0.0, workers=4, items=items)
     got = out.float().cpu().numpy()
     for _, b in items:
         sl = slice(b * m, (b + 1) * m)

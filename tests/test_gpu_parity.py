@@ -5,6 +5,8 @@ for floating point)."""
 import hashlib
 
 import numpy as np
+
+from golden_io import host as _host
 import pytest
 import torch
 
@@ -78,7 +80,7 @@ def test_adjacency_bit_exact():
         assert [lay.n_valid, lay.M_v, lay.M_c, lay.M_total, lay.padded_total, lay.cond_start] == \
             [int(v) for v in row[5:11]]
         st = tcb.StaticMasks.build(lay, g, tcb.build_curve(g))
-        assert np.array_equal(st.adja.cpu().numpy(), adj), dims
+        assert np.array_equal(st.adja, adj), dims
 
 
 # ----------------------------------------------------------------- K3/K4/K5 masks
@@ -92,18 +94,18 @@ def test_pool_relevance_select(case):
         st = tcb.StaticMasks.build(lay, dims, tcb.build_curve(dims))
         q, k, _ = gio.qkv(P["seed"], P["H"], lay.padded_total, P["d"])
         pq = tcb.block_pool(q, lay)
-        assert np.array_equal(pq.values.cpu().numpy(), g[f"{name}_pq"])  # bit-exact
+        assert np.array_equal(_host(pq.values), g[f"{name}_pq"])  # bit-exact
         params = tcb.SelectionParams(k=P["k"], p=P["p"])
         mask, R = tcb.build_block_mask(q, k, lay, st, params)
         np.testing.assert_allclose(R, g[f"{name}_R"], rtol=1e-12, atol=1e-15)
         want = gio.unpack_bits(g[f"{name}_bits"], lay.M_total)
-        got = mask.bits.cpu().numpy()
+        got = _host(mask.bits)
         assert (got == want).mean() >= 0.999
         assert np.array_equal(got, want)
         # bit-exact given the reference's own R
         top = tcb.importance_mask(g[f"{name}_R"], params, lay.M_v)
         u = tcb.union_mask(torch.from_numpy(top).cuda(), st.cond, st.adja, lay)
-        assert np.array_equal(u.bits.cpu().numpy(), want)
+        assert np.array_equal(_host(u.bits), want)
         # CSR is the ascending list of set bits
         idx, cnt = mask.kv_idx.cpu().numpy(), mask.kv_cnt.cpu().numpy()
         for h in range(P["H"]):
@@ -202,7 +204,7 @@ def test_carve_bf16_tcgen05_long_rows_and_determinism():
     assert torch.equal(o1, o2)  # bitwise run-to-run
     L = oracle.layout_scalars(dims.as_tuple(), 128, 200)
     ref = oracle.carve(q.float().cpu().numpy(), k.float().cpu().numpy(), v.float().cpu().numpy(),
-                       mask.bits.cpu().numpy(), L, 0.7, workers=8)
+                       _host(mask.bits), L, 0.7, workers=8)
     err = np.abs(o1.float().cpu().numpy() - ref).max() / np.abs(ref).max()
     assert err <= 2e-2, err  # 2e-2 relative to max|ref|
 
@@ -333,7 +335,7 @@ def test_carve_layer_host_pipeline_bitwise(hpc):
     q32, k32, v32 = (t.float().numpy() for t in (hq, hk, hv))
     o32, m32 = tcb.carve_layer(q32, k32, v32, lay, st, params, heads_per_chunk=2)
     L = oracle.layout_scalars(dims.as_tuple(), 128, 100)
-    ref32 = oracle.carve(q32, k32, v32, m32.bits.cpu().numpy(), L, 0.0, workers=8)
+    ref32 = oracle.carve(q32, k32, v32, _host(m32.bits), L, 0.0, workers=8)
     assert isinstance(o32, np.ndarray)
     np.testing.assert_allclose(o32, ref32, rtol=1e-5, atol=1e-5)
 
@@ -469,7 +471,7 @@ def test_carve_bf16_fuzz_random_layouts():
         out = tcb.carve_attention(tcb.AttentionInputs(q=qb, k=kb, v=vb, layout=lay), mask,
                                   tcb.AmplifierBias(beta))
         L = oracle.layout_scalars(dims.as_tuple(), 128, n_cond)
-        bits = mask.bits.cpu().numpy()
+        bits = _host(mask.bits)
         q32, k32, v32 = (t.float().cpu().numpy() for t in (qb, kb, vb))
         ref = oracle.carve(q32, k32, v32, bits, L, beta, workers=8)
         got = out.float().cpu().numpy()
@@ -540,11 +542,11 @@ def test_carve_fp16_tcgen05_and_pool(d):
     L = oracle.layout_scalars(dims.as_tuple(), 128, 60)
     q32, k32, v32 = (t.float().cpu().numpy() for t in (qh, kh, vh))
     pq, _ = oracle.pool_blocks(q32, L)  # fp16 values pool bit-exactly in float64
-    got_pq = tcb.block_pool(qh, lay).values.cpu().numpy()
+    got_pq = _host(tcb.block_pool(qh, lay).values)
     assert np.array_equal(got_pq, pq)
     out = tcb.carve_attention(tcb.AttentionInputs(q=qh, k=kh, v=vh, layout=lay), mask, tcb.AmplifierBias(0.3))
     assert out.dtype == torch.float16
-    ref = oracle.carve(q32, k32, v32, mask.bits.cpu().numpy(), L, 0.3, workers=8)
+    ref = oracle.carve(q32, k32, v32, _host(mask.bits), L, 0.3, workers=8)
     got = out.float().cpu().numpy()
     err = np.abs(got - ref).max() / np.abs(ref).max()
     assert err <= 1e-2, err

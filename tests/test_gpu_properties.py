@@ -13,6 +13,8 @@ fp32 inputs run the fp32-math kernels (1e-5), bf16 the tcgen05 kernel (north_sta
 tolerance)."""
 
 import numpy as np
+
+from golden_io import host as _host
 import pytest
 import torch
 from hypothesis import HealthCheck, given, settings
@@ -44,11 +46,11 @@ def test_pool_constant_and_padding_excluded(dims, m, n_cond, seed):
     valid = lay.token_valid_mask
     x_pad = x.copy()
     x_pad[:, ~valid] = 1e6  # padding content must not matter
-    a = tcb.block_pool(x, lay).values.cpu().numpy()
-    b = tcb.block_pool(x_pad, lay).values.cpu().numpy()
+    a = _host(tcb.block_pool(x, lay).values)
+    b = _host(tcb.block_pool(x_pad, lay).values)
     assert np.array_equal(a, b)
     c = np.full_like(x, 3.25)
-    pc = tcb.block_pool(c, lay).values.cpu().numpy()
+    pc = _host(tcb.block_pool(c, lay).values)
     counts = np.asarray(lay.block_valid_counts)
     assert np.all(pc[:, counts > 0] == 3.25)
 
@@ -81,7 +83,7 @@ def test_heads_are_independent(dims, seed):
         m1, _ = tcb.build_block_mask(q[h:h + 1], k[h:h + 1], lay, stt, params)
         o1 = tcb.carve_attention(tcb.AttentionInputs(q=q[h:h + 1], k=k[h:h + 1], v=v[h:h + 1],
                                                      layout=lay), m1)
-        assert np.array_equal(np.asarray(m1.bits.cpu())[0], np.asarray(mask.bits.cpu())[h])
+        assert np.array_equal(_host(m1.bits)[0], _host(mask.bits)[h])
         assert np.array_equal(o1[0], out[h])
 
 
@@ -140,7 +142,7 @@ def test_output_rows_are_convex_combinations(dims, seed):
                .cuda().to(torch.bfloat16) for _ in range(3))
     mask, _ = tcb.build_block_mask(q, k, lay, stt, tcb.SelectionParams(k=0.2, p=0.0))
     out = tcb.carve_attention(tcb.AttentionInputs(q=q, k=k, v=v, layout=lay), mask).float().cpu()
-    bits = mask.bits.cpu().numpy()
+    bits = _host(mask.bits)
     vn = v.float().cpu().numpy()
     valid = lay.token_valid_mask
     m = lay.m

@@ -36,5 +36,5 @@ print("separate (n,H,d) sources", f"{t:.4f} ms {byts / t / 1e6:.0f} GB/s")
 # write side alone: token-major destination (no transpose) via a plain gather of 6 KB rows
 x = qkv[:, 0].contiguous()
 y = torch.empty_like(x)
-t = timed(lambda: tcb.gather_rows(x, perm.forward, out=y))
+t = timed(lambda: tcb.gather_rows(x, perm.forward_dev, out=y))
 print("gather_rows 6 KB rows", f"{t:.4f} ms {2 * x.numel() * 2 / t / 1e6:.0f} GB/s")
