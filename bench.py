@@ -108,6 +108,7 @@ def run_gpu(args):
     import paper_2505_16864_b200 as tcb
     from paper_2505_16864_b200 import _native
     from paper_2505_16864_b200.attention import _workspace
+    from paper_2505_16864_b200.masks import fused_scratch, launch_mask, mask_buffers
     from paper_2505_16864_b200.partition import mask_words
 
     world, rank, local = dist_env()
@@ -148,35 +149,29 @@ def run_gpu(args):
 
     pq = torch.empty((Hl, Mt, D), dtype=torch.float64, device=dev)
     pk = torch.empty_like(pq)
-    R = torch.empty((Hl, Mv, Mt), dtype=torch.float64, device=dev)
-    bits = torch.empty((Hl, Mv, words), dtype=torch.int32, device=dev)
-    kv_idx = torch.empty((Hl, Mv, Mt), dtype=torch.int32, device=dev)
-    kv_cnt = torch.empty((Hl, Mv), dtype=torch.int32, device=dev)
+    bits, kv_cnt = mask_buffers(Hl, layout, dev)
+    scratch = fused_scratch(layout, D, P_CUT, dev)
     work = _workspace(dev)
-    n_floor = params.n_floor(Mv)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def layer(qh, kh, vh, out, marks=None, h0=0):
-        """The four launches of one carved-attention layer on head-major views; mask
-        buffers are used from local head h0 on (an exchange chunk's slice)."""
+        """The launches of one carved-attention layer on head-major views (pool, fused
+        scores + select + union -- two passes, the second only re-runs undecided rows -- and
+        carve); mask buffers are used from local head h0 on (an exchange chunk's slice)."""
         sh, sn = qh.stride(0), qh.stride(1)
         Hc = qh.shape[0]  # all local heads, or one exchange chunk of them
-        bq, bk, bR = pq[h0:h0 + Hc], pk[h0:h0 + Hc], R[h0:h0 + Hc]
-        bb, bi, bc = bits[h0:h0 + Hc], kv_idx[h0:h0 + Hc], kv_cnt[h0:h0 + Hc]
+        bq, bk = pq[h0:h0 + Hc], pk[h0:h0 + Hc]
+        bb, bc = bits[h0:h0 + Hc], kv_cnt[h0:h0 + Hc]
         if marks: marks[0].record()
         _native.call("tcb_block_pool", qh.data_ptr(), kh.data_ptr(), 1, sh, sn, Hc, D, M, Mv, Mt,
                      layout.n_valid, layout.n_cond, bq.data_ptr(), bk.data_ptr(), sptr)
         if marks: marks[1].record()
-        _native.call("tcb_block_scores", bq.data_ptr(), Mt, bk.data_ptr(), Hc, Mv, Mt, D,
-                     bR.data_ptr(), sptr)
+        launch_mask(bq, bk, layout, adja, params, bb, bc, sptr, scratch)
         if marks: marks[2].record()
-        _native.call("tcb_block_select_scores", bR.data_ptr(), Hc, Mv, Mt, adja.data_ptr(), words,
-                     n_floor, float(P_CUT), 1, bb.data_ptr(), bi.data_ptr(), bc.data_ptr(), sptr)
-        if marks: marks[3].record()
         _native.call("tcb_carve_fwd", qh.data_ptr(), kh.data_ptr(), vh.data_ptr(), out.data_ptr(), 1,
-                     sh, sn, bi.data_ptr(), bc.data_ptr(), Hc, D, M, Mv, Mt, layout.n_valid,
+                     sh, sn, bb.data_ptr(), words, bc.data_ptr(), Hc, D, M, Mv, Mt, layout.n_valid,
                      layout.n_cond, 0.0, work.data_ptr(), sptr)
-        if marks: marks[4].record()
+        if marks: marks[3].record()
         return out
 
     if world == 1:
@@ -235,7 +230,7 @@ def run_gpu(args):
         dist.all_reduce(t)
         pairs = int(t.item())
 
-    marks = [[ev() for _ in range(5)] for _ in range(args.steps)]
+    marks = [[ev() for _ in range(4)] for _ in range(args.steps)]
     t0, t1 = ev(), ev()
     barrier()
     with Clocks(local) as clk:
@@ -245,17 +240,17 @@ def run_gpu(args):
         t1.record()
         barrier()
     total_ms = t0.elapsed_time(t1)
-    per = np.array([[marks[i][j].elapsed_time(marks[i][j + 1]) for j in range(4)]
+    per = np.array([[marks[i][j].elapsed_time(marks[i][j + 1]) for j in range(3)]
                     for i in range(args.steps)])
     ms_step = total_ms / args.steps
     if world > 1:
         t = torch.tensor([ms_step], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
-    k_pool, k_rel, k_sel, k_carve = per.mean(axis=0)
+    k_pool, k_sel, k_carve = per.mean(axis=0)
     chunked = world > 1 and args.a2a_chunks > 1
     if chunked:  # per-kernel marks do not separate the pipelined chunks: use the layer time
-        k_pool = k_rel = k_sel = float("nan")
+        k_pool = k_sel = float("nan")
         k_carve = ms_step
     flops = 4.0 * M * M * D * pairs
     flops_local = 4.0 * M * M * D * pairs_local
@@ -296,7 +291,7 @@ def run_gpu(args):
                     "build_block_mask + carve_attention on the head shard, all-to-all) -> D2H")
 
             def local_api(qh, kh, vh, lay):
-                mask, _ = tcb.build_block_mask(qh, kh, lay, statics, params)
+                mask, _ = tcb.build_block_mask(qh, kh, lay, statics, params, need_relevance=False)
                 return tcb.carve_attention(tcb.AttentionInputs(q=qh, k=kh, v=vh, layout=lay), mask)
 
             def e2e_step():
@@ -359,8 +354,9 @@ def run_gpu(args):
         "layer_tflops": round(flops / (ms_step * 1e-3) / 1e12, 1),
         "cuda_graph_ms_per_step": graph_ms,
         "kernels_ms": None if chunked else {
-            "block_pool": round(float(k_pool), 4), "block_scores": round(float(k_rel), 4),
-            "block_softmax_select": round(float(k_sel), 4), "carve_fwd": round(float(k_carve), 4)},
+            "block_pool": round(float(k_pool), 4),
+            "block_mask_fused (scores + select + union)": round(float(k_sel), 4),
+            "carve_fwd": round(float(k_carve), 4)},
         "roofline": {"bound": "tensor", "kernel": "k_carve_tc<128>",
                      "achieved": round(carve_tflops, 1), "peak": tf_sust, "unit": "TFLOP/s",
                      "frac": round(carve_tflops / tf_sust, 4),
@@ -373,6 +369,8 @@ def run_gpu(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "gpu_launches": 4 * args.steps * (min(args.a2a_chunks, Hl) if chunked else 1),
+        "launches_per_layer": "k_pool, k_select_fused (pass 1), k_select_fused (pass 2: undecided "
+                              "rows only), k_carve_tc",
         "clocks": clk.result,
     }
     print(json.dumps(line))

@@ -30,6 +30,7 @@ sys.path.insert(0, ROOT)
 import paper_2505_16864_b200 as tcb  # noqa: E402
 from paper_2505_16864_b200 import _native  # noqa: E402
 from paper_2505_16864_b200.attention import _workspace  # noqa: E402
+from paper_2505_16864_b200.masks import fused_scratch, launch_mask, mask_buffers  # noqa: E402
 from paper_2505_16864_b200.partition import mask_words  # noqa: E402
 
 
@@ -57,7 +58,7 @@ def peaks():
 
 
 class Layer:
-    """Device buffers + the four launches of one carved-attention layer."""
+    """Device buffers + the launches of one carved-attention layer."""
 
     def __init__(self, dims, n_cond, H, k_rate, seed=0, p_cut=0.0, beta=0.0):
         self.dims = tcb.GridDims(*dims)
@@ -73,31 +74,25 @@ class Layer:
         self.o = torch.empty_like(self.q)
         self.pq = torch.empty((H, L.M_total, 128), dtype=torch.float64, device="cuda")
         self.pk = torch.empty_like(self.pq)
-        self.R = torch.empty((H, L.M_v, L.M_total), dtype=torch.float64, device="cuda")
         self.words = mask_words(L.M_total)
-        self.bits = torch.empty((H, L.M_v, self.words), dtype=torch.int32, device="cuda")
-        self.kv_idx = torch.empty((H, L.M_v, L.M_total), dtype=torch.int32, device="cuda")
-        self.kv_cnt = torch.empty((H, L.M_v), dtype=torch.int32, device="cuda")
+        self.bits, self.kv_cnt = mask_buffers(H, L, self.q.device)
+        self.scratch = fused_scratch(L, 128, p_cut, self.q.device)
         self.work = _workspace(self.q.device)
         self.s = torch.cuda.current_stream().cuda_stream
 
     def mask(self):
         L, H = self.lay, self.H
-        n_floor = tcb.SelectionParams(k=self.k, p=self.p).n_floor(L.M_v)
         _native.call("tcb_block_pool", self.q.data_ptr(), self.kk.data_ptr(), 1, self.q.stride(0),
                      self.q.stride(1), H, 128, 128, L.M_v, L.M_total, L.n_valid, L.n_cond,
                      self.pq.data_ptr(), self.pk.data_ptr(), self.s)
-        _native.call("tcb_block_scores", self.pq.data_ptr(), L.M_total, self.pk.data_ptr(), H, L.M_v,
-                     L.M_total, 128, self.R.data_ptr(), self.s)
-        _native.call("tcb_block_select_scores", self.R.data_ptr(), H, L.M_v, L.M_total,
-                     self.adja.data_ptr(), self.words, n_floor, float(self.p), 1, self.bits.data_ptr(),
-                     self.kv_idx.data_ptr(), self.kv_cnt.data_ptr(), self.s)
+        launch_mask(self.pq, self.pk, L, self.adja, tcb.SelectionParams(k=self.k, p=self.p),
+                    self.bits, self.kv_cnt, self.s, self.scratch)
 
     def carve(self):
         L = self.lay
         _native.call("tcb_carve_fwd", self.q.data_ptr(), self.kk.data_ptr(), self.v.data_ptr(),
                      self.o.data_ptr(), 1, self.q.stride(0), self.q.stride(1),
-                     self.kv_idx.data_ptr(), self.kv_cnt.data_ptr(), self.H, 128, 128, L.M_v,
+                     self.bits.data_ptr(), self.words, self.kv_cnt.data_ptr(), self.H, 128, 128, L.M_v,
                      L.M_total, L.n_valid, L.n_cond, float(self.beta), self.work.data_ptr(), self.s)
 
     def pairs(self):

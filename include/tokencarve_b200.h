@@ -38,7 +38,7 @@ extern "C" {
 #define TCB_F64 3 /* tcb_block_pool and the stage point ops only (reference float64 callers) */
 
 const char* tcb_last_error(void);
-int tcb_abi_version(void);
+int tcb_abi_version(void); /* 2 since the packed-bit mask ABI (no kv_idx) */
 
 /* K1 -- space-filling-curve index builder.
  * Replaces build_curve (sfc.py:198-210) = _gilbert2d/_gen2d (sfc.py:98-157)
@@ -73,52 +73,75 @@ int tcb_block_pool(const void* x0, const void* x1, int dtype, int64_t stride_h, 
 int tcb_block_relevance(const double* pq, int pq_blocks, const double* pk, int H, int rows,
                         int M_total, int d, double* R, void* stream);
 
+/* Mask representation (every select entry point writes it, every carve entry point reads
+ * it): bits (rows, words) uint32 -- column j of a row is bit j % 32 of word j / 32 -- plus
+ * the row popcounts kv_cnt (rows) int32.  The carve kernels walk the set bits of a row in
+ * ascending order, i.e. the reference's flatnonzero(bits[h, qb]) (attention.py:179); no
+ * CSR index array exists.  (H, M_v, words) at C2 is 2.7 MB; at the 8,192-block maximum
+ * 24 heads take 201 MB. */
+
 /* K5 + K6 union -- importance selection + union with condition and adjacency.
  * Replaces importance_mask (masks.py:137-159) and union_mask (masks.py:162-175).
  * R: (H, M_v, M_total) float64; adja: (M_v, words) or NULL (no adjacency term);
- * outputs: bits (H, M_v, words) uint32, ascending CSR kv_idx (H, M_v, M_total)
- * int32 (row capacity M_total) and kv_cnt (H, M_v) int32.  n_floor =
- * max(1, ceil(k*M_v)) computed by the host in float64 (masks.py:154).
- * with_union=0 returns the bare importance mask (no cond / adjacency OR). */
+ * outputs: bits (H, M_v, words), kv_cnt (H, M_v).  n_floor = max(1, ceil(k*M_v)) computed
+ * by the host in float64 (masks.py:154).  with_union=0 returns the bare importance mask
+ * (no cond / adjacency OR).  Bit-exact given R. */
 int tcb_block_select(const double* R, int H, int M_v, int M_total, const uint32_t* adja, int words,
-                     int n_floor, double p, int with_union, uint32_t* bits, int32_t* kv_idx,
-                     int32_t* kv_cnt, void* stream);
+                     int n_floor, double p, int with_union, uint32_t* bits, int32_t* kv_cnt,
+                     void* stream);
 
 /* K4a -- scaled pooled scores S[h,i,j] = pq[h,i].pk[h,j] / sqrt(d) (masks.py:130-131),
  * float64, i < rows, j < M_total.  First half of tcb_block_relevance. */
 int tcb_block_scores(const double* pq, int pq_blocks, const double* pk, int H, int rows,
                      int M_total, int d, double* S, void* stream);
 
-/* K4b+K5 fused -- S (from tcb_block_scores) is turned into R in place (row softmax,
+/* K4b+K5 -- S (from tcb_block_scores) is turned into R in place (row softmax,
  * masks.py:132-134, numpy pairwise row sums) and selected like tcb_block_select:
- * the build_block_mask fast path (masks.py:178-199) in two launches. */
+ * build_block_mask (masks.py:178-199) when the caller wants R back. */
 int tcb_block_select_scores(double* S, int H, int M_v, int M_total, const uint32_t* adja,
                             int words, int n_floor, double p, int with_union, uint32_t* bits,
-                            int32_t* kv_idx, int32_t* kv_cnt, void* stream);
+                            int32_t* kv_cnt, void* stream);
+
+/* K4+K5 fused -- the mask of build_block_mask (masks.py:178-199) from the pooled means
+ * without materialising R: each CTA computes the scores of an 8-row tile of one head on the
+ * FP64 tensor core into shared memory and selects those rows there (p == 0 selects on the
+ * scores directly: the softmax is monotone; rows whose top-k boundary is a near tie re-run
+ * exactly).  pq: (H, pq_blocks, d), pk: (H, M_total, d) float64.  Shapes the fused kernel
+ * does not cover (d not in {64, 128}, or a score tile beyond shared memory) run scores +
+ * select per row chunk through `scratch` (scratch_elems doubles, >= M_total; NULL is fine
+ * for covered shapes).  Union with cond columns and adja is always applied. */
+int tcb_block_mask_fused(const double* pq, int pq_blocks, const double* pk, int H, int M_v,
+                         int M_total, int d, const uint32_t* adja, int words, int n_floor, double p,
+                         uint32_t* bits, int32_t* kv_cnt, double* scratch, int64_t scratch_elems,
+                         void* stream);
+
+/* Scratch doubles tcb_block_mask_fused needs for a shape: 0 when the fused kernel covers it,
+ * else one bounded row chunk of scores (<= 256 MB). */
+int64_t tcb_block_mask_fused_scratch(int M_v, int M_total, int d, double p);
 
 /* Mask conversions for user-built BlockMask(bits=bool array) (masks.py:78-95). */
 int tcb_mask_pack(const uint8_t* dense, int64_t rows, int M_total, int words, uint32_t* bits,
-                  int32_t* kv_idx, int32_t* kv_cnt, void* stream);
+                  int32_t* kv_cnt, void* stream);
 int tcb_mask_unpack(const uint32_t* bits, int64_t rows, int M_total, int words, uint8_t* dense,
                     void* stream);
 
 /* K7/K8 -- block-sparse flash-attention forward.  Replaces carve_attention /
  * _carve_rows (attention.py:162-243).  q,k,v,o: (H, N_pad, d) with element
  * strides (stride_h, stride_n, 1), N_pad = M_total*m.  Vision q-block i of
- * head h streams kv blocks kv_idx[h,i,:kv_cnt[h,i]] (ascending); condition
- * q-blocks attend all M_total blocks; padding keys get -inf, beta is added on
- * condition keys of vision rows, padding rows of o are zeroed.
+ * head h streams the kv blocks set in bits[h,i,:] (words per row), ascending, kv_cnt[h,i]
+ * of them; condition q-blocks attend all M_total blocks; padding keys get -inf, beta is
+ * added on condition keys of vision rows, padding rows of o are zeroed.
  * dtype TCB_BF16 or TCB_F16 with m == 128 and d in {64,128} runs the tcgen05/TMEM/TMA
  * kernel; everything else runs the fp32 SIMT kernel (parity path).
  * work: caller-provided scratch of >= 16 bytes (scheduler counter). */
 int tcb_carve_fwd(const void* q, const void* k, const void* v, void* o, int dtype,
-                  int64_t stride_h, int64_t stride_n, const int32_t* kv_idx,
+                  int64_t stride_h, int64_t stride_n, const uint32_t* bits, int words,
                   const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
                   int64_t n_valid, int64_t n_cond, float beta, int32_t* work, void* stream);
 
 /* Like tcb_carve_fwd but forces the fp32-math SIMT kernel for any shape. */
 int tcb_carve_fwd_simt(const void* q, const void* k, const void* v, void* o, int dtype,
-                       int64_t stride_h, int64_t stride_n, const int32_t* kv_idx,
+                       int64_t stride_h, int64_t stride_n, const uint32_t* bits, int words,
                        const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
                        int64_t n_valid, int64_t n_cond, float beta, void* stream);
 

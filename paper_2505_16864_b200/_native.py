@@ -33,14 +33,16 @@ SIGNATURES = {
     "tcb_adjacency_build": [_P, _I, _I, _I, _I, _I, _I, _P, _P],
     "tcb_block_pool": [_P, _P, _I, _I64, _I64, _I, _I, _I, _I, _I, _I64, _I64, _P, _P, _P],
     "tcb_block_relevance": [_P, _I, _P, _I, _I, _I, _I, _P, _P],
-    "tcb_block_select": [_P, _I, _I, _I, _P, _I, _I, _D, _I, _P, _P, _P, _P],
+    "tcb_block_select": [_P, _I, _I, _I, _P, _I, _I, _D, _I, _P, _P, _P],
     "tcb_block_scores": [_P, _I, _P, _I, _I, _I, _I, _P, _P],
-    "tcb_block_select_scores": [_P, _I, _I, _I, _P, _I, _I, _D, _I, _P, _P, _P, _P],
-    "tcb_mask_pack": [_P, _I64, _I, _I, _P, _P, _P, _P],
+    "tcb_block_select_scores": [_P, _I, _I, _I, _P, _I, _I, _D, _I, _P, _P, _P],
+    "tcb_block_mask_fused": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _D, _P, _P, _P, _I64, _P],
+    "tcb_block_mask_fused_scratch": [_I, _I, _I, _D],
+    "tcb_mask_pack": [_P, _I64, _I, _I, _P, _P, _P],
     "tcb_mask_unpack": [_P, _I64, _I, _I, _P, _P],
-    "tcb_carve_fwd": [_P, _P, _P, _P, _I, _I64, _I64, _P, _P, _I, _I, _I, _I, _I, _I64, _I64,
-                      _F, _P, _P],
-    "tcb_carve_fwd_simt": [_P, _P, _P, _P, _I, _I64, _I64, _P, _P, _I, _I, _I, _I, _I, _I64,
+    "tcb_carve_fwd": [_P, _P, _P, _P, _I, _I64, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _I64,
+                      _I64, _F, _P, _P],
+    "tcb_carve_fwd_simt": [_P, _P, _P, _P, _I, _I64, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _I64,
                            _I64, _F, _P],
     "tcb_upsample_renoise": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _I, _U64, _U64, _P],
     "tcb_euler_step": [_P, _P, _P, _I64, _F, _P],
@@ -81,12 +83,18 @@ def load():
         for name, args in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.argtypes = args
-            fn.restype = C.c_char_p if name == "tcb_last_error" else C.c_int
+            fn.restype = (C.c_char_p if name == "tcb_last_error" else
+                          C.c_int64 if name == "tcb_block_mask_fused_scratch" else C.c_int)
         _lib = lib
     return _lib
 
 
 _EXC = {1: ShapeError, 2: DomainError, 3: SizeError, 4: ContractError}
+
+
+def query(name: str, *args) -> int:
+    """A C-ABI entry that returns a value instead of a status (no error mapping)."""
+    return int(getattr(load(), name)(*args))
 
 
 def call(name: str, *args) -> None:

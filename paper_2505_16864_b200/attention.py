@@ -98,7 +98,7 @@ def carve_raw(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: BlockMask
         raise ShapeError(f"q/k/v dtypes differ: {q.dtype}, {k.dtype}, {v.dtype}")
     if not (q.shape == k.shape == v.shape) or q.ndim != 3:
         raise ShapeError(f"q/k/v must share one (heads, N, d_k) shape")
-    _dev.same_device(q, k, v, mask.kv_idx, *(() if out is None else (out,)))
+    _dev.same_device(q, k, v, mask.words, *(() if out is None else (out,)))
     H, N, d = q.shape
     if k.stride() != q.stride() or v.stride() != q.stride() or q.stride(2) != 1:
         q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
@@ -108,8 +108,9 @@ def carve_raw(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: BlockMask
         if out.stride() != q.stride() or out.dtype != q.dtype or out.shape != q.shape:
             raise ShapeError("output must share the inputs' shape, dtype and strides")
         args = (q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), _dev.code_of(q.dtype),
-                q.stride(0), q.stride(1), mask.kv_idx.data_ptr(), mask.kv_cnt.data_ptr(), H, d,
-                layout.m, layout.M_v, layout.M_total, layout.n_valid, layout.n_cond, float(beta))
+                q.stride(0), q.stride(1), mask.words.data_ptr(), mask.words.shape[-1],
+                mask.kv_cnt.data_ptr(), H, d, layout.m, layout.M_v, layout.M_total, layout.n_valid,
+                layout.n_cond, float(beta))
         if simt:
             _native.call("tcb_carve_fwd_simt", *args, _dev.stream())
         else:

@@ -23,4 +23,4 @@ int check_launch(const char* what) {
 
 extern "C" const char* tcb_last_error(void) { return tcb::g_err; }
 
-extern "C" int tcb_abi_version(void) { return 1; }
+extern "C" int tcb_abi_version(void) { return 2; }  // 2: packed-bit masks, no kv_idx

@@ -31,7 +31,7 @@
 namespace tcb {
 
 struct CarveShape {
-  int H, d, m, M_v, M_total;
+  int H, d, m, M_v, M_total, W;  // W = uint32 words per packed mask row
   int64_t n_valid, n_cond;
   int64_t sh, sn;  // element strides (head, token)
 };
@@ -89,7 +89,7 @@ template <typename T>
 __global__ void __launch_bounds__(128) k_carve_simt(const T* __restrict__ q,
                                                     const T* __restrict__ k,
                                                     const T* __restrict__ v, T* __restrict__ o,
-                                                    CarveShape s, const int32_t* __restrict__ kv_idx,
+                                                    CarveShape s, const uint32_t* __restrict__ bits,
                                                     const int32_t* __restrict__ kv_cnt,
                                                     float beta, float scale) {
   extern __shared__ float sm_simt[];
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(128) k_carve_simt(const T* __restrict__ q,
   const int qb = blockIdx.x - h * s.M_total;
   const bool vis = qb < s.M_v;
   const int nkv = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-  const int32_t* list = vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr;
+  const uint32_t* brow = vis ? bits + ((int64_t)h * s.M_v + qb) * s.W : nullptr;
   const int qvalid = block_valid(qb, s.m, s.M_v, s.n_valid, s.n_cond);
   const T* qh = q + (int64_t)h * s.sh;
   const T* kh = k + (int64_t)h * s.sh;
@@ -120,8 +120,9 @@ __global__ void __launch_bounds__(128) k_carve_simt(const T* __restrict__ q,
 #pragma unroll
     for (int i = 0; i < SIMT_MAXC; ++i) acc[i] = 0.f;
     float mi = -INFINITY, li = 0.f;
+    BitWalk bw(brow);
     for (int t = 0; t < nkv; ++t) {
-      const int b = vis ? list[t] : t;
+      const int b = vis ? bw.get(t) : t;
       const int kvalid = block_valid(b, s.m, s.M_v, s.n_valid, s.n_cond);
       const bool add_beta = vis && beta != 0.f && b >= s.M_v;
       for (int j = 0; j < s.m; ++j) {
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(128) k_carve_simt(const T* __restrict__ q,
 template <typename T, int MT, int DT>
 __global__ void __launch_bounds__(256, 1) k_carve_f32t(const T* __restrict__ q, const T* __restrict__ k,
                                                        const T* __restrict__ v, T* __restrict__ o,
-                                                       CarveShape s, const int32_t* __restrict__ kv_idx,
+                                                       CarveShape s, const uint32_t* __restrict__ bits,
                                                        const int32_t* __restrict__ kv_cnt, float beta,
                                                        float scale) {
   constexpr int M = 16 * MT, D = 16 * DT;
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(256, 1) k_carve_f32t(const T* __restrict__ q, 
   const int qb = blockIdx.x - h * s.M_total;
   const bool vis = qb < s.M_v;
   const int nkv = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-  const int32_t* list = vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr;
+  BitWalk bw(vis ? bits + ((int64_t)h * s.M_v + qb) * s.W : nullptr);
   const int qvalid = block_valid(qb, M, s.M_v, s.n_valid, s.n_cond);
   const T* qh = q + (int64_t)h * s.sh;
   const T* kh = k + (int64_t)h * s.sh;
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(256, 1) k_carve_f32t(const T* __restrict__ q, 
     for (int j = 0; j < DT; ++j) acc[i][j] = 0.f;
   }
   for (int t = 0; t < nkv; ++t) {
-    const int b = vis ? __ldg(list + t) : t;
+    const int b = vis ? bw.get(t) : t;
     const int kvalid = block_valid(b, M, s.M_v, s.n_valid, s.n_cond);
     const bool add_beta = vis && beta != 0.f && b >= s.M_v;
     __syncthreads();  // previous block's P / V reads done
@@ -439,24 +440,6 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
   return (uint64_t)lo | ((uint64_t)hi << 32);
 }
 
-// Warp-cooperative view of a row's ascending kv list: lane l caches entry 32*c + l of the
-// current chunk c; block(j) broadcasts entry j (all 32 lanes must call it together).
-struct KvList {
-  const int32_t* list;
-  int n, lane, chunk, cache;
-  __device__ KvList(const int32_t* l, int n_, int lane_) : list(l), n(n_), lane(lane_), chunk(-1), cache(0) {}
-  __device__ __forceinline__ int block(int j) {
-    if (!list) return j;
-    const int c = j >> 5;
-    if (c != chunk) {
-      chunk = c;
-      const int idx = c * 32 + lane;
-      cache = idx < n ? __ldg(list + idx) : 0;
-    }
-    return __shfl_sync(0xffffffffu, cache, j & 31);
-  }
-};
-
 // Timeline stamps for tools/carve_trace1.py: compiled only into trace builds
 // (TCB_NVCC_EXTRA=-DTCB_CARVE_TRACE python -m paper_2505_16864_b200._build), enabled at run
 // time by TCB_CARVE_DEBUG bit 3; CTA 0 writes clock64() per (event, half-step).
@@ -478,7 +461,7 @@ template <int D, int EMU, typename E = __nv_bfloat16>
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     k_carve_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, E* __restrict__ o,
-               CarveShape s, const int32_t* __restrict__ kv_idx,
+               CarveShape s, const uint32_t* __restrict__ bits,
                const int32_t* __restrict__ kv_cnt, int* __restrict__ counter, int total_items,
                float scale_log2, float beta_log2, int dbg) {
   using L = Smem<D>;
@@ -547,7 +530,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       decode_item(item, s, h, qb);
       const bool vis = qb < s.M_v;
       const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
-      KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
+      const uint32_t* brow = bits + ((int64_t)h * s.M_v + (vis ? qb : 0)) * s.W;
+      BitWalk wk(brow), wv(brow);  // K runs one half-step ahead of V: one walk per stream
       const int T = 2 * n;
       if (lane == 0) {
         ptx::mbar_wait(&bars->q_empty, (it & 1) ^ 1);
@@ -557,8 +541,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
           ptx::tma_load_3d(sQ + c * L::Q_CHUNK, &tm_q, &bars->q_full, c * 64, qb * BM, h, pol_q);
       }
       auto load = [&](const CUtensorMap* tm, uint8_t* base, uint64_t* full, uint64_t* empty,
-                      int slots, uint32_t& cnt, int t) {
-        const int b = kl.block(t >> 1);
+                      int slots, uint32_t& cnt, int t, BitWalk& walk) {
+        const int b = vis ? walk.get(t >> 1) : (t >> 1);
         if (lane == 0) {
           const int sl = cnt % slots;
           ptx::mbar_wait(&empty[sl], ((cnt / slots) & 1) ^ 1);
@@ -576,10 +560,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       };
       // same order the MMA warp consumes: K0, K1, V0, K2, V1, ..., V(T-1); an empty row
       // (T == 0, only reachable through a hand-built mask) loads nothing, like the MMA warp
-      if (T > 0) load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, 0);
+      if (T > 0) load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, 0, wk);
       for (int t = 0; t < T; ++t) {
-        if (t + 1 < T) load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, t + 1);
-        load(&tm_v, sV, bars->v_full, bars->v_empty, V_SLOTS, gv, t);
+        if (t + 1 < T) load(&tm_k, sK, bars->k_full, bars->k_empty, K_SLOTS, gk, t + 1, wk);
+        load(&tm_v, sV, bars->v_full, bars->v_empty, V_SLOTS, gv, t, wv);
       }
     }
   } else if (warp == 1) {
@@ -686,14 +670,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       decode_item(item, s, h, qb);
       const bool vis = qb < s.M_v;
       const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      KvList kl(vis ? kv_idx + ((int64_t)h * s.M_v + qb) * s.M_total : nullptr, n, lane);
+      BitWalk bw(bits + ((int64_t)h * s.M_v + (vis ? qb : 0)) * s.W);
       const int T = 2 * n;
       float m_run = -INFINITY, l_run = 0.f;
       int b = 0, kvalid = BK;
       float bias = 0.f;
       for (int t = 0; t < T; ++t, ++g) {
         if ((t & 1) == 0) {
-          b = kl.block(t >> 1);
+          b = vis ? bw.get(t >> 1) : (t >> 1);
           kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond);
           bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
         }
@@ -870,14 +854,16 @@ static cudaError_t once_per_device(std::atomic<uint64_t>& seen, F&& set_attr) {
 }
 
 static int validate(const void* q, const void* k, const void* v, void* o, int dtype,
-                    const int32_t* kv_idx, const int32_t* kv_cnt, const CarveShape& s) {
+                    const uint32_t* bits, const int32_t* kv_cnt, const CarveShape& s) {
   TCB_CHECK_ARG(q && k && v && o, TCB_ESHAPE, "null q/k/v/o");
   TCB_CHECK_ARG(dtype == TCB_F32 || dtype == TCB_BF16 || dtype == TCB_F16, TCB_EDOMAIN,
                 "unsupported dtype %d", dtype);
   TCB_CHECK_ARG(s.H >= 1 && s.d >= 1 && s.m >= 1 && s.M_v >= 0 && s.M_total >= s.M_v &&
                     s.M_total >= 1,
                 TCB_ESHAPE, "bad carve shape");
-  TCB_CHECK_ARG(s.M_v == 0 || (kv_idx && kv_cnt), TCB_ESHAPE, "null kv list");
+  TCB_CHECK_ARG(s.M_v == 0 || (bits && kv_cnt), TCB_ESHAPE, "null mask");
+  TCB_CHECK_ARG(s.W >= (s.M_total + 31) / 32, TCB_ESHAPE, "mask row has %d words < %d columns", s.W,
+                s.M_total);
   TCB_CHECK_ARG((int64_t)s.H * s.M_total < (int64_t)1 << 31, TCB_ESIZE, "too many work items");
   return TCB_OK;
 }
@@ -888,7 +874,7 @@ using namespace tcb;
 
 template <typename T, int MT, int DT>
 static int launch_f32t(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                       const int32_t* kv_idx, const int32_t* kv_cnt, float beta, cudaStream_t st) {
+                       const uint32_t* bits, const int32_t* kv_cnt, float beta, cudaStream_t st) {
   constexpr int M = 16 * MT, D = 16 * DT;
   // Q, K (M x (D+4)), V^T (D x (M+4)), and P (M x (M+4)) unless it fits in K's tile
   size_t smem = ((size_t)2 * M * (D + 4) + (size_t)D * (M + 4)) * sizeof(float);
@@ -903,35 +889,35 @@ static int launch_f32t(const void* q, const void* k, const void* v, void* o, con
   }
   const float scale = (float)(1.0 / sqrt((double)s.d));
   k_carve_f32t<T, MT, DT><<<(unsigned)((int64_t)s.H * s.M_total), 256, smem, st>>>(
-      (const T*)q, (const T*)k, (const T*)v, (T*)o, s, kv_idx, kv_cnt, beta, scale);
+      (const T*)q, (const T*)k, (const T*)v, (T*)o, s, bits, kv_cnt, beta, scale);
   return check_launch("k_carve_f32t");
 }
 
 template <typename T>
 static int try_f32t(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                    const int32_t* kv_idx, const int32_t* kv_cnt, float beta, cudaStream_t st) {
+                    const uint32_t* bits, const int32_t* kv_cnt, float beta, cudaStream_t st) {
   const int key = (s.m << 16) | s.d;
   switch (key) {
-    case (128 << 16) | 128: return launch_f32t<T, 8, 8>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
-    case (128 << 16) | 64: return launch_f32t<T, 8, 4>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
-    case (64 << 16) | 128: return launch_f32t<T, 4, 8>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
-    case (64 << 16) | 64: return launch_f32t<T, 4, 4>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
-    case (64 << 16) | 32: return launch_f32t<T, 4, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
-    case (32 << 16) | 64: return launch_f32t<T, 2, 4>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
-    case (32 << 16) | 32: return launch_f32t<T, 2, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
-    case (128 << 16) | 32: return launch_f32t<T, 8, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
-    case (128 << 16) | 16: return launch_f32t<T, 8, 1>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
-    case (64 << 16) | 16: return launch_f32t<T, 4, 1>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
-    case (16 << 16) | 16: return launch_f32t<T, 1, 1>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    case (128 << 16) | 128: return launch_f32t<T, 8, 8>(q, k, v, o, s, bits, kv_cnt, beta, st);
+    case (128 << 16) | 64: return launch_f32t<T, 8, 4>(q, k, v, o, s, bits, kv_cnt, beta, st);
+    case (64 << 16) | 128: return launch_f32t<T, 4, 8>(q, k, v, o, s, bits, kv_cnt, beta, st);
+    case (64 << 16) | 64: return launch_f32t<T, 4, 4>(q, k, v, o, s, bits, kv_cnt, beta, st);
+    case (64 << 16) | 32: return launch_f32t<T, 4, 2>(q, k, v, o, s, bits, kv_cnt, beta, st);
+    case (32 << 16) | 64: return launch_f32t<T, 2, 4>(q, k, v, o, s, bits, kv_cnt, beta, st);
+    case (32 << 16) | 32: return launch_f32t<T, 2, 2>(q, k, v, o, s, bits, kv_cnt, beta, st);
+    case (128 << 16) | 32: return launch_f32t<T, 8, 2>(q, k, v, o, s, bits, kv_cnt, beta, st);
+    case (128 << 16) | 16: return launch_f32t<T, 8, 1>(q, k, v, o, s, bits, kv_cnt, beta, st);
+    case (64 << 16) | 16: return launch_f32t<T, 4, 1>(q, k, v, o, s, bits, kv_cnt, beta, st);
+    case (16 << 16) | 16: return launch_f32t<T, 1, 1>(q, k, v, o, s, bits, kv_cnt, beta, st);
     default: return -1;  // not tiled: the per-row kernel takes it
   }
 }
 
 template <typename T>
 static int launch_simt_t(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                         const int32_t* kv_idx, const int32_t* kv_cnt, float beta, cudaStream_t st) {
+                         const uint32_t* bits, const int32_t* kv_cnt, float beta, cudaStream_t st) {
   {  // tiled fp32-math kernel for the common block / head sizes
-    const int rc = try_f32t<T>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+    const int rc = try_f32t<T>(q, k, v, o, s, bits, kv_cnt, beta, st);
     if (rc != -1) return rc;
   }
   TCB_CHECK_ARG(s.d <= 32 * SIMT_MAXC, TCB_ESIZE, "SIMT carve supports d <= %d", 32 * SIMT_MAXC);
@@ -943,17 +929,17 @@ static int launch_simt_t(const void* q, const void* k, const void* v, void* o, c
                                          (int)smem);
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "simt smem: %s", cudaGetErrorString(e));
   }
-  k_carve_simt<T><<<grid, 128, smem, st>>>((const T*)q, (const T*)k, (const T*)v, (T*)o, s, kv_idx,
+  k_carve_simt<T><<<grid, 128, smem, st>>>((const T*)q, (const T*)k, (const T*)v, (T*)o, s, bits,
                                            kv_cnt, beta, scale);
   return check_launch("k_carve_simt");
 }
 
 static int launch_simt(const void* q, const void* k, const void* v, void* o, int dtype,
-                       const CarveShape& s, const int32_t* kv_idx, const int32_t* kv_cnt,
+                       const CarveShape& s, const uint32_t* bits, const int32_t* kv_cnt,
                        float beta, cudaStream_t st) {
-  if (dtype == TCB_F32) return launch_simt_t<float>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
-  if (dtype == TCB_BF16) return launch_simt_t<__nv_bfloat16>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
-  return launch_simt_t<__half>(q, k, v, o, s, kv_idx, kv_cnt, beta, st);
+  if (dtype == TCB_F32) return launch_simt_t<float>(q, k, v, o, s, bits, kv_cnt, beta, st);
+  if (dtype == TCB_BF16) return launch_simt_t<__nv_bfloat16>(q, k, v, o, s, bits, kv_cnt, beta, st);
+  return launch_simt_t<__half>(q, k, v, o, s, bits, kv_cnt, beta, st);
 }
 
 // TCB_CARVE_DEBUG bit 0: stream no K/V after the first ring fill; bit 1: skip the softmax
@@ -969,7 +955,7 @@ static int dbg_flags() {
 
 template <int D, int EMU, typename E = __nv_bfloat16>
 static int launch_tc(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
-                     const int32_t* kv_idx, const int32_t* kv_cnt, float beta, int32_t* work,
+                     const uint32_t* bits, const int32_t* kv_cnt, float beta, int32_t* work,
                      cudaStream_t st) {
   CUtensorMap tq, tk, tv;
   const int64_t n_pad = (int64_t)s.M_total * s.m;
@@ -996,7 +982,7 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
   if (grid > total) grid = total;
   const float LOG2E = 1.4426950408889634f;
   const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  tc::k_carve_tc<D, EMU, E><<<grid, tc::NUM_THREADS, smem, st>>>(tq, tk, tv, (E*)o, s, kv_idx,
+  tc::k_carve_tc<D, EMU, E><<<grid, tc::NUM_THREADS, smem, st>>>(tq, tk, tv, (E*)o, s, bits,
                                                          kv_cnt, work, total, scale_log2,
                                                          beta * LOG2E, dbg_flags());
   return check_launch("k_carve_tc");
@@ -1006,29 +992,30 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
 
 
 extern "C" int tcb_carve_fwd_simt(const void* q, const void* k, const void* v, void* o, int dtype,
-                                  int64_t stride_h, int64_t stride_n, const int32_t* kv_idx,
-                                  const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
-                                  int64_t n_valid, int64_t n_cond, float beta, void* stream) {
-  CarveShape s{H, d, m, M_v, M_total, n_valid, n_cond, stride_h, stride_n};
-  int rc = validate(q, k, v, o, dtype, kv_idx, kv_cnt, s);
+                                  int64_t stride_h, int64_t stride_n, const uint32_t* bits,
+                                  int words, const int32_t* kv_cnt, int H, int d, int m, int M_v,
+                                  int M_total, int64_t n_valid, int64_t n_cond, float beta,
+                                  void* stream) {
+  CarveShape s{H, d, m, M_v, M_total, words, n_valid, n_cond, stride_h, stride_n};
+  int rc = validate(q, k, v, o, dtype, bits, kv_cnt, s);
   if (rc) return rc;
-  return launch_simt(q, k, v, o, dtype, s, kv_idx, kv_cnt, beta, as_stream(stream));
+  return launch_simt(q, k, v, o, dtype, s, bits, kv_cnt, beta, as_stream(stream));
 }
 
 extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* o, int dtype,
-                             int64_t stride_h, int64_t stride_n, const int32_t* kv_idx,
+                             int64_t stride_h, int64_t stride_n, const uint32_t* bits, int words,
                              const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
                              int64_t n_valid, int64_t n_cond, float beta, int32_t* work,
                              void* stream) {
-  CarveShape s{H, d, m, M_v, M_total, n_valid, n_cond, stride_h, stride_n};
-  int rc = validate(q, k, v, o, dtype, kv_idx, kv_cnt, s);
+  CarveShape s{H, d, m, M_v, M_total, words, n_valid, n_cond, stride_h, stride_n};
+  int rc = validate(q, k, v, o, dtype, bits, kv_cnt, s);
   if (rc) return rc;
   const bool aligned = ((uintptr_t)q % 16 == 0) && ((uintptr_t)k % 16 == 0) &&
                        ((uintptr_t)v % 16 == 0) && ((uintptr_t)o % 16 == 0) &&
                        (stride_n * 2) % 16 == 0 && (stride_h * 2) % 16 == 0;
   const bool tc_ok = (dtype == TCB_BF16 || dtype == TCB_F16) && m == 128 && (d == 128 || d == 64) &&
                      aligned && work && M_v > 0;
-  if (!tc_ok) return launch_simt(q, k, v, o, dtype, s, kv_idx, kv_cnt, beta, as_stream(stream));
+  if (!tc_ok) return launch_simt(q, k, v, o, dtype, s, bits, kv_cnt, beta, as_stream(stream));
   // pairs (of 8) whose exp2 runs on the FMA pipe instead of MUFU; TCB_CARVE_EMU overrides
   static int emu = -1;
   if (emu < 0) {
@@ -1038,17 +1025,17 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
   }
   cudaStream_t st = as_stream(stream);
   if (dtype == TCB_F16)  // fp16 operands and P (kind::f16 with f16 inputs), f32 accumulation
-    return d == 128 ? launch_tc<128, 0, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st)
-                    : launch_tc<64, 0, __half>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
+    return d == 128 ? launch_tc<128, 0, __half>(q, k, v, o, s, bits, kv_cnt, beta, work, st)
+                    : launch_tc<64, 0, __half>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
   if (d == 128) {
     switch (emu) {
-      case 3: return launch_tc<128, 3>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-      case 4: return launch_tc<128, 4>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-      case 2: return launch_tc<128, 2>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
-      default: return launch_tc<128, 0>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
+      case 3: return launch_tc<128, 3>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
+      case 4: return launch_tc<128, 4>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
+      case 2: return launch_tc<128, 2>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
+      default: return launch_tc<128, 0>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
     }
   }
-  return launch_tc<64, 0>(q, k, v, o, s, kv_idx, kv_cnt, beta, work, st);
+  return launch_tc<64, 0>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
 }
 
 #ifdef TCB_CARVE_TRACE

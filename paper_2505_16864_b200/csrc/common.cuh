@@ -36,6 +36,27 @@ __host__ __device__ __forceinline__ int block_valid(int b, int m, int M_v, int64
   return (int)cnt;
 }
 
+// Ascending walk over the set bits of one packed mask row (32 columns per uint32 word,
+// column j = bit j % 32 of word j / 32): the mask's kv list without a materialised CSR.
+// Every calling thread runs it identically (uniform, L1-resident loads); get(j) returns the
+// j-th set column for non-decreasing j -- kv_idx[j] of the reference's ascending
+// flatnonzero(bits[h, qb]) (attention.py:179).  The caller bounds j by the row's count.
+struct BitWalk {
+  const uint32_t* row;
+  int w, j, b;
+  uint32_t cur;
+  __device__ explicit BitWalk(const uint32_t* r) : row(r), w(-1), j(-1), b(0), cur(0u) {}
+  __device__ __forceinline__ int get(int jj) {
+    while (j < jj) {
+      while (cur == 0u) cur = __ldg(row + ++w);
+      b = w * 32 + __ffs((int)cur) - 1;
+      cur &= cur - 1u;
+      ++j;
+    }
+    return b;
+  }
+};
+
 }  // namespace tcb
 
 #define TCB_CHECK_ARG(cond, code, ...)                  \

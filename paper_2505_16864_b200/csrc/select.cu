@@ -437,40 +437,6 @@ __device__ __forceinline__ double key_value(uint64_t k) {
   return __longlong_as_double((long long)b);
 }
 
-__device__ void emit_row(uint32_t* sbits, int words, int M_total, uint32_t* __restrict__ bits_row,
-                         int32_t* __restrict__ kv_row, int32_t* __restrict__ cnt_out,
-                         int* s_scan) {
-  const int tid = threadIdx.x;
-  for (int w = tid; w < words; w += blockDim.x) bits_row[w] = sbits[w];
-  __syncthreads();
-  if (tid < 32) {  // warp-level exclusive scan of popcounts over the row's words
-    int run = 0;
-    for (int w0 = 0; w0 < words; w0 += 32) {
-      const int w = w0 + tid;
-      const int c = (w < words) ? __popc(sbits[w]) : 0;
-      int incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (tid >= o) incl += y;
-      }
-      if (w < words) s_scan[w] = run + incl - c;
-      run += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (tid == 0) *cnt_out = run;
-  }
-  __syncthreads();
-  for (int w = tid; w < words; w += blockDim.x) {
-    uint32_t x = sbits[w];
-    int pos = s_scan[w];
-    while (x) {
-      const int b = __ffs(x) - 1;
-      x &= x - 1;
-      kv_row[pos++] = w * 32 + b;
-    }
-  }
-}
-
 // The pairwise-sum tree of a row depends only on M_total: built once on the host per launch
 // and passed by value (it used to be built by thread 0 of every CTA while the CTA waited).
 struct PwProg {
@@ -866,80 +832,61 @@ __device__ int warp_sorted_cut(uint64_t* skey, int* scol, int cnt, int np2, doub
   return __shfl_sync(FULL, cut, 0);
 }
 
-// One warp per (head, vision row).  RAW: the row holds scaled pooled scores and is first
-// turned into R in place (max, exp, numpy-pairwise sum, divide; masks.py:132-134).
-// Per-warp smem: keys[M_pad] | hist[256] | sbits[words_pad] | leaf[nslots] |
-//                (SORT) skey[max(np2, 544)] | scol[max(np2, 544)]
-// MODE 0: complete kernel (shared memory for a full-row sort).  MODE 1: slim main pass for
+// ---- the row program ----------------------------------------------------------------
+// One warp selects one (head, vision row).  `vals` holds the row in shared memory: float64
+// probabilities (RAW = false), or scaled pooled scores (RAW = true) that are first turned
+// into R in place (max, exp, numpy-pairwise sum, divide; masks.py:132-134) and written back
+// to Rr when Rr != nullptr.  FASTS (RAW, p == 0 only): the selection is taken on the scores
+// themselves -- R = exp(S - max) / sum is monotone in S, so the top-n_floor set of R is the
+// top-n_floor set of S -- unless the set's boundary is a near tie (|S_in - S_out| within
+// 1e-12 of the exp argument, where exp / divide rounding could merge or swap the two values)
+// or lies in exp's underflow range; such rows are marked kv_cnt = -1 for the exact pass.
+// MODE 0: complete program (shared memory for a full-row sort).  MODE 1: slim main pass of
 // the cutoff path -- staging for the register sort only; a row whose cut cannot be decided
-// in the top-512 window (p near the row total, or negative values) is marked kv_cnt = -1
-// and left to MODE 2, which re-runs only the marked rows with the full-sort memory (R has
-// already been turned into probabilities by MODE 1, so MODE 2 runs with RAW = false).
-template <bool RAW, bool SORT, int MODE = 0>
-__global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R, int64_t n_rows,
-                                                          int M_v, int M_total, int np2,
-                                                          const uint32_t* __restrict__ adja,
-                                                          int words, int n_floor, double p,
-                                                          int with_union,
-                                                          uint32_t* __restrict__ bits,
-                                                          int32_t* __restrict__ kv_idx,
-                                                          int32_t* __restrict__ kv_cnt,
-                                                          int per_warp_bytes, int nslots,
-                                                          const __grid_constant__ PwProg prog) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int leaf_off[SEL_MAX_LEAVES], leaf_len[SEL_MAX_LEAVES];
-  __shared__ int2 fold_ops[SEL_MAX_LEAVES];
-  const int s_nl = prog.nl, s_nops = prog.nops;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (RAW) {
-    for (int i = threadIdx.x; i < s_nl; i += blockDim.x) {
-      leaf_off[i] = prog.off[i];
-      leaf_len[i] = prog.len[i];
-    }
-    for (int i = threadIdx.x; i < s_nops; i += blockDim.x) fold_ops[i] = prog.ops[i];
-    __syncthreads();
-  }
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  if (row >= n_rows) return;
-  if (MODE == 2 && kv_cnt[row] != -1) return;
-  unsigned char* base = smem + (size_t)warp * per_warp_bytes;
-  const int M_pad = (M_total + 1) & ~1;
-  uint64_t* keys = reinterpret_cast<uint64_t*>(base);
-  double* vals = reinterpret_cast<double*>(base);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(keys + M_pad);
-  uint32_t* sbits = hist + 256;
-  const int words_pad = (words + 1) & ~1;
-  double* leaf = reinterpret_cast<double*>(sbits + words_pad);
-  uint64_t* skey = reinterpret_cast<uint64_t*>(leaf + nslots);
-  int* scol = reinterpret_cast<int*>(skey + (MODE == 1 ? 544 : (np2 > 544 ? np2 : 544)));
-  const int i = (int)(row % M_v);
-  double* Rr = R + row * M_total;
+// in the top-512 window (p near the row total, or negative values) is marked kv_cnt = -1.
+// MODE 2: the exact pass over the marked rows only.
+// Output: the packed row (union with the condition columns and the adjacency row when
+// with_union) and its popcount kv_cnt -- the carve kernels walk the packed bits, so no CSR.
+struct RowScratch {
+  uint32_t* hist;  // 256
+  uint32_t* sbits; // words_pad
+  double* leaf;    // nslots
+  uint64_t* skey;  // SORT: max(np2, 544) (MODE 1: 544)
+  int* scol;
+};
 
-  // ---- load (+ softmax) ----
+template <bool RAW, bool SORT, int MODE, bool FASTS>
+__device__ void select_row(double* vals, double* __restrict__ Rr, const RowScratch& sc,
+                           int64_t row, int i, int M_v, int M_total, int words, int n_floor,
+                           double p, int with_union, const uint32_t* __restrict__ adja,
+                           uint32_t* __restrict__ bits, int32_t* __restrict__ kv_cnt, int nl,
+                           int nops, const int* leaf_off, const int* leaf_len,
+                           const int2* fold_ops) {
+  const int lane = threadIdx.x & 31;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(vals);  // keys overwrite vals in place
+  uint32_t* hist = sc.hist;
+  uint32_t* sbits = sc.sbits;
+  double* leaf = sc.leaf;
+  uint64_t* skey = sc.skey;
+  int* scol = sc.scol;
   double mx = -INFINITY;
-  for (int j = lane; j < M_total; j += 32) {
-    const double v = Rr[j];
-    vals[j] = v;
-    mx = fmax(mx, v);
-  }
-  if (RAW) {
+  for (int j = lane; j < M_total; j += 32) mx = fmax(mx, vals[j]);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+  if (RAW && !FASTS) {
     for (int j = lane; j < M_total; j += 32) vals[j] = exp(vals[j] - mx);
     __syncwarp();
-    const int nl = s_nl;
     for (int l = lane; l < nl; l += 32) leaf[l] = pw_leaf(vals + leaf_off[l], leaf_len[l]);
     __syncwarp();
     double tot = 0.0;
     if (lane == 0) {
-      const int nops = s_nops;
       for (int q = 0; q < nops; ++q) leaf[nl + q] = leaf[fold_ops[q].x] + leaf[fold_ops[q].y];
       tot = leaf[nops ? nl + nops - 1 : 0];
     }
     tot = __shfl_sync(FULL, tot, 0);
     for (int j = lane; j < M_total; j += 32) {
       const double v = vals[j] / tot;
-      Rr[j] = v;
+      if (Rr) Rr[j] = v;
       vals[j] = v;
     }
   }
@@ -958,25 +905,19 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
 
   // ---- n_cut = 1 + #(sorted sequential prefix <= p)  (masks.py:150-153) ----
   int n_cut;
-  int reg_keep = 0;
   bool reg_bits = false;  // the register path already wrote the top-keep set
-  if (!neg && p == 0.0) {
+  if (FASTS) {
+    n_cut = 1;  // every softmax row has a positive maximum
+  } else if (!neg && p == 0.0) {
     n_cut = pos ? 1 : M_total + 1;  // prefix_0 = row max
   } else if (SORT) {
-    // Bound the crossing rank without a value-weighted histogram (fp64 shared atomics are
-    // CAS loops; they were half of this path's time): grow T (64, 128, ...) until the
-    // (any-order) sum of the top-T values exceeds p by more than the largest possible
-    // summation-order rounding difference, so the exact sequential prefix (np.cumsum
-    // order) crosses p within the top T.  Only those T are then sorted and scanned.
     // The register path sorts the top min(512, M_total) (one radix select) and scans them
     // exactly; it decides n_cut whenever the prefix crosses p inside that window (or the
     // window is the whole row).  Otherwise (p close to the row total, or negative values
-    // from an external R) the smem path below sorts as much as needed.
+    // from an external R) the shared-memory paths below sort as much as needed.
     const int k_ub = min(512, M_total);
     bool done = false;
-    if (MODE != 2 && !neg && k_ub <= 512) {
-      // common case: the crossing lies in the top <= 512 -> register sort + shuffle scan
-      // (MODE 2 only sees the rows where this already failed)
+    if (MODE != 2 && !neg) {
       const RadixState t = warp_radix(keys, M_total, k_ub, hist);
       uint64_t* stage_k = skey;  // staging with one pad slot per 16 (conflict-free lane reads)
       int* stage_c = scol;
@@ -992,31 +933,30 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
       for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
       __syncwarp();
       // the (any-order) window total must exceed p by more than any summation-order
-      // rounding for the exact prefix to cross inside the window; else go straight to the
-      // full sort
+      // rounding for the exact prefix to cross inside the window
       const bool window_ok = k_ub == M_total || part > p + 1e-12 * (1.0 + part);
       if (window_ok) {
-      KC x[16];
+        KC x[16];
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        x[r].k = stage_k[lane * 17 + r];
-        x[r].c = stage_c[lane * 17 + r];
-      }
-      reg_sort_window(x, k_ub, M_total);
-      bool crossed;
-      __syncwarp();
-      n_cut = par_cut<16>([&](int r) { return x[r].k; }, k_ub, p, &crossed);
-      if (n_cut < 0) n_cut = reg_sorted_cut(x, stage_k, k_ub, p, &crossed);
-      if (crossed || k_ub == M_total) {
-        done = true;
-        reg_keep = max(n_cut, n_floor);
-        if (reg_keep <= k_ub) {  // the top-keep set is the first keep sorted slots
-#pragma unroll
-          for (int r = 0; r < 16; ++r)
-            if (lane * 16 + r < reg_keep) atomicOr(sbits + (x[r].c >> 5), 1u << (x[r].c & 31));
-          reg_bits = true;
+        for (int r = 0; r < 16; ++r) {
+          x[r].k = stage_k[lane * 17 + r];
+          x[r].c = stage_c[lane * 17 + r];
         }
-      }
+        reg_sort_window(x, k_ub, M_total);
+        bool crossed;
+        __syncwarp();
+        n_cut = par_cut<16>([&](int r) { return x[r].k; }, k_ub, p, &crossed);
+        if (n_cut < 0) n_cut = reg_sorted_cut(x, stage_k, k_ub, p, &crossed);
+        if (crossed || k_ub == M_total) {
+          done = true;
+          const int reg_keep = max(n_cut, n_floor);
+          if (reg_keep <= k_ub) {  // the top-keep set is the first keep sorted slots
+#pragma unroll
+            for (int r = 0; r < 16; ++r)
+              if (lane * 16 + r < reg_keep) atomicOr(sbits + (x[r].c >> 5), 1u << (x[r].c & 31));
+            reg_bits = true;
+          }
+        }
       }
       __syncwarp();
     }
@@ -1026,8 +966,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
     }
     if (!done && !neg && M_total <= 1024) {
       // whole row in registers (32 keys per lane), keys only; then the exact sequential
-      // scan by lane 0 over the sorted keys staged with one pad slot per 32 (the staging
-      // may run 32 slots past skey's np2 into scol, which this path does not use)
+      // scan by lane 0 over the sorted keys staged with one pad slot per 32
       uint64_t y[32];
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
@@ -1068,68 +1007,254 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
   int keep = max(n_cut, n_floor);
   keep = min(keep, M_total);
 
-  // ---- top-n_keep set -> bits, union, CSR ----
+  // ---- top-n_keep set -> bits ----
   if (!reg_bits) {
     const RadixState t = warp_radix(keys, M_total, keep, hist);
-    warp_topk_visit(keys, M_total, t,
-                    [&](int j, int) { atomicOr(sbits + (j >> 5), 1u << (j & 31)); });
+    if (FASTS) {
+      // boundary check: smallest selected vs largest unselected score
+      double vin = INFINITY, vout = -INFINITY;
+      int eq_base = 0;
+      for (int j0 = 0; j0 < M_total; j0 += 32) {
+        const int j = j0 + lane;
+        uint64_t km = ~0ull;
+        if (j < M_total) km = keys[j] & t.mask;
+        const bool eq = (j < M_total) && km == t.prefix;
+        const unsigned eqb = __ballot_sync(FULL, eq);
+        const int eq_rank = eq_base + __popc(eqb & ((1u << lane) - 1u));
+        const bool sel = (j < M_total) && (km < t.prefix || (eq && eq_rank < t.remaining));
+        if (j < M_total) {
+          const double v = key_value(keys[j]);
+          if (sel) {
+            vin = fmin(vin, v);
+            atomicOr(sbits + (j >> 5), 1u << (j & 31));
+          } else {
+            vout = fmax(vout, v);
+          }
+        }
+        eq_base += __popc(eqb);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        vin = fmin(vin, __shfl_xor_sync(FULL, vin, o));
+        vout = fmax(vout, __shfl_xor_sync(FULL, vout, o));
+      }
+      const double scale = fmax(1.0, fmax(fabs(vin - mx), fabs(vout - mx)));
+      const bool exact = vin - mx > -700.0 && (vout == -INFINITY || vin - vout > 1e-12 * scale);
+      if (!exact) {  // leave the row to the exact pass (MODE 2, softmax on)
+        if (lane == 0) kv_cnt[row] = -1;
+        return;
+      }
+    } else {
+      warp_topk_visit(keys, M_total, t,
+                      [&](int j, int) { atomicOr(sbits + (j >> 5), 1u << (j & 31)); });
+    }
   }
   __syncwarp();
   uint32_t* brow = bits + row * words;
-  int32_t* krow = kv_idx + row * M_total;
   int run = 0;
-  for (int w0 = 0; w0 < words; w0 += 32) {
-    const int w = w0 + lane;
-    uint32_t x = 0;
-    if (w < words) {
-      x = sbits[w];
-      if (with_union) {
-        if (adja) x |= adja[(int64_t)i * words + w];
-        const int lo = w * 32;  // condition columns j >= M_v (masks.py:173)
+  for (int w = lane; w < words; w += 32) {
+    uint32_t x = sbits[w];
+    if (with_union) {
+      if (adja) x |= __ldg(adja + (int64_t)i * words + w);
+      const int lo = w * 32;  // condition columns j >= M_v (masks.py:173)
+      if (lo + 32 <= M_total && lo >= M_v) {
+        x = ~0u;
+      } else {
         for (int bb = 0; bb < 32; ++bb) {
           const int j = lo + bb;
           if (j >= M_v && j < M_total) x |= 1u << bb;
         }
       }
-      brow[w] = x;
     }
-    const int c = __popc(x);
-    int incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
-    }
-    int pos_ = run + incl - c;
-    while (x) {
-      const int b = __ffs(x) - 1;
-      x &= x - 1;
-      krow[pos_++] = w * 32 + b;
-    }
-    run += __shfl_sync(FULL, incl, 31);
+    brow[w] = x;
+    run += __popc(x);
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) run += __shfl_xor_sync(FULL, run, o);
   if (lane == 0) kv_cnt[row] = run;
+}
+
+// Per-warp shared-memory carve-up shared by both select kernels.
+__device__ __forceinline__ RowScratch carve_scratch(unsigned char* base, int words, int nslots,
+                                                    int sortn) {
+  RowScratch sc;
+  sc.hist = reinterpret_cast<uint32_t*>(base);
+  sc.sbits = sc.hist + 256;
+  const int words_pad = (words + 1) & ~1;
+  sc.leaf = reinterpret_cast<double*>(sc.sbits + words_pad);
+  sc.skey = reinterpret_cast<uint64_t*>(sc.leaf + nslots);
+  sc.scol = reinterpret_cast<int*>(sc.skey + sortn);
+  return sc;
+}
+
+__device__ __forceinline__ void load_prog(const PwProg& prog, int* leaf_off, int* leaf_len,
+                                          int2* fold_ops) {
+  for (int i = threadIdx.x; i < prog.nl; i += blockDim.x) {
+    leaf_off[i] = prog.off[i];
+    leaf_len[i] = prog.len[i];
+  }
+  for (int i = threadIdx.x; i < prog.nops; i += blockDim.x) fold_ops[i] = prog.ops[i];
+}
+
+// One warp per (head, vision row) over a row-major R / score tensor in global memory.
+// Per-warp smem: vals[M_pad] | scratch (hist, sbits, leaves, sort buffers).
+template <bool RAW, bool SORT, int MODE = 0>
+__global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R, int64_t n_rows,
+                                                          int M_v, int M_total, int np2,
+                                                          const uint32_t* __restrict__ adja,
+                                                          int words, int n_floor, double p,
+                                                          int with_union,
+                                                          uint32_t* __restrict__ bits,
+                                                          int32_t* __restrict__ kv_cnt,
+                                                          int per_warp_bytes, int nslots,
+                                                          const __grid_constant__ PwProg prog) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int leaf_off[SEL_MAX_LEAVES], leaf_len[SEL_MAX_LEAVES];
+  __shared__ int2 fold_ops[SEL_MAX_LEAVES];
+  if (RAW) {
+    load_prog(prog, leaf_off, leaf_len, fold_ops);
+    __syncthreads();
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (row >= n_rows) return;
+  if (MODE == 2 && kv_cnt[row] != -1) return;
+  unsigned char* base = smem + (size_t)warp * per_warp_bytes;
+  const int M_pad = (M_total + 1) & ~1;
+  double* vals = reinterpret_cast<double*>(base);
+  const RowScratch sc = carve_scratch(base + (size_t)M_pad * 8, words, nslots,
+                                      MODE == 1 ? 544 : (np2 > 544 ? np2 : 544));
+  double* Rr = R + row * M_total;
+  for (int j = lane; j < M_total; j += 32) vals[j] = Rr[j];
+  __syncwarp();
+  // MODE 2 runs after MODE 1 turned R into probabilities in place: no softmax again
+  select_row<RAW && MODE != 2, SORT, MODE, false>(
+      vals, RAW ? Rr : nullptr, sc, row, (int)(row % M_v), M_v, M_total, words, n_floor, p,
+      with_union, adja, bits, kv_cnt, prog.nl, prog.nops, leaf_off, leaf_len, fold_ops);
+}
+
+// ---- fused scores + selection (no R in global memory) ------------------------------------
+// CTA = (head h, tile of RT = 8 * RG vision rows).  Phase 1: S[r, j] = pq[h, r] . pk[h, j] /
+// sqrt(d) for the tile's rows and every column j < M_total on the FP64 tensor core
+// (DMMA 8x8x4, the same product and scaling as k_scores_dmma / masks.py:130-131) into shared
+// memory; each warp owns 4 column tiles at a time (4 independent accumulator chains), pq
+// fragments stay in registers, pk fragments come from L1/L2.  Phase 2: the warps select the
+// tile's rows from shared memory (select_row; FASTS when p == 0).  MODE 2 re-runs only CTAs
+// holding a row marked -1 by MODE 1 / FASTS, recomputing their scores.
+template <int RG, int DK>
+__device__ __forceinline__ void dmma_tile_scores(const double* __restrict__ pqh,
+                                                 const double* __restrict__ pkh, int r0,
+                                                 int rows_valid, int M_total, double sqrt_d,
+                                                 double* S, int ldS) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  constexpr int KS = DK / 4;
+  const int n_ct = (M_total + 7) >> 3;  // 8-column tiles
+  for (int g = 0; g < RG; ++g) {
+    const int rr = min(g * 8 + fr, rows_valid - 1);  // clamp: rows beyond the tile are dropped
+    double a[KS];
+#pragma unroll
+    for (int s = 0; s < KS; ++s) a[s] = __ldg(pqh + (int64_t)(r0 + rr) * DK + 4 * s + fk);
+    for (int c0 = warp * 4; c0 < n_ct; c0 += nw * 4) {
+      double acc[4][2];
+      const double* bp[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc[u][0] = acc[u][1] = 0.0;
+        const int col = min((c0 + u) * 8 + fr, M_total - 1);
+        bp[u] = pkh + (int64_t)col * DK + fk;
+      }
+#pragma unroll
+      for (int s = 0; s < KS; ++s) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma_8x8x4(acc[u][0], acc[u][1], a[s], __ldg(bp[u] + 4 * s));
+      }
+      const int orow = g * 8 + fr;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = (c0 + u) * 8 + 2 * fk + e;
+          if (c0 + u < n_ct && col < M_total) S[(size_t)orow * ldS + col] = acc[u][e] / sqrt_d;
+        }
+    }
+  }
+}
+
+template <int RG, int DK, bool SORT, int MODE, bool FASTS>
+__global__ void __launch_bounds__(SW_WARPS * 32) k_select_fused(
+    const double* __restrict__ pq, int pq_blocks, const double* __restrict__ pk, int n_heads,
+    int M_v, int M_total, int np2, const uint32_t* __restrict__ adja, int words, int n_floor, double p,
+    int with_union, uint32_t* __restrict__ bits, int32_t* __restrict__ kv_cnt,
+    int per_warp_bytes, int nslots, double sqrt_d, const __grid_constant__ PwProg prog) {
+  constexpr int RT = 8 * RG;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int leaf_off[SEL_MAX_LEAVES], leaf_len[SEL_MAX_LEAVES];
+  __shared__ int2 fold_ops[SEL_MAX_LEAVES];
+  __shared__ int s_any;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (!FASTS) {
+    load_prog(prog, leaf_off, leaf_len, fold_ops);
+    __syncthreads();
+  }
+  const int M_pad = (M_total + 1) & ~1;
+  double* S = reinterpret_cast<double*>(smem);
+  unsigned char* base = smem + (size_t)RT * M_pad * 8 + (size_t)warp * per_warp_bytes;
+  const RowScratch sc = carve_scratch(base, words, nslots,
+                                      MODE == 1 ? 544 : (np2 > 544 ? np2 : 544));
+  const int tiles_per_head = (M_v + RT - 1) / RT;
+  const int n_tiles = tiles_per_head * n_heads;
+  // grid-stride over (head, row tile), head-major: concurrently resident tiles share pk[h]
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int h = tile / tiles_per_head;
+    const int r0 = (tile - h * tiles_per_head) * RT;
+    const int rows_valid = min(RT, M_v - r0);
+    const int64_t row0 = (int64_t)h * M_v + r0;
+    if (MODE == 2) {  // only tiles holding a row the first pass left undecided (-1)
+      __syncthreads();
+      if (threadIdx.x == 0) s_any = 0;
+      __syncthreads();
+      if (threadIdx.x < rows_valid && kv_cnt[row0 + threadIdx.x] == -1) s_any = 1;
+      __syncthreads();
+      if (!s_any) continue;
+    }
+    __syncthreads();  // the previous tile's rows are done with S
+    dmma_tile_scores<RG, DK>(pq + (int64_t)h * pq_blocks * DK, pk + (int64_t)h * M_total * DK,
+                             r0, rows_valid, M_total, sqrt_d, S, M_pad);
+    __syncthreads();
+    for (int r = warp; r < rows_valid; r += nw) {
+      const int64_t row = row0 + r;
+      if (MODE == 2 && kv_cnt[row] != -1) continue;
+      select_row<true, SORT, MODE, FASTS>(S + (size_t)r * M_pad, nullptr, sc, row, r0 + r, M_v,
+                                          M_total, words, n_floor, p, with_union, adja, bits,
+                                          kv_cnt, prog.nl, prog.nops, leaf_off, leaf_len,
+                                          fold_ops);
+      __syncwarp();
+    }
+  }
 }
 
 __global__ void __launch_bounds__(128) k_mask_pack(const uint8_t* __restrict__ dense, int M_total,
                                                    int words, uint32_t* __restrict__ bits,
-                                                   int32_t* __restrict__ kv_idx,
                                                    int32_t* __restrict__ kv_cnt) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* sbits = reinterpret_cast<uint32_t*>(smem);
-  int* s_scan = reinterpret_cast<int*>(sbits + words);
+  __shared__ int s_cnt;
   const int64_t row = blockIdx.x;
   const uint8_t* d = dense + row * M_total;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  int cnt = 0;
   for (int w = threadIdx.x; w < words; w += blockDim.x) {
     uint32_t x = 0;
     for (int bb = 0; bb < 32; ++bb) {
-      int j = w * 32 + bb;
+      const int j = w * 32 + bb;
       if (j < M_total && d[j]) x |= 1u << bb;
     }
-    sbits[w] = x;
+    bits[row * words + w] = x;
+    cnt += __popc(x);
   }
+  atomicAdd(&s_cnt, cnt);
   __syncthreads();
-  emit_row(sbits, words, M_total, bits + row * words, kv_idx + row * M_total, kv_cnt + row, s_scan);
+  if (threadIdx.x == 0) kv_cnt[row] = s_cnt;
 }
 
 __global__ void k_mask_unpack(const uint32_t* __restrict__ bits, int64_t rows, int M_total,
@@ -1228,81 +1353,185 @@ extern "C" int tcb_block_relevance(const double* pq, int pq_blocks, const double
   return check_launch("k_row_softmax");
 }
 
-static int launch_select(double* R, bool raw, int H, int M_v, int M_total, const uint32_t* adja,
-                         int words, int n_floor, double p, int with_union, uint32_t* bits,
-                         int32_t* kv_idx, int32_t* kv_cnt, cudaStream_t s) {
-  TCB_CHECK_ARG(R && bits && kv_idx && kv_cnt, TCB_ESHAPE, "null tensor");
-  TCB_CHECK_ARG(H >= 1 && M_v >= 0 && M_total >= 1, TCB_ESHAPE, "bad select shape");
+struct SelPlan {
+  int nslots, np2, words_pad, M_pad;
+  PwProg prog;
+};
+
+static SelPlan plan_select(int M_total, int words) {
+  SelPlan pl;
+  // per-warp leaf slots: nl leaves + (nl - 1) folds, nl <= 8192 / 64 = SEL_MAX_LEAVES
+  pl.prog.nl = pw_leaves(M_total, pl.prog.off, pl.prog.len);
+  pl.prog.nops = pw_program(M_total, pl.prog.nl, pl.prog.ops);
+  pl.nslots = (2 * pl.prog.nl + 1) & ~1;
+  pl.np2 = 2;
+  while (pl.np2 < M_total) pl.np2 <<= 1;
+  pl.M_pad = (M_total + 1) & ~1;
+  pl.words_pad = (words + 1) & ~1;
+  return pl;
+}
+
+// scratch bytes per warp (without the row values): hist | sbits | leaves | sort buffers
+static size_t scratch_bytes(const SelPlan& pl, int sortn) {
+  const size_t b = 256 * 4 + (size_t)pl.words_pad * 4 + (size_t)pl.nslots * 8 + (size_t)sortn * 12;
+  return (b + 15) & ~size_t(15);
+}
+
+constexpr size_t SMEM_CAP = 232448 - 8192;  // opt-in limit minus the static leaf tables
+
+// n_rows rows of R (row r uses adjacency row r % M_v; chunk callers offset the pointers)
+static int launch_select(double* R, bool raw, int64_t n_rows, int M_v, int M_total,
+                         const uint32_t* adja, int words, int n_floor, double p, int with_union,
+                         uint32_t* bits, int32_t* kv_cnt, cudaStream_t s) {
+  TCB_CHECK_ARG(R && bits && kv_cnt, TCB_ESHAPE, "null tensor");
+  TCB_CHECK_ARG(n_rows >= 0 && M_v >= 0 && M_total >= 1, TCB_ESHAPE, "bad select shape");
   TCB_CHECK_ARG(words >= ceil_div(M_total, 32), TCB_ESHAPE, "words too small");
   TCB_CHECK_ARG(M_total <= 8192, TCB_ESIZE, "M_total %d > 8192 unsupported", M_total);
-  // per-warp leaf slots: nl leaves + (nl - 1) folds, nl <= 8192 / 64 = SEL_MAX_LEAVES
-  int nl = 0;
-  {
-    int st[64], sp = 0;
-    st[sp++] = M_total;
-    while (sp) {
-      const int l = st[--sp];
-      if (l <= 128) { ++nl; continue; }
-      int n2 = l / 2;
-      n2 -= n2 % 8;
-      st[sp++] = l - n2;
-      st[sp++] = n2;
-    }
-  }
-  const int nslots = (2 * nl + 1) & ~1;
-  PwProg prog;
-  prog.nl = pw_leaves(M_total, prog.off, prog.len);
-  prog.nops = pw_program(M_total, prog.nl, prog.ops);
   TCB_CHECK_ARG(n_floor >= 1, TCB_EDOMAIN, "n_floor must be >= 1");
-  const int64_t n_rows = (int64_t)H * M_v;
+  const SelPlan pl = plan_select(M_total, words);
   if (n_rows == 0) return TCB_OK;
   const bool sort = !raw || p > 0.0;
-  int np2 = 2;
-  while (np2 < M_total) np2 <<= 1;
-  const int M_pad = (M_total + 1) & ~1, words_pad = (words + 1) & ~1;
-  size_t per_warp = (size_t)M_pad * 8 + 256 * 4 + (size_t)words_pad * 4 + (size_t)nslots * 8;
-  // (np2 >= 544: the register-sort path stages 512 slots + one pad per 16 in skey/scol)
-  if (sort) per_warp += (size_t)(np2 > 544 ? np2 : 544) * 12;
-  per_warp = (per_warp + 15) & ~size_t(15);
+  const int full_sort = pl.np2 > 544 ? pl.np2 : 544;
   // rows (warps) per CTA: SW_WARPS while their shared memory fits, fewer for long rows
   // (M_total = 8192 with the sort buffers needs 163 KB for one warp)
-  constexpr size_t SMEM_CAP = 232448 - 8192;  // opt-in limit minus the static leaf tables
-  auto go = [&](auto kern, size_t pw) -> int {
+  auto go = [&](auto kern, int sortn) -> int {
+    const size_t pw = (size_t)pl.M_pad * 8 + scratch_bytes(pl, sortn);
     const int wpc = (int)std::min<size_t>(SW_WARPS, SMEM_CAP / pw);
     if (wpc < 1) return set_error(TCB_ESIZE, "k_select: %zu B of shared memory per row", pw);
     const size_t sm = pw * wpc;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "k_select smem: %s", cudaGetErrorString(e));
     kern<<<(unsigned)ceil_div(n_rows, wpc), wpc * 32, sm, s>>>(
-        R, n_rows, M_v, M_total, np2, adja, words, n_floor, p, with_union, bits, kv_idx, kv_cnt,
-        (int)pw, nslots, prog);
+        R, n_rows, M_v, M_total, pl.np2, adja, words, n_floor, p, with_union, bits, kv_cnt,
+        (int)pw, pl.nslots, pl.prog);
     return check_launch("k_select");
   };
-  if (raw && !sort) return go(k_select<true, false>, per_warp);
+  if (raw && !sort) return go(k_select<true, false>, 0);
   // cutoff path: slim pass (register sort of the top-512 window, ~35 % less shared memory
   // per warp -> 1.5x the resident warps), then the full-sort pass over the rows it left
-  size_t slim = (size_t)M_pad * 8 + 256 * 4 + (size_t)words_pad * 4 + (size_t)nslots * 8 + 544 * 12;
-  slim = (slim + 15) & ~size_t(15);
-  int rc = raw ? go(k_select<true, true, 1>, slim) : go(k_select<false, true, 1>, slim);
+  int rc = raw ? go(k_select<true, true, 1>, 544) : go(k_select<false, true, 1>, 544);
   if (rc) return rc;
-  return go(k_select<false, true, 2>, per_warp);
+  return go(k_select<false, true, 2>, full_sort);
+}
+
+// Whether the fused kernel covers (M_total, d, p): 8-row score tile + per-warp scratch fit.
+static bool fused_fits(int M_total, int d, int words, double p) {
+  if (d != 64 && d != 128) return false;
+  const SelPlan pl = plan_select(M_total, words);
+  const int full_sort = pl.np2 > 544 ? pl.np2 : 544;
+  return (size_t)8 * pl.M_pad * 8 + scratch_bytes(pl, p > 0.0 ? full_sort : 0) * SW_WARPS <= SMEM_CAP;
+}
+
+// Fused scores + selection: returns -1 (nothing launched) when the shape is not covered
+// (d not in {64, 128}, or the 8-row score tile plus scratch exceeds shared memory).
+template <int DK>
+static int launch_fused_dk(const double* pq, int pq_blocks, const double* pk, int H, int M_v,
+                           int M_total, const uint32_t* adja, int words, int n_floor, double p,
+                           int with_union, uint32_t* bits, int32_t* kv_cnt, cudaStream_t s) {
+  constexpr int RG = 1, RT = 8 * RG;
+  const SelPlan pl = plan_select(M_total, words);
+  const int full_sort = pl.np2 > 544 ? pl.np2 : 544;
+  const size_t tile = (size_t)RT * pl.M_pad * 8;
+  const int sort1 = p > 0.0 ? 544 : 0, sort2 = p > 0.0 ? full_sort : 0;
+  const size_t pw1 = scratch_bytes(pl, sort1), pw2 = scratch_bytes(pl, sort2);
+  if (tile + pw2 * SW_WARPS > SMEM_CAP) return -1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int n_tiles = H * (int)ceil_div(M_v, RT);
+  const double sqrt_d = sqrt((double)DK);
+  auto go = [&](auto kern, size_t pw, int grid) -> int {
+    const size_t sm = tile + pw * SW_WARPS;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return set_error(TCB_ECUDA, "k_select_fused smem: %s", cudaGetErrorString(e));
+    kern<<<(unsigned)grid, SW_WARPS * 32, sm, s>>>(pq, pq_blocks, pk, H, M_v, M_total, pl.np2, adja,
+                                                   words, n_floor, p, with_union, bits, kv_cnt,
+                                                   (int)pw, pl.nslots, sqrt_d, pl.prog);
+    return check_launch("k_select_fused");
+  };
+  // pass 2 (rows pass 1 left undecided, usually none) runs grid-stride on a small grid
+  const int grid2 = std::min(n_tiles, 2 * sms);
+  int rc;
+  if (p == 0.0) {
+    rc = go(k_select_fused<RG, DK, false, 1, true>, pw1, n_tiles);
+    if (rc) return rc;
+    return go(k_select_fused<RG, DK, false, 2, false>, pw2, grid2);
+  }
+  rc = go(k_select_fused<RG, DK, true, 1, false>, pw1, n_tiles);
+  if (rc) return rc;
+  return go(k_select_fused<RG, DK, true, 2, false>, pw2, grid2);
 }
 
 extern "C" int tcb_block_select(const double* R, int H, int M_v, int M_total,
                                 const uint32_t* adja, int words, int n_floor, double p,
-                                int with_union, uint32_t* bits, int32_t* kv_idx, int32_t* kv_cnt,
-                                void* stream) {
+                                int with_union, uint32_t* bits, int32_t* kv_cnt, void* stream) {
   // R is only read on this path (RAW=false never writes it)
-  return launch_select(const_cast<double*>(R), false, H, M_v, M_total, adja, words, n_floor, p,
-                       with_union, bits, kv_idx, kv_cnt, as_stream(stream));
+  TCB_CHECK_ARG(H >= 1, TCB_ESHAPE, "bad select shape");
+  return launch_select(const_cast<double*>(R), false, (int64_t)H * M_v, M_v, M_total, adja, words,
+                       n_floor, p, with_union, bits, kv_cnt, as_stream(stream));
 }
 
 extern "C" int tcb_block_select_scores(double* S, int H, int M_v, int M_total,
                                        const uint32_t* adja, int words, int n_floor, double p,
-                                       int with_union, uint32_t* bits, int32_t* kv_idx,
-                                       int32_t* kv_cnt, void* stream) {
-  return launch_select(S, true, H, M_v, M_total, adja, words, n_floor, p, with_union, bits, kv_idx,
-                       kv_cnt, as_stream(stream));
+                                       int with_union, uint32_t* bits, int32_t* kv_cnt,
+                                       void* stream) {
+  TCB_CHECK_ARG(H >= 1, TCB_ESHAPE, "bad select shape");
+  return launch_select(S, true, (int64_t)H * M_v, M_v, M_total, adja, words, n_floor, p, with_union,
+                       bits, kv_cnt, as_stream(stream));
+}
+
+// Scratch doubles tcb_block_mask_fused needs for a shape (0: the fused kernel covers it).
+extern "C" int64_t tcb_block_mask_fused_scratch(int M_v, int M_total, int d, double p) {
+  const int words = (int)ceil_div(M_total, 32);
+  if (fused_fits(M_total, d, words, p)) return 0;
+  const int64_t cap = (int64_t)32 << 20;  // <= 256 MB of float64 scores per chunk
+  const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(M_v, cap / std::max(1, M_total)));
+  return rows * M_total;
+}
+
+extern "C" int tcb_block_mask_fused(const double* pq, int pq_blocks, const double* pk, int H,
+                                    int M_v, int M_total, int d, const uint32_t* adja, int words,
+                                    int n_floor, double p, uint32_t* bits, int32_t* kv_cnt,
+                                    double* scratch, int64_t scratch_elems, void* stream) {
+  TCB_CHECK_ARG(pq && pk && bits && kv_cnt, TCB_ESHAPE, "null tensor");
+  TCB_CHECK_ARG(H >= 1 && M_v >= 0 && M_total >= M_v && M_total >= 1 && d >= 1 &&
+                    M_v <= pq_blocks,
+                TCB_ESHAPE, "bad mask shape");
+  TCB_CHECK_ARG(words >= ceil_div(M_total, 32), TCB_ESHAPE, "words too small");
+  TCB_CHECK_ARG(M_total <= 8192, TCB_ESIZE, "M_total %d > 8192 unsupported", M_total);
+  TCB_CHECK_ARG(n_floor >= 1, TCB_EDOMAIN, "n_floor must be >= 1");
+  TCB_CHECK_ARG(p >= 0.0 && p < 1.0, TCB_EDOMAIN, "p %g outside [0, 1)", p);
+  if ((int64_t)H * M_v == 0) return TCB_OK;
+  cudaStream_t s = as_stream(stream);
+  int rc = -1;
+  if (d == 128)
+    rc = launch_fused_dk<128>(pq, pq_blocks, pk, H, M_v, M_total, adja, words, n_floor, p, 1, bits,
+                              kv_cnt, s);
+  else if (d == 64)
+    rc = launch_fused_dk<64>(pq, pq_blocks, pk, H, M_v, M_total, adja, words, n_floor, p, 1, bits,
+                             kv_cnt, s);
+  if (rc != -1) return rc;
+  // not fused: scores + select through the caller's bounded scratch, one row chunk at a time
+  // (rows_chunk x M_total doubles), so no (H, M_v, M_total) tensor is ever allocated
+  TCB_CHECK_ARG(scratch && scratch_elems >= M_total, TCB_ESIZE,
+                "scratch of %lld doubles < one row of %d", (long long)scratch_elems, M_total);
+  const int rows_chunk = (int)std::min<int64_t>(M_v, scratch_elems / M_total);
+  const int words_row = words;
+  for (int h = 0; h < H; ++h) {
+    for (int r0 = 0; r0 < M_v; r0 += rows_chunk) {
+      const int nr = std::min(rows_chunk, M_v - r0);
+      rc = launch_scores(pq + ((int64_t)h * pq_blocks + r0) * d, nr, pk + (int64_t)h * M_total * d,
+                         1, nr, M_total, d, scratch, s);
+      if (rc) return rc;
+      // rows r0.. of head h: the adjacency rows start at r0 (select_row uses row % M_v)
+      rc = launch_select(scratch, true, nr, M_v, M_total,
+                         adja ? adja + (int64_t)r0 * words_row : nullptr, words_row, n_floor, p, 1,
+                         bits + ((int64_t)h * M_v + r0) * words_row, kv_cnt + (int64_t)h * M_v + r0,
+                         s);
+      if (rc) return rc;
+    }
+  }
+  return TCB_OK;
 }
 
 extern "C" int tcb_block_scores(const double* pq, int pq_blocks, const double* pk, int H, int rows,
@@ -1315,13 +1544,11 @@ extern "C" int tcb_block_scores(const double* pq, int pq_blocks, const double* p
 }
 
 extern "C" int tcb_mask_pack(const uint8_t* dense, int64_t rows, int M_total, int words,
-                             uint32_t* bits, int32_t* kv_idx, int32_t* kv_cnt, void* stream) {
-  TCB_CHECK_ARG(dense && bits && kv_idx && kv_cnt, TCB_ESHAPE, "null tensor");
+                             uint32_t* bits, int32_t* kv_cnt, void* stream) {
+  TCB_CHECK_ARG(dense && bits && kv_cnt, TCB_ESHAPE, "null tensor");
   TCB_CHECK_ARG(words >= ceil_div(M_total, 32), TCB_ESHAPE, "words too small");
   if (rows == 0) return TCB_OK;
-  const size_t smem = (size_t)words * 4 + (size_t)(words + 1) * 4;
-  k_mask_pack<<<(unsigned)rows, 128, smem, as_stream(stream)>>>(dense, M_total, words, bits,
-                                                                kv_idx, kv_cnt);
+  k_mask_pack<<<(unsigned)rows, 128, 0, as_stream(stream)>>>(dense, M_total, words, bits, kv_cnt);
   return check_launch("k_mask_pack");
 }
 

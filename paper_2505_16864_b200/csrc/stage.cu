@@ -69,20 +69,19 @@ __device__ __forceinline__ float philox_normal(uint64_t seed, uint64_t idx) {
 // for every channel of the group.  VEC = channels per thread (4: float4 / 2x double2 loads and
 // stores along C; 1: any C).  Index math is int32 (the host guarantees n_cells * C < 2^31).
 template <typename TI, typename TO, int VEC>
-__global__ void __launch_bounds__(256) k_upsample_renoise(
+__global__ void __launch_bounds__(256, 4) k_upsample_renoise(
     const TI* __restrict__ x, const float* __restrict__ vel, const int32_t* __restrict__ inv,
     const float* __restrict__ eps, TO* __restrict__ out, int st, int sh, int sw, int dt, int dh,
     int dw, int C, float sigma_f, int mode, uint64_t seed, uint64_t offset) {
+  // grid (x: (ow, channel group) of one output row, y: oh, z: ot) -- no per-element index
+  // division beyond the group split, and the t / h taps are uniform across the CTA
   const int groups = C / VEC;
-  const int n = dt * dh * dw * groups;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n) return;
-  const int cell = e / groups;
-  const int c0 = (e - cell * groups) * VEC;
-  const int ow = cell % dw;
-  const int rest = cell / dw;
-  const int oh = rest % dh;
-  const int ot = rest / dh;
+  const int x_ = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x_ >= dw * groups) return;
+  const int ow = x_ / groups;
+  const int c0 = (x_ - ow * groups) * VEC;
+  const int oh = blockIdx.y, ot = blockIdx.z;
+  const int cell = (ot * dh + oh) * dw + ow;
   const Taps tt = axis_taps(ot, st, dt), th = axis_taps(oh, sh, dh), tw = axis_taps(ow, sw, dw);
   // Always two taps per axis: a missing second tap repeats the first index with weight 0,
   // and 0 * x adds an exact zero -- as the reference's dense tensordot rows do.
@@ -181,14 +180,19 @@ static int launch_switch(const TI* x, const float* vel, const int32_t* inv, cons
                 TCB_ESIZE, "latent too large");
   const bool vec = (C % 4 == 0) && ((uintptr_t)x % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
                    (!eps || (uintptr_t)eps % 16 == 0) && (!vel || (uintptr_t)vel % 16 == 0);
-  const int64_t n = (int64_t)dt * dh * dw * (vec ? C / 4 : C);
-  const unsigned grid = (unsigned)ceil_div(n, 256);
+  TCB_CHECK_ARG(dh <= 65535 && dt <= 65535, TCB_ESIZE, "target t/h above 65535");
+  const int64_t row = (int64_t)dw * (vec ? C / 4 : C);
+  const int64_t nblk = ceil_div(row, 256);
+  const int threads = (int)ceil_div(ceil_div(row, nblk), 32) * 32;  // balanced, warp multiple
+  const dim3 grid((unsigned)nblk, (unsigned)dh, (unsigned)dt);
   if (vec)
-    k_upsample_renoise<TI, TO, 4><<<grid, 256, 0, stream>>>(x, vel, inv, eps, out, st, sh, sw, dt, dh,
-                                                           dw, C, (float)sigma, mode, seed, offset);
+    k_upsample_renoise<TI, TO, 4><<<grid, threads, 0, stream>>>(x, vel, inv, eps, out, st, sh, sw, dt,
+                                                               dh, dw, C, (float)sigma, mode, seed,
+                                                               offset);
   else
-    k_upsample_renoise<TI, TO, 1><<<grid, 256, 0, stream>>>(x, vel, inv, eps, out, st, sh, sw, dt, dh,
-                                                           dw, C, (float)sigma, mode, seed, offset);
+    k_upsample_renoise<TI, TO, 1><<<grid, threads, 0, stream>>>(x, vel, inv, eps, out, st, sh, sw, dt,
+                                                               dh, dw, C, (float)sigma, mode, seed,
+                                                               offset);
   return check_launch("k_upsample_renoise");
 }
 

@@ -8,7 +8,7 @@ the sparse flash-attention of head h read only head h.  With host inputs the lay
 therefore runs as a head-chunked pipeline on three CUDA streams --
 
     copy stream   H2D  q/k/v[chunk c+1]
-    compute       pool -> scores -> select -> carve on chunk c      (4 launches)
+    compute       pool -> fused scores/select -> carve on chunk c
     copy stream   D2H  out[chunk c-1]
 
 -- so the PCIe transfers overlap the kernels and each other (PCIe is full duplex).
@@ -24,8 +24,8 @@ import torch
 from . import _dev, _native
 from .attention import AmplifierBias, _workspace
 from .errors import ShapeError
-from .masks import BlockMask, SelectionParams
-from .partition import BlockLayout, StaticMasks, mask_words
+from .masks import BlockMask, SelectionParams, fused_scratch, launch_mask, mask_buffers
+from .partition import BlockLayout, StaticMasks
 
 __all__ = ["carve_layer", "CarveLayerGraph"]
 
@@ -40,22 +40,19 @@ def _copy_streams(dev: torch.device):
     return s
 
 
-def _launch_chunk(q, k, v, o, pq, pk, R, bits, kv_idx, kv_cnt, adja, layout, params, beta, work,
+def _launch_chunk(q, k, v, o, pq, pk, bits, kv_cnt, scratch, adja, layout, params, beta, work,
                   sptr):
-    """pool -> scores -> softmax/select/union -> carve on head-slice views (H_c, N, d)."""
+    """pool -> fused scores/select/union -> carve on head-slice views (H_c, N, d)."""
     Hc, _, d = q.shape
     sh, sn = q.stride(0), q.stride(1)
     Mv, Mt = layout.M_v, layout.M_total
     _native.call("tcb_block_pool", q.data_ptr(), k.data_ptr(), _dev.code_of(q.dtype), sh, sn, Hc, d,
                  layout.m, Mv, Mt, layout.n_valid, layout.n_cond, pq.data_ptr(), pk.data_ptr(), sptr)
-    _native.call("tcb_block_scores", pq.data_ptr(), Mt, pk.data_ptr(), Hc, Mv, Mt, d, R.data_ptr(),
-                 sptr)
-    _native.call("tcb_block_select_scores", R.data_ptr(), Hc, Mv, Mt, _native.ptr(adja),
-                 mask_words(Mt), params.n_floor(Mv), float(params.p), 1, bits.data_ptr(),
-                 kv_idx.data_ptr(), kv_cnt.data_ptr(), sptr)
+    launch_mask(pq, pk, layout, adja, params, bits, kv_cnt, sptr, scratch)
     _native.call("tcb_carve_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
-                 _dev.code_of(q.dtype), sh, sn, kv_idx.data_ptr(), kv_cnt.data_ptr(), Hc, d, layout.m,
-                 Mv, Mt, layout.n_valid, layout.n_cond, float(beta), work.data_ptr(), sptr)
+                 _dev.code_of(q.dtype), sh, sn, bits.data_ptr(), bits.shape[-1], kv_cnt.data_ptr(),
+                 Hc, d, layout.m, Mv, Mt, layout.n_valid, layout.n_cond, float(beta), work.data_ptr(),
+                 sptr)
 
 
 def carve_layer(q, k, v, layout: BlockLayout, statics: StaticMasks, params: SelectionParams,
@@ -73,7 +70,7 @@ def carve_layer(q, k, v, layout: BlockLayout, statics: StaticMasks, params: Sele
         from .attention import AttentionInputs, carve_attention
         from .masks import build_block_mask
 
-        mask, _ = build_block_mask(q, k, layout, statics, params)
+        mask, _ = build_block_mask(q, k, layout, statics, params, need_relevance=False)
         o = carve_attention(AttentionInputs(q=q, k=k, v=v, layout=layout), mask, beta)
         if out is not None:
             out.copy_(o)
@@ -96,16 +93,13 @@ def carve_layer(q, k, v, layout: BlockLayout, statics: StaticMasks, params: Sele
         out = torch.empty((H, N, d), dtype=hq.dtype, pin_memory=True)
     elif tuple(out.shape) != (H, N, d) or out.dtype != hq.dtype or out.is_cuda:
         raise ShapeError("out must be a host tensor of the input shape and dtype")
-    Mv, Mt = layout.M_v, layout.M_total
-    words = mask_words(Mt)
+    Mt = layout.M_total
     dq, dk, dv = (torch.empty((H, N, d), dtype=hq.dtype, device=dev) for _ in range(3))
     do = torch.empty((H, N, d), dtype=hq.dtype, device=dev)
     pq = torch.empty((H, Mt, d), dtype=torch.float64, device=dev)
     pk = torch.empty_like(pq)
-    R = torch.empty((H, Mv, Mt), dtype=torch.float64, device=dev)
-    bits = torch.empty((H, Mv, words), dtype=torch.int32, device=dev)
-    kv_idx = torch.empty((H, Mv, Mt), dtype=torch.int32, device=dev)
-    kv_cnt = torch.empty((H, Mv), dtype=torch.int32, device=dev)
+    bits, kv_cnt = mask_buffers(H, layout, dev)
+    scratch = fused_scratch(layout, d, params.p, dev)
     adja = statics.packed(layout)
     work = _workspace(dev)
 
@@ -121,16 +115,16 @@ def carve_layer(q, k, v, layout: BlockLayout, statics: StaticMasks, params: Sele
                 dst[h0:h1].copy_(src[h0:h1], non_blocking=True)
         comp.wait_stream(s_in)
         sl = slice(h0, h1)
-        _launch_chunk(dq[sl], dk[sl], dv[sl], do[sl], pq[sl], pk[sl], R[sl], bits[sl], kv_idx[sl],
-                      kv_cnt[sl], adja, layout, params, beta.beta, work, comp.cuda_stream)
+        _launch_chunk(dq[sl], dk[sl], dv[sl], do[sl], pq[sl], pk[sl], bits[sl], kv_cnt[sl], scratch,
+                      adja, layout, params, beta.beta, work, comp.cuda_stream)
         s_out.wait_stream(comp)
         with torch.cuda.stream(s_out):
             out[h0:h1].copy_(do[h0:h1], non_blocking=True)
     comp.wait_stream(s_out)
-    for t in (dq, dk, dv, do, pq, pk, R):  # keep the caching allocator from recycling early
+    for t in (dq, dk, dv, do, pq, pk):  # keep the caching allocator from recycling early
         t.record_stream(s_in)
         t.record_stream(s_out)
-    mask = BlockMask(words=bits, kv_idx=kv_idx, kv_cnt=kv_cnt, M_total=Mt, nonempty=True)
+    mask = BlockMask(words=bits, kv_cnt=kv_cnt, M_total=Mt, nonempty=True)
     comp.synchronize()  # a host result is complete on return, like the reference's arrays
     return (out.numpy() if numpy_in else out), mask
 
@@ -138,8 +132,8 @@ def carve_layer(q, k, v, layout: BlockLayout, statics: StaticMasks, params: Sele
 class CarveLayerGraph:
     """One carved-attention layer captured as a CUDA graph on fixed device buffers.
 
-    A DiT runs the same layer geometry every step, so the four launches
-    (pool -> scores -> select/union -> carve) and the carve kernel's work-counter reset are
+    A DiT runs the same layer geometry every step, so the launches
+    (pool -> fused scores/select/union -> carve) and the carve kernel's work-counter reset are
     recorded once and replayed with one ``cudaGraphLaunch``.  Like ``torch.cuda.CUDAGraph``
     the buffers are static: write the step's Q/K/V into ``q``/``k``/``v`` (or pass the
     tensors the caller already fills in place), call :meth:`replay`, read ``out`` and
@@ -160,21 +154,18 @@ class CarveLayerGraph:
             raise ShapeError("Q/K/V must share strides with a contiguous innermost axis")
         H, N, d = q.shape
         dev = q.device
-        Mv, Mt = layout.M_v, layout.M_total
+        Mt = layout.M_total
         self.q, self.k, self.v = q, k, v
         self.out = torch.empty_like(q)
         self._pq = torch.empty((H, Mt, d), dtype=torch.float64, device=dev)
         self._pk = torch.empty_like(self._pq)
-        self._R = torch.empty((H, Mv, Mt), dtype=torch.float64, device=dev)
-        self._bits = torch.empty((H, Mv, mask_words(Mt)), dtype=torch.int32, device=dev)
-        self._kv_idx = torch.empty((H, Mv, Mt), dtype=torch.int32, device=dev)
-        self._kv_cnt = torch.empty((H, Mv), dtype=torch.int32, device=dev)
+        self._bits, self._kv_cnt = mask_buffers(H, layout, dev)
+        self._scratch = fused_scratch(layout, d, params.p, dev)
         self._adja = statics.packed(layout)
         self._work = torch.zeros(16, dtype=torch.int32, device=dev)  # private: replays may overlap
-        self.mask = BlockMask(words=self._bits, kv_idx=self._kv_idx, kv_cnt=self._kv_cnt, M_total=Mt,
-                              nonempty=True)
-        args = (self.q, self.k, self.v, self.out, self._pq, self._pk, self._R, self._bits,
-                self._kv_idx, self._kv_cnt, self._adja, layout, params, beta.beta, self._work)
+        self.mask = BlockMask(words=self._bits, kv_cnt=self._kv_cnt, M_total=Mt, nonempty=True)
+        args = (self.q, self.k, self.v, self.out, self._pq, self._pk, self._bits, self._kv_cnt,
+                self._scratch, self._adja, layout, params, beta.beta, self._work)
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):  # eager warm-up: kernel attributes, tensor-map driver entry

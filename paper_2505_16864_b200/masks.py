@@ -1,13 +1,17 @@
 """Dynamic block selection on the GPU (reference: tokencarve masks.py).
 
-``build_block_mask`` is three launches: K3 ``tcb_block_pool`` (Q and K in one
-pass, float64 accumulation -> pooled means bit-exact with masks.py:112-116),
-K4a ``tcb_block_scores`` (float64 pooled scores / sqrt(d), masks.py:130-131) and
-the fused K4b+K5 ``tcb_block_select_scores`` (row softmax with numpy's pairwise
-sums, masks.py:132-134, then radix-select of the top n_keep under the stable
-descending order, the exact sequential prefix cutoff, and the union with the
-condition columns and the packed adjacency, masks.py:137-175).  The mask is kept packed (H, M_v, words)
-plus an ascending CSR (kv_idx, kv_cnt) that the attention kernel walks.
+``build_block_mask`` runs K3 ``tcb_block_pool`` (Q and K in one pass, float64
+accumulation -> pooled means bit-exact with masks.py:112-116) and then either
+* (R wanted -- the reference's return value) K4a ``tcb_block_scores`` (float64 pooled
+  scores / sqrt(d), masks.py:130-131) and ``tcb_block_select_scores`` (row softmax with
+  numpy's pairwise sums, masks.py:132-134, radix-select of the top n_keep under the stable
+  descending order, the exact sequential prefix cutoff, and the union with the condition
+  columns and the packed adjacency, masks.py:137-175), R left in place; or
+* (``need_relevance=False``: the layer path) ``tcb_block_mask_fused``: scores of an 8-row
+  tile on the FP64 tensor core into shared memory and the same selection there, R never
+  written (p == 0 selects on the scores themselves, the softmax being monotone).
+The mask is packed (H, M_v, words) uint32 plus row counts; the attention kernel walks the
+set bits of a row in ascending order.
 """
 
 from __future__ import annotations
@@ -76,15 +80,18 @@ class SelectionParams:
 class BlockMask:
     """Selection mask (H, M_v, M_total) (masks.py:78-95).
 
-    Device form: packed ``words`` (H, M_v, ceil(M_total/32)) and the ascending CSR
-    ``kv_idx`` (H, M_v, M_total capacity) / ``kv_cnt`` (H, M_v).  ``BlockMask(bits)``
+    Device form: packed ``words`` (H, M_v, ceil(M_total/32)) uint32 -- column j of a row is
+    bit j % 32 of word j // 32 -- and the row counts ``kv_cnt`` (H, M_v).  The carve kernels
+    walk a row's set bits in ascending order (the reference's flatnonzero, attention.py:179),
+    so no index list is stored; ``kv_idx`` materialises the padded ascending lists on demand
+    for inspection.  ``BlockMask(bits)``
     accepts a dense bool array/tensor like the reference and packs it on the device.
     ``.bits`` is the dense bool mask: a read-only numpy array when the mask came from
     numpy (a numpy ``bits`` argument, or ``build_block_mask`` on numpy Q/K), as the
     reference returns (masks.py:87); otherwise the device tensor (``bits_dev``).
     """
 
-    def __init__(self, bits=None, *, words=None, kv_idx=None, kv_cnt=None, M_total=None,
+    def __init__(self, bits=None, *, words=None, kv_cnt=None, M_total=None,
                  nonempty: bool = False, host: bool | None = None):
         self._np = None
         if bits is not None:
@@ -95,18 +102,16 @@ class BlockMask:
                 self._np = bits
             dense = _dev.as_cuda(bits)
             M_total = int(dense.shape[-1])
-            with _dev.on(dense):
-                words, kv_idx, kv_cnt = pack_rows(dense, M_total)
+            words, kv_cnt = pack_rows(dense, M_total)
             self._dense = dense
             nonempty = False
             if host is None:
                 host = isinstance(bits, np.ndarray)
         else:
-            if words is None or kv_idx is None or kv_cnt is None or M_total is None:
-                raise ShapeError("BlockMask needs bits= or the packed (words, kv_idx, kv_cnt)")
+            if words is None or kv_cnt is None or M_total is None:
+                raise ShapeError("BlockMask needs bits= or the packed (words, kv_cnt)")
             self._dense = None
         self.words = words
-        self.kv_idx = kv_idx
         self.kv_cnt = kv_cnt
         self.M_total = int(M_total)
         self._nonempty = nonempty
@@ -132,6 +137,16 @@ class BlockMask:
             a.setflags(write=False)
             self._np = a
         return self._np
+
+    @property
+    def kv_idx(self) -> torch.Tensor:
+        """(H, M_v, M_total) int32: row r's ascending kv blocks in its first kv_cnt[r] entries
+        (the rest -1) -- derived from the bits on the device; the kernels never read it."""
+        dense = self.bits_dev
+        cols = torch.arange(self.M_total, dtype=torch.int32, device=dense.device)
+        key = torch.where(dense, cols, torch.full_like(cols, self.M_total))
+        srt = torch.sort(key, dim=-1).values
+        return torch.where(srt < self.M_total, srt, torch.full_like(srt, -1))
 
     @property
     def n_heads(self) -> int:
@@ -223,12 +238,11 @@ def _select(R: torch.Tensor, params: SelectionParams, M_v: int, adja_bits, with_
     dev = R.device
     with _dev.on(R):
         bits = torch.empty((H, rows, words), dtype=torch.int32, device=dev)
-        kv_idx = torch.empty((H, rows, n_cols), dtype=torch.int32, device=dev)
         kv_cnt = torch.empty((H, rows), dtype=torch.int32, device=dev)
         _native.call("tcb_block_select", R.data_ptr(), H, rows, n_cols, _native.ptr(adja_bits),
                      words, params.n_floor(M_v), float(params.p), 1 if with_union else 0,
-                     bits.data_ptr(), kv_idx.data_ptr(), kv_cnt.data_ptr(), _dev.stream())
-    return bits, kv_idx, kv_cnt
+                     bits.data_ptr(), kv_cnt.data_ptr(), _dev.stream())
+    return bits, kv_cnt
 
 
 def importance_mask(R, params: SelectionParams, M_v: int):
@@ -236,7 +250,7 @@ def importance_mask(R, params: SelectionParams, M_v: int):
     if R.ndim != 3:
         raise ShapeError(f"relevance must be rank 3, got shape {tuple(R.shape)}")
     Rd = _dev.as_cuda(R, torch.float64).contiguous()
-    bits, _, _ = _select(Rd, params, M_v, None, with_union=False)
+    bits, _ = _select(Rd, params, M_v, None, with_union=False)
     return _dev.to_like(unpack_rows(bits, Rd.shape[-1]), R)
 
 
@@ -255,37 +269,68 @@ def union_mask(b_top, cond, adja, layout: BlockLayout) -> BlockMask:
     return BlockMask(bits=dense, host=_dev.is_numpy(b_top))
 
 
-def build_block_mask(q, k, layout: BlockLayout, statics: StaticMasks, params: SelectionParams):
+def build_block_mask(q, k, layout: BlockLayout, statics: StaticMasks, params: SelectionParams,
+                     *, need_relevance: bool = True):
     """Pool -> score -> select -> union; returns (BlockMask, R) (masks.py:178-199).
 
-    Three launches: K3 pool (Q and K together), K4a float64 scores, and the fused
-    row-softmax + selection + union kernel, which leaves R in the score buffer."""
+    With R (the reference's return value): pool, float64 scores into R, and the row-softmax +
+    selection + union kernel that leaves R in place -- three launches.  ``need_relevance=False``
+    (keyword extension; returns ``(mask, None)``) runs the fused kernel that never writes R:
+    pool + one scores-and-select launch (plus an exact re-run of undecided rows)."""
     qd, kd = _poolable(q), _poolable(k)
     if qd.dtype != kd.dtype:
         qd, kd = qd.to(torch.float64), kd.to(torch.float64)
     _dev.same_device(qd, kd)
     with _dev.on(qd):
-        return _build_block_mask(qd, kd, layout, statics, params, host=_dev.is_numpy(q))
+        return _build_block_mask(qd, kd, layout, statics, params, host=_dev.is_numpy(q),
+                                 need_relevance=need_relevance)
 
 
-def _build_block_mask(qd, kd, layout, statics, params, host):
+def mask_buffers(H: int, layout: BlockLayout, device):
+    """(bits, kv_cnt) device buffers of a mask with H heads."""
+    words = mask_words(layout.M_total)
+    return (torch.empty((H, layout.M_v, words), dtype=torch.int32, device=device),
+            torch.empty((H, layout.M_v), dtype=torch.int32, device=device))
+
+
+def fused_scratch(layout: BlockLayout, d: int, p: float, device):
+    """Score scratch the fused mask launch needs for this shape (None: none)."""
+    n = _native.query("tcb_block_mask_fused_scratch", layout.M_v, layout.M_total, d, float(p))
+    return None if n == 0 else torch.empty(n, dtype=torch.float64, device=device)
+
+
+def launch_mask(pq: torch.Tensor, pk: torch.Tensor, layout: BlockLayout, adja, params,
+                bits: torch.Tensor, kv_cnt: torch.Tensor, stream: int, scratch=None) -> None:
+    """The fused scores + select + union launch on pooled (H, M_total, d) float64 means."""
+    H, _, d = pq.shape
+    _native.call("tcb_block_mask_fused", pq.data_ptr(), pq.shape[1], pk.data_ptr(), H, layout.M_v,
+                 layout.M_total, d, _native.ptr(adja), mask_words(layout.M_total),
+                 params.n_floor(layout.M_v), float(params.p), bits.data_ptr(), kv_cnt.data_ptr(),
+                 _native.ptr(scratch), 0 if scratch is None else scratch.numel(), stream)
+
+
+def _build_block_mask(qd, kd, layout, statics, params, host, need_relevance=True):
     d_k = qd.shape[-1]
     H = qd.shape[0]
     pq, pk = _pool_one_or_two(qd, kd, layout)
-    R = torch.empty((H, layout.M_v, layout.M_total), dtype=torch.float64, device=qd.device)
-    _native.call("tcb_block_scores", pq.values.data_ptr(), layout.M_total, pk.values.data_ptr(),
-                 H, layout.M_v, layout.M_total, d_k, R.data_ptr(), _dev.stream())
-    words = mask_words(layout.M_total)
-    bits = torch.empty((H, layout.M_v, words), dtype=torch.int32, device=qd.device)
-    kv_idx = torch.empty((H, layout.M_v, layout.M_total), dtype=torch.int32, device=qd.device)
-    kv_cnt = torch.empty((H, layout.M_v), dtype=torch.int32, device=qd.device)
+    bits, kv_cnt = mask_buffers(H, layout, qd.device)
     adja = statics.packed(layout)
-    _native.call("tcb_block_select_scores", R.data_ptr(), H, layout.M_v, layout.M_total,
-                 _native.ptr(adja), words, params.n_floor(layout.M_v), float(params.p), 1,
-                 bits.data_ptr(), kv_idx.data_ptr(), kv_cnt.data_ptr(), _dev.stream())
-    mask = BlockMask(words=bits, kv_idx=kv_idx, kv_cnt=kv_cnt, M_total=layout.M_total,
-                     nonempty=True, host=host)
-    return mask, (R.cpu().numpy() if host else R)
+    if not need_relevance:
+        launch_mask(pq.values, pk.values, layout, adja, params, bits, kv_cnt, _dev.stream(),
+                    fused_scratch(layout, d_k, params.p, qd.device))
+        R = None
+    else:
+        R = torch.empty((H, layout.M_v, layout.M_total), dtype=torch.float64, device=qd.device)
+        _native.call("tcb_block_scores", pq.values.data_ptr(), layout.M_total,
+                     pk.values.data_ptr(), H, layout.M_v, layout.M_total, d_k, R.data_ptr(),
+                     _dev.stream())
+        _native.call("tcb_block_select_scores", R.data_ptr(), H, layout.M_v, layout.M_total,
+                     _native.ptr(adja), mask_words(layout.M_total), params.n_floor(layout.M_v),
+                     float(params.p), 1, bits.data_ptr(), kv_cnt.data_ptr(), _dev.stream())
+    mask = BlockMask(words=bits, kv_cnt=kv_cnt, M_total=layout.M_total, nonempty=True, host=host)
+    if R is not None and host:
+        R = R.cpu().numpy()
+    return mask, R
 
 
 def mask_stats(mask: BlockMask, R=None, p: float | None = None) -> dict:

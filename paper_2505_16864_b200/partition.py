@@ -226,14 +226,14 @@ class StaticMasks:
 
 
 def pack_rows(dense: torch.Tensor, n_cols: int):
-    """Dense bool/uint8 (..., n_cols) -> (packed uint32 rows, CSR kv_idx, kv_cnt)."""
+    """Dense bool/uint8 (..., n_cols) -> (packed uint32 rows, row popcounts kv_cnt)."""
     d8 = dense.contiguous().view(torch.uint8) if dense.dtype == torch.bool else dense.contiguous()
     lead = d8.shape[:-1]
     rows = int(np.prod(lead)) if len(lead) else 1
     words = mask_words(n_cols)
-    bits = torch.empty((*lead, words), dtype=torch.int32, device=d8.device)
-    kv_idx = torch.empty((*lead, n_cols), dtype=torch.int32, device=d8.device)
-    kv_cnt = torch.empty(lead, dtype=torch.int32, device=d8.device)
-    _native.call("tcb_mask_pack", d8.data_ptr(), rows, n_cols, words, bits.data_ptr(),
-                 kv_idx.data_ptr(), kv_cnt.data_ptr(), _dev.stream())
-    return bits, kv_idx, kv_cnt
+    with _dev.on(d8):
+        bits = torch.empty((*lead, words), dtype=torch.int32, device=d8.device)
+        kv_cnt = torch.empty(lead, dtype=torch.int32, device=d8.device)
+        _native.call("tcb_mask_pack", d8.data_ptr(), rows, n_cols, words, bits.data_ptr(),
+                     kv_cnt.data_ptr(), _dev.stream())
+    return bits, kv_cnt

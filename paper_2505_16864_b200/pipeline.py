@@ -438,7 +438,7 @@ def toy_transformer_denoiser(channels: int = 1, n_heads: int = 2, d_k: int = 16,
         q = torch.einsum("nf,hfd->hnd", padded, wq).contiguous()
         k = torch.einsum("nf,hfd->hnd", padded, wk).contiguous()
         v = torch.einsum("nf,hfd->hnd", padded, wv).contiguous()
-        mask, _ = build_block_mask(q, k, layout, ctx.statics, ctx.params)
+        mask, _ = build_block_mask(q, k, layout, ctx.statics, ctx.params, need_relevance=False)
         out = carve_attention(AttentionInputs(q=q, k=k, v=v, layout=layout), mask, ctx.beta)
         ctx.metrics["effective_sparsity"] = 1.0 - mask.selected_fraction
         merged = out.permute(1, 0, 2).reshape(layout.padded_total, n_heads * d_k)

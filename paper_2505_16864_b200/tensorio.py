@@ -141,5 +141,5 @@ def read_block_mask(path):
     dense = torch.empty((H, rows, M_total), dtype=torch.uint8, device=dev)
     _native.call("tcb_packbits_to_dense", pk.data_ptr(), H * rows, M_total, dense.data_ptr(),
                  _dev.stream())
-    words, kv_idx, kv_cnt = pack_rows(dense, M_total)
-    return BlockMask(words=words, kv_idx=kv_idx, kv_cnt=kv_cnt, M_total=M_total)
+    words, kv_cnt = pack_rows(dense, M_total)
+    return BlockMask(words=words, kv_cnt=kv_cnt, M_total=M_total)

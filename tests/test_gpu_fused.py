@@ -135,8 +135,8 @@ def test_torch_ops_eager_and_compiled_match_api():
     def layer(x):
         q, k, v = (torch.einsum("nf,fhd->hnd", x, w[i].view(64, 2, 128)).to(torch.bfloat16).contiguous()
                    for i in range(3))
-        bits, kv_idx, kv_cnt = torch.ops.tokencarve.block_mask(q, k, adja, *args, prm.n_floor(lay.M_v), 0.0)
-        o = torch.ops.tokencarve.carve(q, k, v, kv_idx, kv_cnt, *args, 0.0)
+        bits, kv_cnt = torch.ops.tokencarve.block_mask(q, k, adja, *args, prm.n_floor(lay.M_v), 0.0)
+        o = torch.ops.tokencarve.carve(q, k, v, bits, kv_cnt, *args, 0.0)
         return o.float().sum(dim=0), bits
 
     eager, bits = layer(x)

@@ -551,3 +551,63 @@ def test_carve_fp16_tcgen05_and_pool(d):
     err = np.abs(got - ref).max() / np.abs(ref).max()
     assert err <= 1e-2, err
     assert np.all(got[:, ~oracle.token_valid(L)] == 0.0)
+
+
+# ----------------------------------------------------------------- fused scores + select
+FUSED_CASES = [
+    # (dims, m, n_cond, d, H, k, p): fused kernel (d 64 / 128, incl. the cutoff path and a
+    # crossing beyond the 512-wide window), the bounded-scratch path (d = 96; 7,201 blocks)
+    ((5, 12, 16), 128, 40, 128, 3, 0.1, 0.0),
+    ((5, 12, 16), 128, 40, 128, 3, 0.2, 0.3),
+    ((4, 10, 12), 8, 12, 64, 2, 0.3, 0.3),
+    ((4, 10, 12), 8, 12, 64, 2, 0.05, 0.7),
+    ((6, 20, 30), 16, 0, 64, 2, 0.02, 0.0),
+    ((3, 9, 11), 8, 5, 96, 2, 0.25, 0.0),
+    ((3, 9, 11), 8, 5, 96, 2, 0.25, 0.3),
+    ((64, 90, 160), 128, 77, 64, 1, 0.02, 0.0),
+]
+
+
+@pytest.mark.parametrize("case", FUSED_CASES)
+def test_fused_mask_equals_unfused(case):
+    """need_relevance=False (fused tiles, no R in global memory; p == 0 selects on the
+    scores) gives bitwise the mask of the R-materialising path, and both match the oracle
+    on sampled rows."""
+    dims, m, nc, d, H, k, p = case
+    g = tcb.GridDims(*dims)
+    lay = tcb.build_layout(g, m, nc)
+    st = tcb.StaticMasks.build(lay, g, tcb.build_curve(g))
+    gen = torch.Generator(device="cuda").manual_seed(sum(dims) + d)
+    q, kk = (torch.randn((H, lay.padded_total, d), generator=gen, device="cuda").to(torch.bfloat16)
+             for _ in range(2))
+    prm = tcb.SelectionParams(k=k, p=p)
+    m_ref, R = tcb.build_block_mask(q, kk, lay, st, prm)
+    m_fused, none = tcb.build_block_mask(q, kk, lay, st, prm, need_relevance=False)
+    assert none is None
+    assert torch.equal(m_fused.words, m_ref.words)
+    assert torch.equal(m_fused.kv_cnt, m_ref.kv_cnt)
+    rows = np.unique(np.r_[0:4, lay.M_v // 2, lay.M_v - 1])
+    top = oracle.select_topk(R[:, rows].cpu().numpy(), k, p, lay.M_v)
+    want = oracle.union_bits(top, st.adja[rows], lay.M_v)
+    assert np.array_equal(m_fused.bits_dev[:, rows].cpu().numpy(), want)
+
+
+def test_fused_score_ties_fall_back_to_the_exact_order():
+    """Identical key blocks give exactly tied scores: the score-order fast path (p == 0) must
+    not decide the top-k boundary and re-runs those rows through the softmax + stable order
+    (ascending block index on ties, masks.py:150) -- bitwise the R path and the oracle."""
+    dims, m, nc, d = (4, 8, 8), 16, 20, 64
+    g = tcb.GridDims(*dims)
+    lay = tcb.build_layout(g, m, nc)
+    st = tcb.StaticMasks.build(lay, g, tcb.build_curve(g))
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    q = torch.randn((2, lay.padded_total, d), generator=gen, device="cuda")
+    blk = torch.randn((1, m, d), generator=gen, device="cuda")
+    kk = blk.repeat(2, lay.M_total, 1)  # every key block identical -> every score tied
+    kk[1, : 4 * m] += 1.0  # head 1: a few distinct blocks, the rest tied
+    prm = tcb.SelectionParams(k=0.25, p=0.0)
+    m_ref, R = tcb.build_block_mask(q, kk, lay, st, prm)
+    m_fused, _ = tcb.build_block_mask(q, kk, lay, st, prm, need_relevance=False)
+    assert torch.equal(m_fused.words, m_ref.words)
+    top = oracle.select_topk(R.cpu().numpy(), 0.25, 0.0, lay.M_v)
+    assert np.array_equal(m_fused.bits_dev.cpu().numpy(), oracle.union_bits(top, st.adja, lay.M_v))

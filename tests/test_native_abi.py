@@ -18,7 +18,7 @@ HEADER = os.path.join(ROOT, "include", "tokencarve_b200.h")
 
 def header_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:const char\*|int)\s+(tcb_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int64_t|int)\s+(tcb_\w+)\s*\(", text, re.M)))
 
 
 def test_library_builds_and_exports_every_header_symbol():
@@ -31,7 +31,7 @@ def test_library_builds_and_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_native.SIGNATURES), "ctypes table must mirror the header"
-    assert _native.load().tcb_abi_version() == 1
+    assert _native.load().tcb_abi_version() == 2
 
 
 def test_error_mapping_without_gpu():
@@ -50,20 +50,33 @@ def test_error_mapping_without_gpu():
     with pytest.raises(DomainError):
         _native.call("tcb_block_pool", 1, None, 7, 0, 0, 1, 1, 1, 1, 1, 1, 0, 1, None, None)
     # carve: unknown dtype, shape errors, too many work items
+    # (q, k, v, o, dtype, sh, sn, bits, words, kv_cnt, H, d, m, M_v, M_total, n_valid, n_cond,
+    #  beta, work, stream)
     with pytest.raises(DomainError):
-        _native.call("tcb_carve_fwd", 1, 1, 1, 1, 9, 128, 128, 1, 1, 1, 128, 128, 1, 1, 1, 0, 0.0, 1,
-                     None)
+        _native.call("tcb_carve_fwd", 1, 1, 1, 1, 9, 128, 128, 1, 1, 1, 1, 128, 128, 1, 1, 1, 0,
+                     0.0, 1, None)
     with pytest.raises(ShapeError):
-        _native.call("tcb_carve_fwd", None, 1, 1, 1, 1, 128, 128, 1, 1, 1, 128, 128, 1, 1, 1, 0, 0.0,
-                     1, None)
+        _native.call("tcb_carve_fwd", None, 1, 1, 1, 1, 128, 128, 1, 1, 1, 1, 128, 128, 1, 1, 1, 0,
+                     0.0, 1, None)
+    with pytest.raises(ShapeError):  # mask rows narrower than M_total columns
+        _native.call("tcb_carve_fwd", 1, 1, 1, 1, 1, 128, 128, 1, 1, 1, 1, 128, 128, 40, 40, 1, 0,
+                     0.0, 1, None)
     with pytest.raises(SizeError):
-        _native.call("tcb_carve_fwd", 1, 1, 1, 1, 1, 128, 128, 1, 1, 1 << 20, 128, 128, 4096, 4096,
-                     1, 0, 0.0, 1, None)
+        _native.call("tcb_carve_fwd", 1, 1, 1, 1, 1, 128, 128, 1, 128, 1, 1 << 20, 128, 128, 4096,
+                     4096, 1, 0, 0.0, 1, None)
     # selection: M_total beyond the supported range, n_floor < 1
     with pytest.raises(SizeError):
-        _native.call("tcb_block_select", 1, 1, 9000, 9000, None, 300, 1, 0.0, 1, 1, 1, 1, None)
+        _native.call("tcb_block_select", 1, 1, 9000, 9000, None, 300, 1, 0.0, 1, 1, 1, None)
     with pytest.raises(DomainError):
-        _native.call("tcb_block_select", 1, 1, 4, 4, None, 1, 0, 0.0, 1, 1, 1, 1, None)
+        _native.call("tcb_block_select", 1, 1, 4, 4, None, 1, 0, 0.0, 1, 1, 1, None)
+    with pytest.raises(DomainError):  # fused mask: p outside [0, 1)
+        _native.call("tcb_block_mask_fused", 1, 4, 1, 1, 4, 4, 128, None, 1, 1, 1.0, 1, 1, None, 0,
+                     None)
+    # the fused kernel covers C2 (no scratch); a long row or d = 96 needs a bounded chunk
+    assert _native.query("tcb_block_mask_fused_scratch", 929, 931, 128, 0.0) == 0
+    assert _native.query("tcb_block_mask_fused_scratch", 929, 931, 128, 0.3) == 0
+    assert 0 < _native.query("tcb_block_mask_fused_scratch", 8190, 8192, 128, 0.3) <= 32 << 20
+    assert _native.query("tcb_block_mask_fused_scratch", 929, 931, 96, 0.0) == 929 * 931
     # fused neighbours: bad rope sections / strides / patch sizes / grid mismatch
     import ctypes as C
     one = (C.c_void_p * 1)(16)
