@@ -108,7 +108,7 @@ def run_gpu(args):
     import paper_2505_16864_b200 as tcb
     from paper_2505_16864_b200 import _native
     from paper_2505_16864_b200.attention import _workspace
-    from paper_2505_16864_b200.masks import fused_scratch, launch_mask, mask_buffers
+    from paper_2505_16864_b200.masks import mask_scratch, launch_mask, mask_buffers
     from paper_2505_16864_b200.partition import mask_words
 
     world, rank, local = dist_env()
@@ -150,14 +150,15 @@ def run_gpu(args):
     pq = torch.empty((Hl, Mt, D), dtype=torch.float64, device=dev)
     pk = torch.empty_like(pq)
     bits, kv_cnt = mask_buffers(Hl, layout, dev)
-    scratch = fused_scratch(layout, D, P_CUT, dev)
+    scratch = mask_scratch(Hl, layout, dev)
     work = _workspace(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def layer(qh, kh, vh, out, marks=None, h0=0):
-        """The launches of one carved-attention layer on head-major views (pool, fused
-        scores + select + union -- two passes, the second only re-runs undecided rows -- and
-        carve); mask buffers are used from local head h0 on (an exchange chunk's slice)."""
+        """The launches of one carved-attention layer on head-major views (pool; scores into
+        the bounded scratch + select/union on them -- a second select pass only re-runs
+        near-tie rows; carve); mask buffers are used from local head h0 on (an exchange
+        chunk's slice)."""
         sh, sn = qh.stride(0), qh.stride(1)
         Hc = qh.shape[0]  # all local heads, or one exchange chunk of them
         bq, bk = pq[h0:h0 + Hc], pk[h0:h0 + Hc]
@@ -355,7 +356,7 @@ def run_gpu(args):
         "cuda_graph_ms_per_step": graph_ms,
         "kernels_ms": None if chunked else {
             "block_pool": round(float(k_pool), 4),
-            "block_mask_fused (scores + select + union)": round(float(k_sel), 4),
+            "block_mask (scores + select + union, no R)": round(float(k_sel), 4),
             "carve_fwd": round(float(k_carve), 4)},
         "roofline": {"bound": "tensor", "kernel": "k_carve_tc<128>",
                      "achieved": round(carve_tflops, 1), "peak": tf_sust, "unit": "TFLOP/s",
@@ -368,9 +369,9 @@ def run_gpu(args):
                      "hbm_peak_gbs": hbm},
         "e2e": e2e,
         "cpu_baseline": cpu,
-        "gpu_launches": 4 * args.steps * (min(args.a2a_chunks, Hl) if chunked else 1),
-        "launches_per_layer": "k_pool, k_select_fused (pass 1), k_select_fused (pass 2: undecided "
-                              "rows only), k_carve_tc",
+        "gpu_launches": 5 * args.steps * (min(args.a2a_chunks, Hl) if chunked else 1),
+        "launches_per_layer": "k_pool, k_scores_dmma, k_select (scores, p=0 fast path), k_select "
+                              "(exact re-run of near-tie rows only), k_carve_tc",
         "clocks": clk.result,
     }
     print(json.dumps(line))

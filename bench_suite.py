@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 import paper_2505_16864_b200 as tcb  # noqa: E402
 from paper_2505_16864_b200 import _native  # noqa: E402
 from paper_2505_16864_b200.attention import _workspace  # noqa: E402
-from paper_2505_16864_b200.masks import fused_scratch, launch_mask, mask_buffers  # noqa: E402
+from paper_2505_16864_b200.masks import mask_scratch, launch_mask, mask_buffers  # noqa: E402
 from paper_2505_16864_b200.partition import mask_words  # noqa: E402
 
 
@@ -76,7 +76,7 @@ class Layer:
         self.pk = torch.empty_like(self.pq)
         self.words = mask_words(L.M_total)
         self.bits, self.kv_cnt = mask_buffers(H, L, self.q.device)
-        self.scratch = fused_scratch(L, 128, p_cut, self.q.device)
+        self.scratch = mask_scratch(H, L, self.q.device)
         self.work = _workspace(self.q.device)
         self.s = torch.cuda.current_stream().cuda_stream
 

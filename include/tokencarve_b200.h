@@ -102,22 +102,22 @@ int tcb_block_select_scores(double* S, int H, int M_v, int M_total, const uint32
                             int words, int n_floor, double p, int with_union, uint32_t* bits,
                             int32_t* kv_cnt, void* stream);
 
-/* K4+K5 fused -- the mask of build_block_mask (masks.py:178-199) from the pooled means
- * without materialising R: each CTA computes the scores of an 8-row tile of one head on the
- * FP64 tensor core into shared memory and selects those rows there (p == 0 selects on the
- * scores directly: the softmax is monotone; rows whose top-k boundary is a near tie re-run
- * exactly).  pq: (H, pq_blocks, d), pk: (H, M_total, d) float64.  Shapes the fused kernel
- * does not cover (d not in {64, 128}, or a score tile beyond shared memory) run scores +
- * select per row chunk through `scratch` (scratch_elems doubles, >= M_total; NULL is fine
- * for covered shapes).  Union with cond columns and adja is always applied. */
-int tcb_block_mask_fused(const double* pq, int pq_blocks, const double* pk, int H, int M_v,
-                         int M_total, int d, const uint32_t* adja, int words, int n_floor, double p,
-                         uint32_t* bits, int32_t* kv_cnt, double* scratch, int64_t scratch_elems,
-                         void* stream);
+/* K4+K5 without R -- the mask of build_block_mask (masks.py:178-199) from the pooled means,
+ * for callers that do not read R back (the layer path): the float64 scores of a chunk of
+ * heads (all of them at C2) go into the caller's bounded `scratch` (never an (H, M_v,
+ * M_total) R tensor beyond 256 MB), then the select kernel works on them; at p == 0 it
+ * selects on the scores directly (the row softmax is monotone) and re-runs the rows whose
+ * top-k boundary is a near tie through the exact softmax program.  pq: (H, pq_blocks, d),
+ * pk: (H, M_total, d) float64; scratch_elems >= tcb_block_mask_scratch(H, M_v, M_total)
+ * is best (any value >= M_total works, in more chunks).  Union with the condition columns
+ * and adja is always applied.  Bitwise the mask of tcb_block_select_scores. */
+int tcb_block_mask(const double* pq, int pq_blocks, const double* pk, int H, int M_v, int M_total,
+                   int d, const uint32_t* adja, int words, int n_floor, double p, uint32_t* bits,
+                   int32_t* kv_cnt, double* scratch, int64_t scratch_elems, void* stream);
 
-/* Scratch doubles tcb_block_mask_fused needs for a shape: 0 when the fused kernel covers it,
- * else one bounded row chunk of scores (<= 256 MB). */
-int64_t tcb_block_mask_fused_scratch(int M_v, int M_total, int d, double p);
+/* Scratch doubles tcb_block_mask uses for a shape (all heads' scores up to 256 MB, else one
+ * bounded chunk). */
+int64_t tcb_block_mask_scratch(int H, int M_v, int M_total);
 
 /* Mask conversions for user-built BlockMask(bits=bool array) (masks.py:78-95). */
 int tcb_mask_pack(const uint8_t* dense, int64_t rows, int M_total, int words, uint32_t* bits,

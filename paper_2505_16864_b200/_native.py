@@ -36,8 +36,8 @@ SIGNATURES = {
     "tcb_block_select": [_P, _I, _I, _I, _P, _I, _I, _D, _I, _P, _P, _P],
     "tcb_block_scores": [_P, _I, _P, _I, _I, _I, _I, _P, _P],
     "tcb_block_select_scores": [_P, _I, _I, _I, _P, _I, _I, _D, _I, _P, _P, _P],
-    "tcb_block_mask_fused": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _D, _P, _P, _P, _I64, _P],
-    "tcb_block_mask_fused_scratch": [_I, _I, _I, _D],
+    "tcb_block_mask": [_P, _I, _P, _I, _I, _I, _I, _P, _I, _I, _D, _P, _P, _P, _I64, _P],
+    "tcb_block_mask_scratch": [_I, _I, _I],
     "tcb_mask_pack": [_P, _I64, _I, _I, _P, _P, _P],
     "tcb_mask_unpack": [_P, _I64, _I, _I, _P, _P],
     "tcb_carve_fwd": [_P, _P, _P, _P, _I, _I64, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _I64,
@@ -84,7 +84,7 @@ def load():
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = (C.c_char_p if name == "tcb_last_error" else
-                          C.c_int64 if name == "tcb_block_mask_fused_scratch" else C.c_int)
+                          C.c_int64 if name == "tcb_block_mask_scratch" else C.c_int)
         _lib = lib
     return _lib
 

@@ -1098,7 +1098,7 @@ __device__ __forceinline__ void load_prog(const PwProg& prog, int* leaf_off, int
 
 // One warp per (head, vision row) over a row-major R / score tensor in global memory.
 // Per-warp smem: vals[M_pad] | scratch (hist, sbits, leaves, sort buffers).
-template <bool RAW, bool SORT, int MODE = 0>
+template <bool RAW, bool SORT, int MODE = 0, bool FASTS = false>
 __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R, int64_t n_rows,
                                                           int M_v, int M_total, int np2,
                                                           const uint32_t* __restrict__ adja,
@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int leaf_off[SEL_MAX_LEAVES], leaf_len[SEL_MAX_LEAVES];
   __shared__ int2 fold_ops[SEL_MAX_LEAVES];
-  if (RAW) {
+  if (RAW && !FASTS) {
     load_prog(prog, leaf_off, leaf_len, fold_ops);
     __syncthreads();
   }
@@ -1127,111 +1127,11 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
   double* Rr = R + row * M_total;
   for (int j = lane; j < M_total; j += 32) vals[j] = Rr[j];
   __syncwarp();
-  // MODE 2 runs after MODE 1 turned R into probabilities in place: no softmax again
-  select_row<RAW && MODE != 2, SORT, MODE, false>(
+  // RAW: softmax first (a MODE 2 pass after a non-FASTS MODE 1 pass is launched RAW = false:
+  // MODE 1 already turned the row into probabilities in place)
+  select_row<RAW, SORT, MODE, FASTS>(
       vals, RAW ? Rr : nullptr, sc, row, (int)(row % M_v), M_v, M_total, words, n_floor, p,
       with_union, adja, bits, kv_cnt, prog.nl, prog.nops, leaf_off, leaf_len, fold_ops);
-}
-
-// ---- fused scores + selection (no R in global memory) ------------------------------------
-// CTA = (head h, tile of RT = 8 * RG vision rows).  Phase 1: S[r, j] = pq[h, r] . pk[h, j] /
-// sqrt(d) for the tile's rows and every column j < M_total on the FP64 tensor core
-// (DMMA 8x8x4, the same product and scaling as k_scores_dmma / masks.py:130-131) into shared
-// memory; each warp owns 4 column tiles at a time (4 independent accumulator chains), pq
-// fragments stay in registers, pk fragments come from L1/L2.  Phase 2: the warps select the
-// tile's rows from shared memory (select_row; FASTS when p == 0).  MODE 2 re-runs only CTAs
-// holding a row marked -1 by MODE 1 / FASTS, recomputing their scores.
-template <int RG, int DK>
-__device__ __forceinline__ void dmma_tile_scores(const double* __restrict__ pqh,
-                                                 const double* __restrict__ pkh, int r0,
-                                                 int rows_valid, int M_total, double sqrt_d,
-                                                 double* S, int ldS) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int fr = lane >> 2, fk = lane & 3;
-  constexpr int KS = DK / 4;
-  const int n_ct = (M_total + 7) >> 3;  // 8-column tiles
-  for (int g = 0; g < RG; ++g) {
-    const int rr = min(g * 8 + fr, rows_valid - 1);  // clamp: rows beyond the tile are dropped
-    double a[KS];
-#pragma unroll
-    for (int s = 0; s < KS; ++s) a[s] = __ldg(pqh + (int64_t)(r0 + rr) * DK + 4 * s + fk);
-    for (int c0 = warp * 4; c0 < n_ct; c0 += nw * 4) {
-      double acc[4][2];
-      const double* bp[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        acc[u][0] = acc[u][1] = 0.0;
-        const int col = min((c0 + u) * 8 + fr, M_total - 1);
-        bp[u] = pkh + (int64_t)col * DK + fk;
-      }
-#pragma unroll
-      for (int s = 0; s < KS; ++s) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) dmma_8x8x4(acc[u][0], acc[u][1], a[s], __ldg(bp[u] + 4 * s));
-      }
-      const int orow = g * 8 + fr;
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = (c0 + u) * 8 + 2 * fk + e;
-          if (c0 + u < n_ct && col < M_total) S[(size_t)orow * ldS + col] = acc[u][e] / sqrt_d;
-        }
-    }
-  }
-}
-
-template <int RG, int DK, bool SORT, int MODE, bool FASTS>
-__global__ void __launch_bounds__(SW_WARPS * 32) k_select_fused(
-    const double* __restrict__ pq, int pq_blocks, const double* __restrict__ pk, int n_heads,
-    int M_v, int M_total, int np2, const uint32_t* __restrict__ adja, int words, int n_floor, double p,
-    int with_union, uint32_t* __restrict__ bits, int32_t* __restrict__ kv_cnt,
-    int per_warp_bytes, int nslots, double sqrt_d, const __grid_constant__ PwProg prog) {
-  constexpr int RT = 8 * RG;
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int leaf_off[SEL_MAX_LEAVES], leaf_len[SEL_MAX_LEAVES];
-  __shared__ int2 fold_ops[SEL_MAX_LEAVES];
-  __shared__ int s_any;
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (!FASTS) {
-    load_prog(prog, leaf_off, leaf_len, fold_ops);
-    __syncthreads();
-  }
-  const int M_pad = (M_total + 1) & ~1;
-  double* S = reinterpret_cast<double*>(smem);
-  unsigned char* base = smem + (size_t)RT * M_pad * 8 + (size_t)warp * per_warp_bytes;
-  const RowScratch sc = carve_scratch(base, words, nslots,
-                                      MODE == 1 ? 544 : (np2 > 544 ? np2 : 544));
-  const int tiles_per_head = (M_v + RT - 1) / RT;
-  const int n_tiles = tiles_per_head * n_heads;
-  // grid-stride over (head, row tile), head-major: concurrently resident tiles share pk[h]
-  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int h = tile / tiles_per_head;
-    const int r0 = (tile - h * tiles_per_head) * RT;
-    const int rows_valid = min(RT, M_v - r0);
-    const int64_t row0 = (int64_t)h * M_v + r0;
-    if (MODE == 2) {  // only tiles holding a row the first pass left undecided (-1)
-      __syncthreads();
-      if (threadIdx.x == 0) s_any = 0;
-      __syncthreads();
-      if (threadIdx.x < rows_valid && kv_cnt[row0 + threadIdx.x] == -1) s_any = 1;
-      __syncthreads();
-      if (!s_any) continue;
-    }
-    __syncthreads();  // the previous tile's rows are done with S
-    dmma_tile_scores<RG, DK>(pq + (int64_t)h * pq_blocks * DK, pk + (int64_t)h * M_total * DK,
-                             r0, rows_valid, M_total, sqrt_d, S, M_pad);
-    __syncthreads();
-    for (int r = warp; r < rows_valid; r += nw) {
-      const int64_t row = row0 + r;
-      if (MODE == 2 && kv_cnt[row] != -1) continue;
-      select_row<true, SORT, MODE, FASTS>(S + (size_t)r * M_pad, nullptr, sc, row, r0 + r, M_v,
-                                          M_total, words, n_floor, p, with_union, adja, bits,
-                                          kv_cnt, prog.nl, prog.nops, leaf_off, leaf_len,
-                                          fold_ops);
-      __syncwarp();
-    }
-  }
 }
 
 __global__ void __launch_bounds__(128) k_mask_pack(const uint8_t* __restrict__ dense, int M_total,
@@ -1382,7 +1282,7 @@ constexpr size_t SMEM_CAP = 232448 - 8192;  // opt-in limit minus the static lea
 // n_rows rows of R (row r uses adjacency row r % M_v; chunk callers offset the pointers)
 static int launch_select(double* R, bool raw, int64_t n_rows, int M_v, int M_total,
                          const uint32_t* adja, int words, int n_floor, double p, int with_union,
-                         uint32_t* bits, int32_t* kv_cnt, cudaStream_t s) {
+                         uint32_t* bits, int32_t* kv_cnt, cudaStream_t s, bool fasts = false) {
   TCB_CHECK_ARG(R && bits && kv_cnt, TCB_ESHAPE, "null tensor");
   TCB_CHECK_ARG(n_rows >= 0 && M_v >= 0 && M_total >= 1, TCB_ESHAPE, "bad select shape");
   TCB_CHECK_ARG(words >= ceil_div(M_total, 32), TCB_ESHAPE, "words too small");
@@ -1406,60 +1306,20 @@ static int launch_select(double* R, bool raw, int64_t n_rows, int M_v, int M_tot
         (int)pw, pl.nslots, pl.prog);
     return check_launch("k_select");
   };
+  if (raw && !sort && fasts) {
+    // p == 0 on scores nobody reads back as R: select on the scores (FASTS), then the exact
+    // softmax program on the rows whose top-k boundary was a near tie (grid-stride, usually
+    // nothing to do)
+    int rc = go(k_select<true, false, 1, true>, 0);
+    if (rc) return rc;
+    return go(k_select<true, false, 2, false>, 0);
+  }
   if (raw && !sort) return go(k_select<true, false>, 0);
   // cutoff path: slim pass (register sort of the top-512 window, ~35 % less shared memory
   // per warp -> 1.5x the resident warps), then the full-sort pass over the rows it left
   int rc = raw ? go(k_select<true, true, 1>, 544) : go(k_select<false, true, 1>, 544);
   if (rc) return rc;
   return go(k_select<false, true, 2>, full_sort);
-}
-
-// Whether the fused kernel covers (M_total, d, p): 8-row score tile + per-warp scratch fit.
-static bool fused_fits(int M_total, int d, int words, double p) {
-  if (d != 64 && d != 128) return false;
-  const SelPlan pl = plan_select(M_total, words);
-  const int full_sort = pl.np2 > 544 ? pl.np2 : 544;
-  return (size_t)8 * pl.M_pad * 8 + scratch_bytes(pl, p > 0.0 ? full_sort : 0) * SW_WARPS <= SMEM_CAP;
-}
-
-// Fused scores + selection: returns -1 (nothing launched) when the shape is not covered
-// (d not in {64, 128}, or the 8-row score tile plus scratch exceeds shared memory).
-template <int DK>
-static int launch_fused_dk(const double* pq, int pq_blocks, const double* pk, int H, int M_v,
-                           int M_total, const uint32_t* adja, int words, int n_floor, double p,
-                           int with_union, uint32_t* bits, int32_t* kv_cnt, cudaStream_t s) {
-  constexpr int RG = 1, RT = 8 * RG;
-  const SelPlan pl = plan_select(M_total, words);
-  const int full_sort = pl.np2 > 544 ? pl.np2 : 544;
-  const size_t tile = (size_t)RT * pl.M_pad * 8;
-  const int sort1 = p > 0.0 ? 544 : 0, sort2 = p > 0.0 ? full_sort : 0;
-  const size_t pw1 = scratch_bytes(pl, sort1), pw2 = scratch_bytes(pl, sort2);
-  if (tile + pw2 * SW_WARPS > SMEM_CAP) return -1;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int n_tiles = H * (int)ceil_div(M_v, RT);
-  const double sqrt_d = sqrt((double)DK);
-  auto go = [&](auto kern, size_t pw, int grid) -> int {
-    const size_t sm = tile + pw * SW_WARPS;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return set_error(TCB_ECUDA, "k_select_fused smem: %s", cudaGetErrorString(e));
-    kern<<<(unsigned)grid, SW_WARPS * 32, sm, s>>>(pq, pq_blocks, pk, H, M_v, M_total, pl.np2, adja,
-                                                   words, n_floor, p, with_union, bits, kv_cnt,
-                                                   (int)pw, pl.nslots, sqrt_d, pl.prog);
-    return check_launch("k_select_fused");
-  };
-  // pass 2 (rows pass 1 left undecided, usually none) runs grid-stride on a small grid
-  const int grid2 = std::min(n_tiles, 2 * sms);
-  int rc;
-  if (p == 0.0) {
-    rc = go(k_select_fused<RG, DK, false, 1, true>, pw1, n_tiles);
-    if (rc) return rc;
-    return go(k_select_fused<RG, DK, false, 2, false>, pw2, grid2);
-  }
-  rc = go(k_select_fused<RG, DK, true, 1, false>, pw1, n_tiles);
-  if (rc) return rc;
-  return go(k_select_fused<RG, DK, true, 2, false>, pw2, grid2);
 }
 
 extern "C" int tcb_block_select(const double* R, int H, int M_v, int M_total,
@@ -1480,19 +1340,22 @@ extern "C" int tcb_block_select_scores(double* S, int H, int M_v, int M_total,
                        bits, kv_cnt, as_stream(stream));
 }
 
-// Scratch doubles tcb_block_mask_fused needs for a shape (0: the fused kernel covers it).
-extern "C" int64_t tcb_block_mask_fused_scratch(int M_v, int M_total, int d, double p) {
-  const int words = (int)ceil_div(M_total, 32);
-  if (fused_fits(M_total, d, words, p)) return 0;
-  const int64_t cap = (int64_t)32 << 20;  // <= 256 MB of float64 scores per chunk
+// Scratch doubles tcb_block_mask uses: all heads' scores when they fit 256 MB, else one
+// bounded chunk (whole heads, or a row range of one head).
+extern "C" int64_t tcb_block_mask_scratch(int H, int M_v, int M_total) {
+  const int64_t cap = (int64_t)32 << 20;  // 256 MB of float64 scores
+  const int64_t all = (int64_t)H * M_v * M_total;
+  if (all <= cap) return std::max<int64_t>(all, 1);
   const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(M_v, cap / std::max(1, M_total)));
+  const int64_t per_head = (int64_t)M_v * M_total;
+  if (rows == M_v) return (cap / per_head) * per_head;  // whole heads per chunk
   return rows * M_total;
 }
 
-extern "C" int tcb_block_mask_fused(const double* pq, int pq_blocks, const double* pk, int H,
-                                    int M_v, int M_total, int d, const uint32_t* adja, int words,
-                                    int n_floor, double p, uint32_t* bits, int32_t* kv_cnt,
-                                    double* scratch, int64_t scratch_elems, void* stream) {
+extern "C" int tcb_block_mask(const double* pq, int pq_blocks, const double* pk, int H, int M_v,
+                              int M_total, int d, const uint32_t* adja, int words, int n_floor,
+                              double p, uint32_t* bits, int32_t* kv_cnt, double* scratch,
+                              int64_t scratch_elems, void* stream) {
   TCB_CHECK_ARG(pq && pk && bits && kv_cnt, TCB_ESHAPE, "null tensor");
   TCB_CHECK_ARG(H >= 1 && M_v >= 0 && M_total >= M_v && M_total >= 1 && d >= 1 &&
                     M_v <= pq_blocks,
@@ -1502,32 +1365,36 @@ extern "C" int tcb_block_mask_fused(const double* pq, int pq_blocks, const doubl
   TCB_CHECK_ARG(n_floor >= 1, TCB_EDOMAIN, "n_floor must be >= 1");
   TCB_CHECK_ARG(p >= 0.0 && p < 1.0, TCB_EDOMAIN, "p %g outside [0, 1)", p);
   if ((int64_t)H * M_v == 0) return TCB_OK;
-  cudaStream_t s = as_stream(stream);
-  int rc = -1;
-  if (d == 128)
-    rc = launch_fused_dk<128>(pq, pq_blocks, pk, H, M_v, M_total, adja, words, n_floor, p, 1, bits,
-                              kv_cnt, s);
-  else if (d == 64)
-    rc = launch_fused_dk<64>(pq, pq_blocks, pk, H, M_v, M_total, adja, words, n_floor, p, 1, bits,
-                             kv_cnt, s);
-  if (rc != -1) return rc;
-  // not fused: scores + select through the caller's bounded scratch, one row chunk at a time
-  // (rows_chunk x M_total doubles), so no (H, M_v, M_total) tensor is ever allocated
   TCB_CHECK_ARG(scratch && scratch_elems >= M_total, TCB_ESIZE,
                 "scratch of %lld doubles < one row of %d", (long long)scratch_elems, M_total);
-  const int rows_chunk = (int)std::min<int64_t>(M_v, scratch_elems / M_total);
-  const int words_row = words;
+  cudaStream_t s = as_stream(stream);
+  const int64_t per_head = (int64_t)M_v * M_total;
+  const bool fasts = p == 0.0;
+  int rc;
+  if (scratch_elems >= per_head) {  // whole heads per chunk
+    const int hc = (int)std::min<int64_t>(H, scratch_elems / per_head);
+    for (int h0 = 0; h0 < H; h0 += hc) {
+      const int nh = std::min(hc, H - h0);
+      rc = launch_scores(pq + (int64_t)h0 * pq_blocks * d, pq_blocks, pk + (int64_t)h0 * M_total * d,
+                         nh, M_v, M_total, d, scratch, s);
+      if (rc) return rc;
+      rc = launch_select(scratch, true, (int64_t)nh * M_v, M_v, M_total, adja, words, n_floor, p, 1,
+                         bits + (int64_t)h0 * M_v * words, kv_cnt + (int64_t)h0 * M_v, s, fasts);
+      if (rc) return rc;
+    }
+    return TCB_OK;
+  }
+  // a row range of one head per chunk (the adjacency rows of the range start at r0)
+  const int rows_chunk = (int)(scratch_elems / M_total);
   for (int h = 0; h < H; ++h) {
     for (int r0 = 0; r0 < M_v; r0 += rows_chunk) {
       const int nr = std::min(rows_chunk, M_v - r0);
       rc = launch_scores(pq + ((int64_t)h * pq_blocks + r0) * d, nr, pk + (int64_t)h * M_total * d,
                          1, nr, M_total, d, scratch, s);
       if (rc) return rc;
-      // rows r0.. of head h: the adjacency rows start at r0 (select_row uses row % M_v)
-      rc = launch_select(scratch, true, nr, M_v, M_total,
-                         adja ? adja + (int64_t)r0 * words_row : nullptr, words_row, n_floor, p, 1,
-                         bits + ((int64_t)h * M_v + r0) * words_row, kv_cnt + (int64_t)h * M_v + r0,
-                         s);
+      rc = launch_select(scratch, true, nr, M_v, M_total, adja ? adja + (int64_t)r0 * words : nullptr,
+                         words, n_floor, p, 1, bits + ((int64_t)h * M_v + r0) * words,
+                         kv_cnt + (int64_t)h * M_v + r0, s, fasts);
       if (rc) return rc;
     }
   }

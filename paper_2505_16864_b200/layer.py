@@ -8,7 +8,7 @@ the sparse flash-attention of head h read only head h.  With host inputs the lay
 therefore runs as a head-chunked pipeline on three CUDA streams --
 
     copy stream   H2D  q/k/v[chunk c+1]
-    compute       pool -> fused scores/select -> carve on chunk c
+    compute       pool -> scores/select (no R) -> carve on chunk c
     copy stream   D2H  out[chunk c-1]
 
 -- so the PCIe transfers overlap the kernels and each other (PCIe is full duplex).
@@ -24,7 +24,7 @@ import torch
 from . import _dev, _native
 from .attention import AmplifierBias, _workspace
 from .errors import ShapeError
-from .masks import BlockMask, SelectionParams, fused_scratch, launch_mask, mask_buffers
+from .masks import BlockMask, SelectionParams, mask_scratch, launch_mask, mask_buffers
 from .partition import BlockLayout, StaticMasks
 
 __all__ = ["carve_layer", "CarveLayerGraph"]
@@ -42,7 +42,7 @@ def _copy_streams(dev: torch.device):
 
 def _launch_chunk(q, k, v, o, pq, pk, bits, kv_cnt, scratch, adja, layout, params, beta, work,
                   sptr):
-    """pool -> fused scores/select/union -> carve on head-slice views (H_c, N, d)."""
+    """pool -> scores/select/union (no R) -> carve on head-slice views (H_c, N, d)."""
     Hc, _, d = q.shape
     sh, sn = q.stride(0), q.stride(1)
     Mv, Mt = layout.M_v, layout.M_total
@@ -99,7 +99,7 @@ def carve_layer(q, k, v, layout: BlockLayout, statics: StaticMasks, params: Sele
     pq = torch.empty((H, Mt, d), dtype=torch.float64, device=dev)
     pk = torch.empty_like(pq)
     bits, kv_cnt = mask_buffers(H, layout, dev)
-    scratch = fused_scratch(layout, d, params.p, dev)
+    scratch = mask_scratch(H, layout, dev)
     adja = statics.packed(layout)
     work = _workspace(dev)
 
@@ -133,7 +133,7 @@ class CarveLayerGraph:
     """One carved-attention layer captured as a CUDA graph on fixed device buffers.
 
     A DiT runs the same layer geometry every step, so the launches
-    (pool -> fused scores/select/union -> carve) and the carve kernel's work-counter reset are
+    (pool -> scores/select/union (no R) -> carve) and the carve kernel's work-counter reset are
     recorded once and replayed with one ``cudaGraphLaunch``.  Like ``torch.cuda.CUDAGraph``
     the buffers are static: write the step's Q/K/V into ``q``/``k``/``v`` (or pass the
     tensors the caller already fills in place), call :meth:`replay`, read ``out`` and
@@ -160,7 +160,7 @@ class CarveLayerGraph:
         self._pq = torch.empty((H, Mt, d), dtype=torch.float64, device=dev)
         self._pk = torch.empty_like(self._pq)
         self._bits, self._kv_cnt = mask_buffers(H, layout, dev)
-        self._scratch = fused_scratch(layout, d, params.p, dev)
+        self._scratch = mask_scratch(H, layout, dev)
         self._adja = statics.packed(layout)
         self._work = torch.zeros(16, dtype=torch.int32, device=dev)  # private: replays may overlap
         self.mask = BlockMask(words=self._bits, kv_cnt=self._kv_cnt, M_total=Mt, nonempty=True)

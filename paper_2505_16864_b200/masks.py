@@ -7,9 +7,10 @@ accumulation -> pooled means bit-exact with masks.py:112-116) and then either
   numpy's pairwise sums, masks.py:132-134, radix-select of the top n_keep under the stable
   descending order, the exact sequential prefix cutoff, and the union with the condition
   columns and the packed adjacency, masks.py:137-175), R left in place; or
-* (``need_relevance=False``: the layer path) ``tcb_block_mask_fused``: scores of an 8-row
-  tile on the FP64 tensor core into shared memory and the same selection there, R never
-  written (p == 0 selects on the scores themselves, the softmax being monotone).
+* (``need_relevance=False``: the layer path) ``tcb_block_mask``: the same scores into a
+  bounded scratch (never an R tensor beyond 256 MB) and the same selection; at p == 0 it
+  selects on the scores themselves (the softmax is monotone) and re-runs near-tie rows
+  through the exact softmax program.
 The mask is packed (H, M_v, words) uint32 plus row counts; the attention kernel walks the
 set bits of a row in ascending order.
 """
@@ -275,8 +276,9 @@ def build_block_mask(q, k, layout: BlockLayout, statics: StaticMasks, params: Se
 
     With R (the reference's return value): pool, float64 scores into R, and the row-softmax +
     selection + union kernel that leaves R in place -- three launches.  ``need_relevance=False``
-    (keyword extension; returns ``(mask, None)``) runs the fused kernel that never writes R:
-    pool + one scores-and-select launch (plus an exact re-run of undecided rows)."""
+    (keyword extension; returns ``(mask, None)``) never materialises R: the scores go to a
+    bounded scratch and, at p == 0, the selection runs on them directly (plus an exact re-run
+    of near-tie rows) -- bitwise the same mask."""
     qd, kd = _poolable(q), _poolable(k)
     if qd.dtype != kd.dtype:
         qd, kd = qd.to(torch.float64), kd.to(torch.float64)
@@ -293,20 +295,20 @@ def mask_buffers(H: int, layout: BlockLayout, device):
             torch.empty((H, layout.M_v), dtype=torch.int32, device=device))
 
 
-def fused_scratch(layout: BlockLayout, d: int, p: float, device):
-    """Score scratch the fused mask launch needs for this shape (None: none)."""
-    n = _native.query("tcb_block_mask_fused_scratch", layout.M_v, layout.M_total, d, float(p))
-    return None if n == 0 else torch.empty(n, dtype=torch.float64, device=device)
+def mask_scratch(H: int, layout: BlockLayout, device) -> torch.Tensor:
+    """Score scratch of the R-free mask launch (all heads up to 256 MB, else a bounded chunk)."""
+    n = _native.query("tcb_block_mask_scratch", H, layout.M_v, layout.M_total)
+    return torch.empty(n, dtype=torch.float64, device=device)
 
 
 def launch_mask(pq: torch.Tensor, pk: torch.Tensor, layout: BlockLayout, adja, params,
-                bits: torch.Tensor, kv_cnt: torch.Tensor, stream: int, scratch=None) -> None:
-    """The fused scores + select + union launch on pooled (H, M_total, d) float64 means."""
+                bits: torch.Tensor, kv_cnt: torch.Tensor, stream: int, scratch: torch.Tensor) -> None:
+    """Scores -> select -> union on pooled (H, M_total, d) float64 means, no R returned."""
     H, _, d = pq.shape
-    _native.call("tcb_block_mask_fused", pq.data_ptr(), pq.shape[1], pk.data_ptr(), H, layout.M_v,
+    _native.call("tcb_block_mask", pq.data_ptr(), pq.shape[1], pk.data_ptr(), H, layout.M_v,
                  layout.M_total, d, _native.ptr(adja), mask_words(layout.M_total),
                  params.n_floor(layout.M_v), float(params.p), bits.data_ptr(), kv_cnt.data_ptr(),
-                 _native.ptr(scratch), 0 if scratch is None else scratch.numel(), stream)
+                 scratch.data_ptr(), scratch.numel(), stream)
 
 
 def _build_block_mask(qd, kd, layout, statics, params, host, need_relevance=True):
@@ -317,7 +319,7 @@ def _build_block_mask(qd, kd, layout, statics, params, host, need_relevance=True
     adja = statics.packed(layout)
     if not need_relevance:
         launch_mask(pq.values, pk.values, layout, adja, params, bits, kv_cnt, _dev.stream(),
-                    fused_scratch(layout, d_k, params.p, qd.device))
+                    mask_scratch(H, layout, qd.device))
         R = None
     else:
         R = torch.empty((H, layout.M_v, layout.M_total), dtype=torch.float64, device=qd.device)

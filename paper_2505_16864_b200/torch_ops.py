@@ -7,7 +7,7 @@ without breaking the graph at every layer.  The ops launch the same sm_100a kern
 current stream as the ``tokencarve``-API functions:
 
 * ``tokencarve::block_mask(q, k, adja_bits, m, M_v, M_total, n_valid, n_cond, n_floor, p)``
-  -> (words, kv_cnt): pool -> fused scores/select/union (masks.py:178-199);
+  -> (words, kv_cnt): pool -> scores/select/union (no R) (masks.py:178-199);
 * ``tokencarve::carve(q, k, v, words, kv_cnt, m, M_v, M_total, n_valid, n_cond, beta)``
   -> out: block-sparse attention (attention.py:209-243).
 """
@@ -28,7 +28,7 @@ __all__ = ["block_mask", "carve"]
 def block_mask(q: torch.Tensor, k: torch.Tensor, adja_bits: torch.Tensor, m: int, M_v: int,
                M_total: int, n_valid: int, n_cond: int, n_floor: int,
                p: float) -> tuple[torch.Tensor, torch.Tensor]:
-    from .masks import fused_scratch, launch_mask, mask_buffers
+    from .masks import mask_scratch, launch_mask, mask_buffers
     from .partition import BlockLayout
 
     H, _, d = q.shape
@@ -43,7 +43,7 @@ def block_mask(q: torch.Tensor, k: torch.Tensor, adja_bits: torch.Tensor, m: int
                      q.stride(0), q.stride(1), H, d, m, M_v, M_total, n_valid, n_cond,
                      pq.data_ptr(), pk.data_ptr(), s)
         launch_mask(pq, pk, lay, adja_bits, _Floor(n_floor, p), bits, kv_cnt, s,
-                    fused_scratch(lay, d, p, dev))
+                    mask_scratch(H, lay, dev))
     return bits, kv_cnt
 
 

@@ -553,10 +553,10 @@ def test_carve_fp16_tcgen05_and_pool(d):
     assert np.all(got[:, ~oracle.token_valid(L)] == 0.0)
 
 
-# ----------------------------------------------------------------- fused scores + select
+# ----------------------------------------------------------------- R-free mask path
 FUSED_CASES = [
-    # (dims, m, n_cond, d, H, k, p): fused kernel (d 64 / 128, incl. the cutoff path and a
-    # crossing beyond the 512-wide window), the bounded-scratch path (d = 96; 7,201 blocks)
+    # (dims, m, n_cond, d, H, k, p): p == 0 (score-order fast path) and the cutoff path incl.
+    # a crossing beyond the 512-wide window; d = 96; 7,201 blocks (scratch in row chunks)
     ((5, 12, 16), 128, 40, 128, 3, 0.1, 0.0),
     ((5, 12, 16), 128, 40, 128, 3, 0.2, 0.3),
     ((4, 10, 12), 8, 12, 64, 2, 0.3, 0.3),
@@ -570,7 +570,7 @@ FUSED_CASES = [
 
 @pytest.mark.parametrize("case", FUSED_CASES)
 def test_fused_mask_equals_unfused(case):
-    """need_relevance=False (fused tiles, no R in global memory; p == 0 selects on the
+    """need_relevance=False (no R returned: scores in a bounded scratch, p == 0 selects on the
     scores) gives bitwise the mask of the R-materialising path, and both match the oracle
     on sampled rows."""
     dims, m, nc, d, H, k, p = case

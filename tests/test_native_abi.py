@@ -69,14 +69,13 @@ def test_error_mapping_without_gpu():
         _native.call("tcb_block_select", 1, 1, 9000, 9000, None, 300, 1, 0.0, 1, 1, 1, None)
     with pytest.raises(DomainError):
         _native.call("tcb_block_select", 1, 1, 4, 4, None, 1, 0, 0.0, 1, 1, 1, None)
-    with pytest.raises(DomainError):  # fused mask: p outside [0, 1)
-        _native.call("tcb_block_mask_fused", 1, 4, 1, 1, 4, 4, 128, None, 1, 1, 1.0, 1, 1, None, 0,
-                     None)
-    # the fused kernel covers C2 (no scratch); a long row or d = 96 needs a bounded chunk
-    assert _native.query("tcb_block_mask_fused_scratch", 929, 931, 128, 0.0) == 0
-    assert _native.query("tcb_block_mask_fused_scratch", 929, 931, 128, 0.3) == 0
-    assert 0 < _native.query("tcb_block_mask_fused_scratch", 8190, 8192, 128, 0.3) <= 32 << 20
-    assert _native.query("tcb_block_mask_fused_scratch", 929, 931, 96, 0.0) == 929 * 931
+    with pytest.raises(DomainError):  # R-free mask: p outside [0, 1)
+        _native.call("tcb_block_mask", 1, 4, 1, 1, 4, 4, 128, None, 1, 1, 1.0, 1, 1, 1, 4, None)
+    with pytest.raises(SizeError):  # scratch below one row
+        _native.call("tcb_block_mask", 1, 4, 1, 1, 4, 4, 128, None, 1, 1, 0.0, 1, 1, 1, 3, None)
+    # all C2 heads' scores fit the 256 MB cap; the 8,192-block maximum is chunked under it
+    assert _native.query("tcb_block_mask_scratch", 24, 929, 931) == 24 * 929 * 931
+    assert 8192 <= _native.query("tcb_block_mask_scratch", 24, 8190, 8192) <= 32 << 20
     # fused neighbours: bad rope sections / strides / patch sizes / grid mismatch
     import ctypes as C
     one = (C.c_void_p * 1)(16)
