@@ -181,36 +181,30 @@ def run_gpu(args):
         def step(marks=None):
             return layer(q, k, v, o, marks)
     else:
-        from paper_2505_16864_b200.ulysses import head_to_seq, seq_to_head
+        from paper_2505_16864_b200.ulysses import carve_layer_sp, default_chunks, to_exchange_layout
 
-        oh = torch.empty((Np, Hl, D), dtype=torch.bfloat16, device=dev)
+        # token shards held in the exchange layout (C, G, n_loc, hc, d): the collectives send
+        # and receive them without repacking (ulysses.py); converted once, outside the loop
+        if args.a2a_chunks is None:
+            args.a2a_chunks = default_chunks(Hl)
+        C = args.a2a_chunks
+        q, k, v = (to_exchange_layout(t, world, C) for t in (q, k, v))
+        chunk = [0]
 
-        if args.a2a_chunks > 1:
-            from paper_2505_16864_b200.ulysses import carve_layer_sp_chunked
+        def local(qh, kh, vh, _lay, out):
+            h0 = chunk[0] * qh.shape[0]  # mask buffers of this chunk's heads
+            chunk[0] += 1
+            layer(qh, kh, vh, out, h0=h0)
 
-            chunk = [0]
-
-            def local(qh, kh, vh, _lay):
-                out = torch.empty_like(qh)  # same (token-major) strides as the inputs
-                h0 = chunk[0] * qh.shape[0]
-                chunk[0] += 1
-                return layer(qh, kh, vh, out, h0=h0)
-
-            def step(marks=None):
-                chunk[0] = 0
-                if marks:  # per-kernel marks are per chunk here; time the whole layer only
-                    marks[0].record()
-                r = carve_layer_sp_chunked(q, k, v, layout, local, chunks=args.a2a_chunks)
-                if marks:
-                    for mk in marks[1:]:
-                        mk.record()
-                return r
-        else:
-            def step(marks=None):
-                qh, kh, vh = seq_to_head([q, k, v])
-                layer(qh.permute(1, 0, 2), kh.permute(1, 0, 2), vh.permute(1, 0, 2),
-                      oh.permute(1, 0, 2), marks)
-                return head_to_seq(oh)
+        def step(marks=None):
+            chunk[0] = 0
+            if marks:  # per-kernel marks do not separate the exchange: time the whole layer
+                marks[0].record()
+            r = carve_layer_sp(q, k, v, layout, local, chunks=C)
+            if marks:
+                for mk in marks[1:]:
+                    mk.record()
+            return r
 
     red_dev = "cpu" if args.dist_backend == "gloo" else dev  # device of the scalar reductions
 
@@ -249,7 +243,7 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
     k_pool, k_sel, k_carve = per.mean(axis=0)
-    chunked = world > 1 and args.a2a_chunks > 1
+    chunked = world > 1
     if chunked:  # per-kernel marks do not separate the pipelined chunks: use the layer time
         k_pool = k_sel = float("nan")
         k_carve = ms_step
@@ -291,13 +285,13 @@ def run_gpu(args):
             path = ("per rank: pinned host token shard -> H2D -> ulysses.carve_layer_sp (all-to-all, "
                     "build_block_mask + carve_attention on the head shard, all-to-all) -> D2H")
 
-            def local_api(qh, kh, vh, lay):
+            def local_api(qh, kh, vh, lay, out):
                 mask, _ = tcb.build_block_mask(qh, kh, lay, statics, params, need_relevance=False)
-                return tcb.carve_attention(tcb.AttentionInputs(q=qh, k=kh, v=vh, layout=lay), mask)
+                tcb.carve_raw(qh, kh, vh, mask, lay, 0.0, out=out)
 
             def e2e_step():
                 dq, dk, dv = (t.to(dev, non_blocking=True) for t in (hq, hk, hv))
-                o_sh = carve_layer_sp(dq, dk, dv, layout, local_api)
+                o_sh = carve_layer_sp(dq, dk, dv, layout, local_api, chunks=args.a2a_chunks)
                 ho.copy_(o_sh, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
 
@@ -348,7 +342,7 @@ def run_gpu(args):
         "config": {"workload": WORKLOAD, "tokens": Np, "heads": H, "d": D, "block": M,
                    "k": K_RATE, "p": P_CUT, "kept_pairs": pairs,
                    "kept_fraction": round(pairs / (H * Mt * Mt), 4),
-                   "parallelism": (f"ulysses-heads{world}" + (f"-a2a{args.a2a_chunks}chunks" if chunked else ""))
+                   "parallelism": (f"ulysses-heads{world}-a2a{args.a2a_chunks}chunks-exchange-layout")
                    if world > 1 else "single",
                    "l2": "no flush: Q/K/V/O = 2.9 GB per layer > 126 MB L2"},
         "kept_block_tflops": round(carve_tflops, 1),
@@ -369,7 +363,7 @@ def run_gpu(args):
                      "hbm_peak_gbs": hbm},
         "e2e": e2e,
         "cpu_baseline": cpu,
-        "gpu_launches": 5 * args.steps * (min(args.a2a_chunks, Hl) if chunked else 1),
+        "gpu_launches": 5 * args.steps * (args.a2a_chunks if chunked else 1),
         "launches_per_layer": "k_pool, k_scores_dmma, k_select (scores, p=0 fast path), k_select "
                               "(exact re-run of near-tie rows only), k_carve_tc",
         "clocks": clk.result,
@@ -554,8 +548,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--a2a-chunks", type=int, default=1,
-                    help="N>1: pipeline the Ulysses all-to-all over this many head chunks")
+    ap.add_argument("--a2a-chunks", type=int, default=None,
+                    help="N>1: pipeline the Ulysses all-to-all over this many head chunks "
+                         "(default: 2 when a rank holds an even number >= 2 of heads)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help=argparse.SUPPRESS)
     args = ap.parse_args()

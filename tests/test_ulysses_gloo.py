@@ -1,5 +1,7 @@
 """World-size-2 gloo test (CPU) of the Ulysses sequence<->head exchange around a
-per-head attention: sharded result == unsharded oracle result."""
+per-head attention: sharded result == unsharded oracle result, for the packed (n_loc, H, d)
+input, the pipelined exchange, and inputs already in the (C, G, n_loc, hc, d) exchange
+layout."""
 
 import os
 import socket
@@ -34,7 +36,8 @@ def _case():
 def _worker(rank, world, port, out_path, chunks=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2505_16864_b200.ulysses import carve_layer_sp, carve_layer_sp_chunked
+    from paper_2505_16864_b200.ulysses import (carve_layer_sp, carve_layer_sp_chunked,
+                                               from_exchange_layout, to_exchange_layout)
 
     dims, L, q, k, v, adja = _case()
     N = L["padded_total"]
@@ -43,21 +46,25 @@ def _worker(rank, world, port, out_path, chunks=0):
     def shard(x):  # (H, N, d) -> token shard (N/G, H, d)
         return torch.from_numpy(np.ascontiguousarray(x.transpose(1, 0, 2)[rank * n_loc:(rank + 1) * n_loc]))
 
-    def local(qh, kh, vh, layout):
-        # per-head layer on the head shard: mask build + carve (oracle stands in for the kernels)
+    def local(qh, kh, vh, layout, out):
+        # per-head layer on the head shard: mask build + carve (the exchange is what is tested
+        # here; tests/test_gpu_ulysses.py runs the same exchange around the real kernels)
         qn, kn, vn = (t.contiguous().numpy() for t in (qh, kh, vh))
         bits, _ = oracle.block_mask(qn, kn, L, adja, 0.3, 0.3)
-        return torch.from_numpy(oracle.carve(qn, kn, vn, bits, L, 0.25))
+        out.copy_(torch.from_numpy(oracle.carve(qn, kn, vn, bits, L, 0.25)))
 
-    if chunks:
+    if chunks == -1:  # inputs already in the exchange layout: no packing at all
+        xs = [to_exchange_layout(shard(x), world, 2) for x in (q, k, v)]
+        o = carve_layer_sp(*xs, None, local, chunks=None)
+    elif chunks:
         o = carve_layer_sp_chunked(shard(q), shard(k), shard(v), None, local, chunks=chunks)
     else:
         o = carve_layer_sp(shard(q), shard(k), shard(v), None, local)
-    torch.save(o, f"{out_path}.{rank}")
+    torch.save(from_exchange_layout(o, contiguous=True), f"{out_path}.{rank}")
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("chunks", [0, 1, 2])
+@pytest.mark.parametrize("chunks", [0, 1, 2, -1])
 def test_ulysses_roundtrip_world2(tmp_path, chunks):
     if not dist.is_gloo_available():
         pytest.skip("gloo missing")
