@@ -145,6 +145,20 @@ int tcb_carve_fwd_simt(const void* q, const void* k, const void* v, void* o, int
                        const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
                        int64_t n_valid, int64_t n_cond, float beta, void* stream);
 
+/* K7/K8 for fp32 inputs on the tensor cores (the reference's own dtype, attention.py:184-201).
+ * Every fp32 operand is split into fp16 hi + lo (scaled by a power of two per tensor/head or
+ * per query row) and each product is taken as hi.hi + hi.lo + lo.hi on tcgen05 kind::f16 with
+ * fp32 accumulation: within 1e-5 of the reference.  workspace: device scratch of
+ * tcb_carve_f32_workspace_bytes() bytes, 256-byte aligned (split K / V planes).  Shapes the
+ * tensor-core kernel does not take (m != 128, d not in {64,128}, no workspace, misaligned)
+ * run the fp32 SIMT kernel instead.  work: as tcb_carve_fwd. */
+int64_t tcb_carve_f32_workspace_bytes(int H, int M_total, int m, int d);  /* 0: not applicable */
+int tcb_carve_fwd_f32(const float* q, const float* k, const float* v, float* o, int64_t stride_h,
+                      int64_t stride_n, const uint32_t* bits, int words, const int32_t* kv_cnt,
+                      int H, int d, int m, int M_v, int M_total, int64_t n_valid, int64_t n_cond,
+                      float beta, void* workspace, int64_t workspace_bytes, int32_t* work,
+                      void* stream);
+
 /* K9/K10 -- fused predict_clean -> area upsample -> re-noise.
  * Replaces predict_clean (pipeline.py:124-128), upsample_area_3d
  * (pipeline.py:153-173) and stage_transition (pipeline.py:176-194).

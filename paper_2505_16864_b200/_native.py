@@ -44,6 +44,9 @@ SIGNATURES = {
                       _I64, _F, _P, _P],
     "tcb_carve_fwd_simt": [_P, _P, _P, _P, _I, _I64, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _I64,
                            _I64, _F, _P],
+    "tcb_carve_f32_workspace_bytes": [_I, _I, _I, _I],
+    "tcb_carve_fwd_f32": [_P, _P, _P, _P, _I64, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _I64, _I64,
+                          _F, _P, _I64, _P, _P],
     "tcb_upsample_renoise": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _D, _I, _U64, _U64, _P],
     "tcb_euler_step": [_P, _P, _P, _I64, _F, _P],
     "tcb_euler_step_f64": [_P, _P, _P, _I64, _D, _P],
@@ -58,6 +61,9 @@ SIGNATURES = {
     "tcb_rope_permute": [_P, _I64, _I64, _P, _I64, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _P, _I,
                          _I, _I, _P],
 }
+
+
+_I64_RESULT = ("tcb_block_mask_scratch", "tcb_carve_f32_workspace_bytes")
 
 
 class NativeUnavailable(RuntimeError):
@@ -84,7 +90,7 @@ def load():
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = (C.c_char_p if name == "tcb_last_error" else
-                          C.c_int64 if name == "tcb_block_mask_scratch" else C.c_int)
+                          C.c_int64 if name in _I64_RESULT else C.c_int)
         _lib = lib
     return _lib
 

@@ -113,6 +113,13 @@ def carve_raw(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: BlockMask
                 layout.n_cond, float(beta))
         if simt:
             _native.call("tcb_carve_fwd_simt", *args, _dev.stream())
+        elif q.dtype == torch.float32:
+            # fp32 on the tensor cores (split-fp16 products); the library runs the SIMT kernel
+            # itself for shapes that path does not take (workspace size 0)
+            nb = _native.query("tcb_carve_f32_workspace_bytes", H, layout.M_total, layout.m, d)
+            ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=q.device)
+            _native.call("tcb_carve_fwd_f32", *args[:4], *args[5:], ws.data_ptr(), nb,
+                         _workspace(q.device).data_ptr(), _dev.stream())
         else:
             _native.call("tcb_carve_fwd", *args, _workspace(q.device).data_ptr(), _dev.stream())
     return out
