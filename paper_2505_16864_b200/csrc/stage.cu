@@ -77,12 +77,23 @@ __global__ void __launch_bounds__(256, 4) k_upsample_renoise(
   // division beyond the group split, and the t / h taps are uniform across the CTA
   const int groups = C / VEC;
   const int x_ = blockIdx.x * blockDim.x + threadIdx.x;
+  const int oh = blockIdx.y, ot = blockIdx.z;
+  // the float64 tap weights (divisions, floor / ceil) are computed once per CTA: t / h taps
+  // are uniform over the CTA's output row, w taps once per distinct output column (the
+  // per-thread version spent ~80 % of its instructions here)
+  __shared__ Taps s_th[2];
+  __shared__ Taps s_tw[256];
+  const int ow_lo = (blockIdx.x * blockDim.x) / groups;
+  const int ow_hi = min(dw - 1, (int)((blockIdx.x * blockDim.x + blockDim.x - 1) / groups));
+  for (int i = threadIdx.x; i <= ow_hi - ow_lo; i += blockDim.x) s_tw[i] = axis_taps(ow_lo + i, sw, dw);
+  if (threadIdx.x == 0) s_th[0] = axis_taps(ot, st, dt);
+  if (threadIdx.x == min(32, (int)blockDim.x - 1)) s_th[1] = axis_taps(oh, sh, dh);
+  __syncthreads();
   if (x_ >= dw * groups) return;
   const int ow = x_ / groups;
   const int c0 = (x_ - ow * groups) * VEC;
-  const int oh = blockIdx.y, ot = blockIdx.z;
   const int cell = (ot * dh + oh) * dw + ow;
-  const Taps tt = axis_taps(ot, st, dt), th = axis_taps(oh, sh, dh), tw = axis_taps(ow, sw, dw);
+  const Taps tt = s_th[0], th = s_th[1], tw = s_tw[ow - ow_lo];
   // Always two taps per axis: a missing second tap repeats the first index with weight 0,
   // and 0 * x adds an exact zero -- as the reference's dense tensordot rows do.
   const int ti[2] = {tt.i0, tt.n > 1 ? tt.i0 + 1 : tt.i0};
