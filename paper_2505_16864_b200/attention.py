@@ -1,10 +1,11 @@
 """Block-sparse attention over the carve mask (reference: tokencarve attention.py).
 
-``carve_attention`` is one launch of ``tcb_carve_fwd``: bf16 inputs with m=128 and
-d in {64, 128} run the persistent tcgen05/TMEM/TMA kernel; fp32 inputs (the
-reference's own dtype) and other shapes run the fp32 SIMT kernel that mirrors the
-reference's per-block streaming order (attention.py:162-206).  The output has the
-input dtype; numpy inputs come back as float32 numpy like the reference.
+``carve_attention`` is one carve launch: bf16 / fp16 inputs with m=128 and d in {64, 128}
+run the persistent tcgen05/TMEM/TMA kernel (``tcb_carve_fwd``); fp32 inputs (the
+reference's own dtype) with those shapes run the tensor-core split-fp16 kernel
+(``tcb_carve_fwd_f32``, within 1e-5 of the reference); other shapes run the fp32 SIMT
+kernels that mirror the reference's per-block streaming order (attention.py:162-206).  The
+output has the input dtype; numpy inputs come back as float32 numpy like the reference.
 """
 
 from __future__ import annotations
@@ -99,7 +100,6 @@ def carve_raw(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: BlockMask
     if not (q.shape == k.shape == v.shape) or q.ndim != 3:
         raise ShapeError(f"q/k/v must share one (heads, N, d_k) shape")
     _dev.same_device(q, k, v, mask.words, *(() if out is None else (out,)))
-    H, N, d = q.shape
     if k.stride() != q.stride() or v.stride() != q.stride() or q.stride(2) != 1:
         q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     with _dev.on(q):
@@ -107,22 +107,29 @@ def carve_raw(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mask: BlockMask
             out = torch.empty_like(q)
         if out.stride() != q.stride() or out.dtype != q.dtype or out.shape != q.shape:
             raise ShapeError("output must share the inputs' shape, dtype and strides")
-        args = (q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), _dev.code_of(q.dtype),
-                q.stride(0), q.stride(1), mask.words.data_ptr(), mask.words.shape[-1],
-                mask.kv_cnt.data_ptr(), H, d, layout.m, layout.M_v, layout.M_total, layout.n_valid,
-                layout.n_cond, float(beta))
-        if simt:
-            _native.call("tcb_carve_fwd_simt", *args, _dev.stream())
-        elif q.dtype == torch.float32:
-            # fp32 on the tensor cores (split-fp16 products); the library runs the SIMT kernel
-            # itself for shapes that path does not take (workspace size 0)
-            nb = _native.query("tcb_carve_f32_workspace_bytes", H, layout.M_total, layout.m, d)
-            ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=q.device)
-            _native.call("tcb_carve_fwd_f32", *args[:4], *args[5:], ws.data_ptr(), nb,
-                         _workspace(q.device).data_ptr(), _dev.stream())
-        else:
-            _native.call("tcb_carve_fwd", *args, _workspace(q.device).data_ptr(), _dev.stream())
+        launch_carve(q, k, v, out, mask.words, mask.kv_cnt, layout.m, layout.M_v, layout.M_total,
+                     layout.n_valid, layout.n_cond, beta, simt)
     return out
+
+
+def launch_carve(q, k, v, out, words, kv_cnt, m, M_v, M_total, n_valid, n_cond, beta,
+                 simt: bool = False) -> None:
+    """The carve launch shared by carve_raw and the torch op: bf16 / fp16 -> tcgen05 kernel;
+    fp32 -> tensor-core split-fp16 kernel (the library itself falls back to the fp32 SIMT
+    kernel for shapes that path does not take); ``simt`` forces the fp32 SIMT kernel."""
+    H, N, d = q.shape
+    args = (q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), _dev.code_of(q.dtype),
+            q.stride(0), q.stride(1), words.data_ptr(), words.shape[-1], kv_cnt.data_ptr(), H, d,
+            m, M_v, M_total, n_valid, n_cond, float(beta))
+    if simt:
+        _native.call("tcb_carve_fwd_simt", *args, _dev.stream())
+    elif q.dtype == torch.float32:
+        nb = _native.query("tcb_carve_f32_workspace_bytes", H, M_total, m, d)
+        ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=q.device)
+        _native.call("tcb_carve_fwd_f32", *args[:4], *args[5:], ws.data_ptr(), nb,
+                     _workspace(q.device).data_ptr(), _dev.stream())
+    else:
+        _native.call("tcb_carve_fwd", *args, _workspace(q.device).data_ptr(), _dev.stream())
 
 
 def carve_attention(inputs: AttentionInputs, mask: BlockMask,

@@ -17,7 +17,7 @@ from __future__ import annotations
 import torch
 
 from . import _dev, _native
-from .attention import _workspace
+from .attention import launch_carve
 from .errors import ShapeError
 from .partition import mask_words
 
@@ -73,14 +73,9 @@ def carve(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, bits: torch.Tensor,
         raise ShapeError(f"q/k/v dtypes differ: {q.dtype}, {k.dtype}, {v.dtype}")
     if k.stride() != q.stride() or v.stride() != q.stride() or q.stride(2) != 1:
         q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-    H, _, d = q.shape
     with torch.cuda.device(q.device):
         out = torch.empty_like(q)
-        _native.call("tcb_carve_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
-                     _dev.code_of(q.dtype), q.stride(0), q.stride(1), bits.data_ptr(),
-                     bits.shape[-1], kv_cnt.data_ptr(), H, d, m, M_v, M_total, n_valid, n_cond,
-                     float(beta), _workspace(q.device).data_ptr(),
-                     torch.cuda.current_stream(q.device).cuda_stream)
+        launch_carve(q, k, v, out, bits, kv_cnt, m, M_v, M_total, n_valid, n_cond, beta)
     return out
 
 
