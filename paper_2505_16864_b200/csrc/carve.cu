@@ -440,7 +440,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       const bool vis = qb < s.M_v;
       const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
       const uint32_t* brow = bits + ((int64_t)h * s.M_v + (vis ? qb : 0)) * s.W;
-      BitWalk wk(brow), wv(brow);  // K runs one half-step ahead of V: one walk per stream
+      // K runs one half-step ahead of V: one walk per stream (cond rows never walk)
+      WarpKvList wk(vis ? brow : nullptr, s.W, lane), wv(vis ? brow : nullptr, s.W, lane);
       const int T = 2 * n;
       if (lane == 0) {
         ptx::mbar_wait(&bars->q_empty, (it & 1) ^ 1);
@@ -450,8 +451,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
           ptx::tma_load_3d(sQ + c * L::Q_CHUNK, &tm_q, &bars->q_full, c * 64, qb * BM, h, pol_q);
       }
       auto load = [&](const CUtensorMap* tm, uint8_t* base, uint64_t* full, uint64_t* empty,
-                      int slots, uint32_t& cnt, int t, BitWalk& walk) {
-        const int b = vis ? walk.get(t >> 1) : (t >> 1);
+                      int slots, uint32_t& cnt, int t, WarpKvList& walk) {
+        const int b = vis ? walk.block(t >> 1) : (t >> 1);
         if (lane == 0) {
           const int sl = cnt % slots;
           ptx::mbar_wait(&empty[sl], ((cnt / slots) & 1) ^ 1);
@@ -579,16 +580,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       decode_item(item, s, h, qb);
       const bool vis = qb < s.M_v;
       const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      BitWalk bw(bits + ((int64_t)h * s.M_v + (vis ? qb : 0)) * s.W);
+      // the block index itself is not needed here: only where condition keys start and
+      // which entries can be partial blocks (RowShape); condition q-blocks visit 0..M_total-1
+      const RowShape rs = vis ? RowShape(bits + ((int64_t)h * s.M_v + qb) * s.W, s.W, lane, BK, s.M_v,
+                                         s.M_total, s.n_valid, s.n_cond)
+                              : RowShape();
       const int T = 2 * n;
       float m_run = -INFINITY, l_run = 0.f;
-      int b = 0, kvalid = BK;
+      int kvalid = BK;
       float bias = 0.f;
       for (int t = 0; t < T; ++t, ++g) {
         if ((t & 1) == 0) {
-          b = vis ? bw.get(t >> 1) : (t >> 1);
-          kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond);
-          bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
+          const int j = t >> 1;
+          if (vis) {
+            kvalid = j == rs.n_vis - 1 ? rs.kv_last_vis : (j == n - 1 ? rs.kv_last : BK);
+            bias = j >= rs.n_vis ? beta_log2 : 0.f;
+          } else {
+            kvalid = block_valid(j, BK, s.M_v, s.n_valid, s.n_cond);
+          }
         }
         const int hvalid = kvalid - (t & 1) * HN;  // valid keys in this half (may be <= 0)
         if (lane == 0 && (warp & 3) == 2) TRACE(14, g);

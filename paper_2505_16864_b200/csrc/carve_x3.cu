@@ -215,11 +215,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool vis = qb < s.M_v;
       const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
       const uint32_t* brow = bits + ((int64_t)h * s.M_v + (vis ? qb : 0)) * s.W;
-      BitWalk wk(brow), wv(brow);
+      WarpKvList wk(vis ? brow : nullptr, s.W, lane), wv(vis ? brow : nullptr, s.W, lane);
       const int T = 2 * n;
       auto load = [&](const CUtensorMap* tm, uint8_t* base, uint64_t* full, uint64_t* empty,
-                      int slots, uint32_t& cnt, int t, BitWalk& walk) {
-        const int b = vis ? walk.get(t >> 1) : (t >> 1);
+                      int slots, uint32_t& cnt, int t, WarpKvList& walk) {
+        const int b = vis ? walk.block(t >> 1) : (t >> 1);
         if (lane == 0) {
           const int sl = cnt % slots;
           ptx::mbar_wait(&empty[sl], ((cnt / slots) & 1) ^ 1);
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       decode_item(item, s, h, qb);
       const bool vis = qb < s.M_v;
       const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      BitWalk bw(bits + ((int64_t)h * s.M_v + (vis ? qb : 0)) * s.W);
+      WarpKvList bw(vis ? bits + ((int64_t)h * s.M_v + qb) * s.W : nullptr, s.W, lane);
       const int T = 2 * n;
       const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
       const bool live = row < qvalid;
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       float bias = 0.f;
       for (int t = 0; t < T; ++t, ++g) {
         if ((t & 1) == 0) {
-          b = vis ? bw.get(t >> 1) : (t >> 1);
+          b = vis ? bw.block(t >> 1) : (t >> 1);
           kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond);
           bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
         }
