@@ -18,6 +18,14 @@ pytestmark = pytest.mark.gpu
 tcb = pytest.importorskip("paper_2505_16864_b200")
 
 
+# Regression guards for the 16-bit tcgen05 kernel (the north_star bound, 2e-2 of max|ref|,
+# is asserted as well): ~3x the largest max|err|/max|ref| observed on B200 per family --
+# bf16 2.2e-3 .. 4.6e-3 over the golden cases, long rows, softmax extremes and 14 fuzzed
+# layouts; fp16 3.1e-4 / 3.3e-4.  A broken rescale or a dropped block shows up as >= 1e-2.
+BF16_GUARD = 1.4e-2
+FP16_GUARD = 1.0e-3
+
+
 def sha16(a):
     return hashlib.sha256(np.ascontiguousarray(np.asarray(a).astype("<i8")).tobytes()).hexdigest()[:16]
 
@@ -185,7 +193,9 @@ def test_carve_bf16_tcgen05_vs_oracle(case):
                        bits, L, P["beta"])
     got = out.float().cpu().numpy()
     err = np.abs(got - ref).max() / np.abs(ref).max()
+    print(f"[bf16-err] golden {case}: {err:.3e}")
     assert err <= 2e-2, err  # bf16 tolerance (north_star): 2e-2 relative to max|ref|
+    assert err <= BF16_GUARD, err
     assert np.all(got[:, ~oracle.token_valid(L)] == 0.0)
 
 
@@ -206,7 +216,9 @@ def test_carve_bf16_tcgen05_long_rows_and_determinism():
     ref = oracle.carve(q.float().cpu().numpy(), k.float().cpu().numpy(), v.float().cpu().numpy(),
                        _host(mask.bits), L, 0.7, workers=8)
     err = np.abs(o1.float().cpu().numpy() - ref).max() / np.abs(ref).max()
+    print(f"[bf16-err] long rows: {err:.3e}")
     assert err <= 2e-2, err  # 2e-2 relative to max|ref|
+    assert err <= BF16_GUARD, err
 
 
 def test_carve_contract_errors():
@@ -446,7 +458,9 @@ def test_carve_bf16_online_softmax_extremes(pattern):
     ref = oracle.carve(qb.float().cpu().numpy(), kb.float().cpu().numpy(), vb.float().cpu().numpy(),
                        bits, L, 0.5, workers=8)
     err = np.abs(got - ref).max() / np.abs(ref).max()
+    print(f"[bf16-err] extremes {pattern}: {err:.3e}")
     assert err <= 2e-2, err
+    assert err <= BF16_GUARD, err
 
 
 def test_carve_bf16_fuzz_random_layouts():
@@ -476,7 +490,9 @@ def test_carve_bf16_fuzz_random_layouts():
         ref = oracle.carve(q32, k32, v32, bits, L, beta, workers=8)
         got = out.float().cpu().numpy()
         err = np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30)
+        print(f"[bf16-err] fuzz {trial}: {err:.3e}")
         assert err <= 2e-2, (trial, dims.as_tuple(), n_cond, H, err)
+        assert err <= BF16_GUARD, (trial, err)
         o32 = tcb.carve_attention(tcb.AttentionInputs(q=q32, k=k32, v=v32, layout=lay),
                                   tcb.BlockMask(bits=bits), tcb.AmplifierBias(beta))
         np.testing.assert_allclose(o32, ref, rtol=1e-5, atol=1e-5)
@@ -549,7 +565,9 @@ def test_carve_fp16_tcgen05_and_pool(d):
     ref = oracle.carve(q32, k32, v32, _host(mask.bits), L, 0.3, workers=8)
     got = out.float().cpu().numpy()
     err = np.abs(got - ref).max() / np.abs(ref).max()
+    print(f"[bf16-err] fp16 d={d}: {err:.3e}")
     assert err <= 1e-2, err
+    assert err <= FP16_GUARD, err
     assert np.all(got[:, ~oracle.token_valid(L)] == 0.0)
 
 
