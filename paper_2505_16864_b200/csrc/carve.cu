@@ -589,17 +589,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       float m_run = -INFINITY, l_run = 0.f;
       int kvalid = BK;
       float bias = 0.f;
-      for (int t = 0; t < T; ++t, ++g) {
-        if ((t & 1) == 0) {
-          const int j = t >> 1;
-          if (vis) {
-            kvalid = j == rs.n_vis - 1 ? rs.kv_last_vis : (j == n - 1 ? rs.kv_last : BK);
-            bias = j >= rs.n_vis ? beta_log2 : 0.f;
-          } else {
-            kvalid = block_valid(j, BK, s.M_v, s.n_valid, s.n_cond);
-          }
+      // one iteration per kv block, its two 64-key half-steps unrolled (the half index and
+      // the per-block bookkeeping are then compile-time / once per block)
+      for (int j = 0; j < n; ++j) {
+        if (vis) {
+          kvalid = j == rs.n_vis - 1 ? rs.kv_last_vis : (j == n - 1 ? rs.kv_last : BK);
+          bias = j >= rs.n_vis ? beta_log2 : 0.f;
+        } else {
+          kvalid = block_valid(j, BK, s.M_v, s.n_valid, s.n_cond);
         }
-        const int hvalid = kvalid - (t & 1) * HN;  // valid keys in this half (may be <= 0)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf, ++g) {
+        const int t = 2 * j + hf;
+        const int hvalid = kvalid - hf * HN;  // valid keys in this half (may be <= 0)
         if (lane == 0 && (warp & 3) == 2) TRACE(14, g);
         ptx::mbar_wait(&bars->s_full[g & 1], (g >> 1) & 1);
         if (lane == 0 && (warp & 3) == 2) TRACE(10, g);
@@ -678,6 +680,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         ptx::tc_fence_before();
         ptx::mbar_arrive(&bars->p_full[g & 1]);
         if (lane == 0 && (warp & 3) == 2) TRACE(12, g);
+      }
       }
       // ---- epilogue: O / l -> bf16 row, padding rows zero (attention.py:203-206)
       ptx::mbar_wait(&bars->o_full, it & 1);
