@@ -640,7 +640,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         // p = 2^(s * scale_log2 + bias - m_use): one FFMA2 per two keys
         const float c0 = bias - m_use;
         const uint64_t sc2 = f2_pack(scale_log2, scale_log2), c02 = f2_pack(c0, c0);
-        uint64_t acc2[4] = {0, 0, 0, 0};
+        uint64_t acc2[4];
         uint32_t pk[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
             p0 = ptx::ex2(f2_lo(x));
             p1 = ptx::ex2(f2_hi(x));
           }
-          acc2[e & 3] = fadd2(acc2[e & 3], f2_pack(p0, p1));
+          acc2[e & 3] = e < 4 ? f2_pack(p0, p1) : fadd2(acc2[e & 3], f2_pack(p0, p1));
           pk[e] = Elem<E>::pack(p0, p1);
         }
         ptx::tmem_st32(t_row + (g & 1) * HN, pk);
