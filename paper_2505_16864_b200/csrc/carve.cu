@@ -446,9 +446,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       if (lane == 0) {
         ptx::mbar_wait(&bars->q_empty, (it & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(&bars->q_full, L::Q_BYTES);
-#pragma unroll
-        for (int c = 0; c < L::CHUNKS; ++c)
-          ptx::tma_load_3d(sQ + c * L::Q_CHUNK, &tm_q, &bars->q_full, c * 64, qb * BM, h, pol_q);
+        ptx::tma_load_4d(sQ, &tm_q, &bars->q_full, 0, qb * BM, 0, h, pol_q);
       }
       auto load = [&](const CUtensorMap* tm, uint8_t* base, uint64_t* full, uint64_t* empty,
                       int slots, uint32_t& cnt, int t, WarpKvList& walk) {
@@ -460,10 +458,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
             ptx::mbar_arrive(&full[sl]);
           } else {
             ptx::mbar_arrive_expect_tx(&full[sl], L::HALF_BYTES);
-#pragma unroll
-            for (int c = 0; c < L::CHUNKS; ++c)
-              ptx::tma_load_3d(base + sl * L::HALF_BYTES + c * L::H_CHUNK, tm, &full[sl], c * 64,
-                               b * BK + (t & 1) * HN, h, vis ? pol_kv : pol_q);
+            ptx::tma_load_4d(base + sl * L::HALF_BYTES, tm, &full[sl], 0, b * BK + (t & 1) * HN, 0, h,
+                             vis ? pol_kv : pol_q);
           }
         }
         ++cnt;
@@ -829,9 +825,9 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
   CUtensorMap tq, tk, tv;
   const int64_t n_pad = (int64_t)s.M_total * s.m;
   int rc;
-  if ((rc = make_tmap(&tq, q, D, n_pad, s.H, s.sh, s.sn, tc::BM, !tc::Elem<E>::kBf16))) return rc;
-  if ((rc = make_tmap(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::HN, !tc::Elem<E>::kBf16))) return rc;
-  if ((rc = make_tmap(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::HN, !tc::Elem<E>::kBf16))) return rc;
+  if ((rc = make_tmap_rows(&tq, q, D, n_pad, s.H, s.sh, s.sn, tc::BM, !tc::Elem<E>::kBf16))) return rc;
+  if ((rc = make_tmap_rows(&tk, k, D, n_pad, s.H, s.sh, s.sn, tc::HN, !tc::Elem<E>::kBf16))) return rc;
+  if ((rc = make_tmap_rows(&tv, v, D, n_pad, s.H, s.sh, s.sn, tc::HN, !tc::Elem<E>::kBf16))) return rc;
   const int smem = tc::Smem<D>::BYTES;
   static std::atomic<uint64_t> attr{0};
   {

@@ -149,6 +149,25 @@ static inline int make_tmap(CUtensorMap* tm, const void* base, int d, int64_t n_
   return TCB_OK;
 }
 
+// (64, N_pad, d/64, H) view of a (H, N_pad, d) 16-bit tensor with box (64, box_rows, d/64, 1):
+// one TMA request brings all 64-column chunks of a row range, landing chunk-major -- the
+// same shared-memory layout as d/64 separate 3D boxes (128-byte swizzle per chunk).
+static inline int make_tmap_rows(CUtensorMap* tm, const void* base, int d, int64_t n_pad, int H,
+                                 int64_t sh, int64_t sn, int box_rows, bool f16 = false) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return set_error(TCB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {64, (cuuint64_t)n_pad, (cuuint64_t)(d / 64), (cuuint64_t)H};
+  cuuint64_t strides[3] = {(cuuint64_t)sn * 2, 128, (cuuint64_t)sh * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, (cuuint32_t)(d / 64), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(tm, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(TCB_ECUDA, "cuTensorMapEncodeTiled (rows) failed (%d)", (int)r);
+  return TCB_OK;
+}
+
 // Kernel attributes are per device: set one once per device under a lock, and remember the
 // device only after cudaFuncSetAttribute succeeded (a failure is retried on the next launch).
 template <typename F>
