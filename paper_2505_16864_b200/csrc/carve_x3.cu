@@ -343,7 +343,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       decode_item(item, s, h, qb);
       const bool vis = qb < s.M_v;
       const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
-      WarpKvList bw(vis ? bits + ((int64_t)h * s.M_v + qb) * s.W : nullptr, s.W, lane);
+      const RowShape rs = vis ? RowShape(bits + ((int64_t)h * s.M_v + qb) * s.W, s.W, lane, BK, s.M_v,
+                                         s.M_total, s.n_valid, s.n_cond)
+                              : RowShape();
       const int T = 2 * n;
       const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
       const bool live = row < qvalid;
@@ -384,15 +386,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int ev = split_exp(__uint_as_float(__ldg(amax_bits + s.H + h)));
       const float c_row = scale_log2 * pow2(-(eq + ek));  // S_acc -> log2-domain scaled score
       float m_run = -INFINITY, l_run = 0.f;
-      int b = 0, kvalid = BK;
+      int kvalid = BK;
       float bias = 0.f;
-      for (int t = 0; t < T; ++t, ++g) {
-        if ((t & 1) == 0) {
-          b = vis ? bw.block(t >> 1) : (t >> 1);
-          kvalid = block_valid(b, BK, s.M_v, s.n_valid, s.n_cond);
-          bias = (vis && b >= s.M_v) ? beta_log2 : 0.f;
+      for (int j = 0; j < n; ++j) {  // kv blocks; their two half-steps unrolled (see carve.cu)
+        if (vis) {
+          kvalid = j == rs.n_vis - 1 ? rs.kv_last_vis : (j == n - 1 ? rs.kv_last : BK);
+          bias = j >= rs.n_vis ? beta_log2 : 0.f;
+        } else {
+          kvalid = block_valid(j, BK, s.M_v, s.n_valid, s.n_cond);
         }
-        const int hvalid = kvalid - (t & 1) * HN;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf, ++g) {
+        const int t = 2 * j + hf;
+        const int hvalid = kvalid - hf * HN;
         ptx::mbar_wait(&bars->s_full[g & 1], (g >> 1) & 1);
         ptx::tc_fence_after();
         const uint32_t sb = t_row + C::S_COL + (g & 1) * HN;
@@ -463,6 +469,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&bars->p_full[g & 1]);
+      }
       }
       // ---- epilogue: O * 2^-ev / l -> fp32 row, padding rows zero (attention.py:203-206)
       ptx::mbar_wait(&bars->o_full, it & 1);
