@@ -7,7 +7,7 @@ byte-identical to the reference's (round trips are bit-exact both ways).
 
 Device side: ``write_mask`` of a :class:`BlockMask` packs the rows on the GPU straight
 from its uint32 words (``tcb_mask_words_to_packbits``), and ``read_block_mask`` unpacks
-a file on the GPU into the packed words + CSR the attention kernel walks, so a mask file
+a file on the GPU into the packed words + row counts the attention kernels read, so a mask file
 never exists as a dense bool array on the host.  Tensors may be numpy arrays or torch
 tensors (CUDA tensors are copied to the host once).
 """
