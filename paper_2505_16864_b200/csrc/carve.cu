@@ -322,6 +322,8 @@ constexpr int O_COL = 128;
 constexpr int K_SLOTS = 3;        // K half-tiles in flight
 constexpr int V_SLOTS = 2;        // V half-tiles in flight
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units: P <= 2^8 between rescales
+// max-free steps: a half-step whose p-sum stays <= 2^12 keeps the running max (P <= 2^12)
+constexpr float RESCALE_SUM_LIMIT = 4096.0f;
 
 template <int D>
 struct Smem {
@@ -366,7 +368,7 @@ __device__ unsigned long long g_trace[TRACE_EV][TRACE_STEPS];
   } while (0)
 #endif
 
-template <int D, int EMU, typename E = __nv_bfloat16>
+template <int D, int EMU, typename E = __nv_bfloat16, int MAXFREE = 0>
 __global__ void __launch_bounds__(NUM_THREADS, 2)
     k_carve_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                const __grid_constant__ CUtensorMap tm_v, E* __restrict__ o,
@@ -616,48 +618,72 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
           for (int e = 0; e < 64; ++e)
             if (e >= hvalid) sr[e] = __float_as_uint(-INFINITY);
         }
-        float mx8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
-#pragma unroll
-        for (int e = 8; e < 64; e += 16)
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            mx8[q] = fmax3(mx8[q], __uint_as_float(sr[e + q]), __uint_as_float(sr[e + 8 + q]));
-        const float mraw = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]),
-                                 fmaxf(mx8[6], mx8[7]));
-        // block max in the scaled log2 domain (scale > 0 keeps the argmax)
-        const float m_blk = (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
-        const float m_new = fmaxf(m_run, m_blk);
-        const bool first = (t == 0);
-        const bool need = !first && (m_new > m_run + RESCALE_THRESHOLD);
-        const float m_use = (first || need) ? m_new : m_run;
-        const float alpha = need ? ptx::ex2(m_run - m_new) : 1.f;
-        // p = 2^(s * scale_log2 + bias - m_use): one FFMA2 per two keys
-        const float c0 = bias - m_use;
-        const uint64_t sc2 = f2_pack(scale_log2, scale_log2), c02 = f2_pack(c0, c0);
-        uint64_t acc2[4];
+        // p = 2^(s * scale_log2 + bias - m): one FFMA2 per two keys; returns the half's sum
         uint32_t pk[32];
+        auto exps = [&](float c0) -> float {
+          const uint64_t sc2 = f2_pack(scale_log2, scale_log2), c02 = f2_pack(c0, c0);
+          uint64_t acc2[4];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const uint64_t x = ffma2(f2_pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])),
-                                   sc2, c02);
-          float p0, p1;
-          if ((e & 7) >= 8 - EMU) {  // FMA-pipe exp2 for EMU of every 8 pairs
-            const uint64_t pp = exp2_poly2(x);
-            p0 = f2_lo(pp);
-            p1 = f2_hi(pp);
-          } else {
-            p0 = ptx::ex2(f2_lo(x));
-            p1 = ptx::ex2(f2_hi(x));
+          for (int e = 0; e < 32; ++e) {
+            const uint64_t x = ffma2(
+                f2_pack(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sc2, c02);
+            float p0, p1;
+            if ((e & 7) >= 8 - EMU) {  // FMA-pipe exp2 for EMU of every 8 pairs
+              const uint64_t pp = exp2_poly2(x);
+              p0 = f2_lo(pp);
+              p1 = f2_hi(pp);
+            } else {
+              p0 = ptx::ex2(f2_lo(x));
+              p1 = ptx::ex2(f2_hi(x));
+            }
+            acc2[e & 3] = e < 4 ? f2_pack(p0, p1) : fadd2(acc2[e & 3], f2_pack(p0, p1));
+            pk[e] = Elem<E>::pack(p0, p1);
           }
-          acc2[e & 3] = e < 4 ? f2_pack(p0, p1) : fadd2(acc2[e & 3], f2_pack(p0, p1));
-          pk[e] = Elem<E>::pack(p0, p1);
+          const uint64_t sum2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
+          return f2_lo(sum2) + f2_hi(sum2);
+        };
+        // block max in the scaled log2 domain (scale > 0 keeps the argmax)
+        auto block_max = [&]() -> float {
+          float mx8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(sr[e]);
+#pragma unroll
+          for (int e = 8; e < 64; e += 16)
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              mx8[q] = fmax3(mx8[q], __uint_as_float(sr[e + q]), __uint_as_float(sr[e + 8 + q]));
+          const float mraw = fmax3(fmax3(mx8[0], mx8[1], mx8[2]), fmax3(mx8[3], mx8[4], mx8[5]),
+                                   fmaxf(mx8[6], mx8[7]));
+          return (mraw == -INFINITY) ? -INFINITY : fmaf(mraw, scale_log2, bias);
+        };
+        const bool first = (t == 0);
+        bool need = false;
+        float alpha = 1.f, sum;
+        if (MAXFREE && !first) {
+          // Max-free step: exponentiate against the running max first.  Every p <= sum, so a
+          // half whose sum stays <= 2^RESCALE_SUM_LOG2 has no p above that bound and needs no
+          // max at all; otherwise (a new row maximum, or NaN/inf) redo it the classic way.
+          sum = exps(bias - m_run);
+          const bool over = !(sum <= RESCALE_SUM_LIMIT);
+          if (__any_sync(0xffffffffu, over)) {
+            if (over) {
+              const float m_new = fmaxf(m_run, block_max());
+              need = m_new > m_run;
+              if (need) alpha = ptx::ex2(m_run - m_new);
+              m_run = m_new;
+              sum = exps(bias - m_new);
+            }
+          }
+        } else {
+          const float m_new = fmaxf(m_run, block_max());
+          need = !first && (m_new > m_run + RESCALE_THRESHOLD);
+          const float m_use = (first || need) ? m_new : m_run;
+          if (need) alpha = ptx::ex2(m_run - m_new);
+          sum = exps(bias - m_use);
+          m_run = m_use;
         }
         ptx::tmem_st32(t_row + (g & 1) * HN, pk);
-        const uint64_t sum2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
-        l_run = l_run * alpha + (f2_lo(sum2) + f2_hi(sum2));
-        m_run = m_use;
+        l_run = l_run * alpha + sum;
         if (__any_sync(0xffffffffu, need)) {
           // O is final only once PV(t-1) retired: o_done completes once per PV
           ptx::mbar_wait(&bars->o_done, (g - 1) & 1);
@@ -818,7 +844,7 @@ static int dbg_flags() {
   return v;
 }
 
-template <int D, int EMU, typename E = __nv_bfloat16>
+template <int D, int EMU, typename E = __nv_bfloat16, int MAXFREE = 0>
 static int launch_tc(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
                      const uint32_t* bits, const int32_t* kv_cnt, float beta, int32_t* work,
                      cudaStream_t st) {
@@ -832,7 +858,7 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
   static std::atomic<uint64_t> attr{0};
   {
     const cudaError_t e = once_per_device(attr, [&] {
-      return cudaFuncSetAttribute(tc::k_carve_tc<D, EMU, E>,
+      return cudaFuncSetAttribute(tc::k_carve_tc<D, EMU, E, MAXFREE>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     });
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
@@ -847,7 +873,7 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
   if (grid > total) grid = total;
   const float LOG2E = 1.4426950408889634f;
   const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
-  tc::k_carve_tc<D, EMU, E><<<grid, tc::NUM_THREADS, smem, st>>>(tq, tk, tv, (E*)o, s, bits,
+  tc::k_carve_tc<D, EMU, E, MAXFREE><<<grid, tc::NUM_THREADS, smem, st>>>(tq, tk, tv, (E*)o, s, bits,
                                                          kv_cnt, work, total, scale_log2,
                                                          beta * LOG2E, dbg_flags());
   return check_launch("k_carve_tc");
@@ -881,26 +907,29 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
   const bool tc_ok = (dtype == TCB_BF16 || dtype == TCB_F16) && m == 128 && (d == 128 || d == 64) &&
                      aligned && work && M_v > 0;
   if (!tc_ok) return launch_simt(q, k, v, o, dtype, s, bits, kv_cnt, beta, as_stream(stream));
-  // pairs (of 8) whose exp2 runs on the FMA pipe instead of MUFU; TCB_CARVE_EMU overrides
-  static int emu = -1;
+  // pairs (of 8) whose exp2 runs on the FMA pipe instead of MUFU; TCB_CARVE_EMU overrides.
+  // TCB_CARVE_MAXFREE=0 selects the classic per-half-step block max (A/B experiments).
+  static int emu = -1, maxfree = -1;
   if (emu < 0) {
     const char* env = getenv("TCB_CARVE_EMU");
     emu = env ? atoi(env) : 0;
-    if (emu != 0 && emu != 2 && emu != 3 && emu != 4) emu = 0;
+    if (emu < 0 || emu > 2) emu = 0;
+    env = getenv("TCB_CARVE_MAXFREE");
+    maxfree = env ? atoi(env) != 0 : 1;
   }
   cudaStream_t st = as_stream(stream);
   if (dtype == TCB_F16)  // fp16 operands and P (kind::f16 with f16 inputs), f32 accumulation
-    return d == 128 ? launch_tc<128, 0, __half>(q, k, v, o, s, bits, kv_cnt, beta, work, st)
-                    : launch_tc<64, 0, __half>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
+    return d == 128 ? launch_tc<128, 0, __half, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, st)
+                    : launch_tc<64, 0, __half, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
   if (d == 128) {
+    if (!maxfree) return launch_tc<128, 0, __nv_bfloat16, 0>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
     switch (emu) {
-      case 3: return launch_tc<128, 3>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
-      case 4: return launch_tc<128, 4>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
-      case 2: return launch_tc<128, 2>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
-      default: return launch_tc<128, 0>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
+      case 1: return launch_tc<128, 1, __nv_bfloat16, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
+      case 2: return launch_tc<128, 2, __nv_bfloat16, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
+      default: return launch_tc<128, 0, __nv_bfloat16, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
     }
   }
-  return launch_tc<64, 0>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
+  return launch_tc<64, 0, __nv_bfloat16, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
 }
 
 #ifdef TCB_CARVE_TRACE

@@ -95,9 +95,11 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 // 2^x for a packed pair on the FMA pipe (offloads MUFU): x = j + f, j = rint(x) via the
 // 1.5*2^23 magic add, 2^f by a degree-3 minimax polynomial on [-0.5, 0.5] (max rel err
 // 7.5e-5, far below the bf16 rounding of P), 2^j added straight into the exponent bits.
-// x is clamped at -126 so the exponent never underflows into the sign bit.
+// x is clamped to [-126, 126] so the exponent never wraps into the sign bit (the max-free
+// carve step feeds x > 0 before it knows the block max; 2^126 still trips its redo check).
 __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
-  const float x0 = fmaxf(f2_lo(x), -126.f), x1 = fmaxf(f2_hi(x), -126.f);
+  const float x0 = fmaxf(fminf(f2_lo(x), 126.f), -126.f);
+  const float x1 = fmaxf(fminf(f2_hi(x), 126.f), -126.f);
   const uint64_t xc = f2_pack(x0, x1);
   const uint64_t magic = f2_pack(12582912.f, 12582912.f);
   const uint64_t t = fadd2(xc, magic);

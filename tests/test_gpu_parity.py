@@ -429,10 +429,12 @@ def test_token_major_head_shard_layout_bitwise():
     assert torch.equal(o_tm, o_ref)
 
 
-@pytest.mark.parametrize("pattern", ["rising", "falling", "spiky"])
+@pytest.mark.parametrize("pattern", ["rising", "falling", "spiky", "late_block"])
 def test_carve_bf16_online_softmax_extremes(pattern):
     # forces the lazy-rescale path every block (rising scores), total underflow of late
-    # blocks (falling), and isolated huge logits (spiky) -- no NaN/Inf, oracle tolerance
+    # blocks (falling), isolated huge logits (spiky), and one late block far above every
+    # earlier one (the max-free half-step's sum overflows and it redoes the step with the
+    # block max, rescaling O mid-row) -- no NaN/Inf, oracle tolerance
     dims = tcb.GridDims(4, 16, 24)
     lay = tcb.build_layout(dims, 128, 30)
     rng = np.random.default_rng(17)
@@ -446,8 +448,10 @@ def test_carve_bf16_online_softmax_extremes(pattern):
         k *= (0.2 + 0.9 * blk)[None, :, None]
     elif pattern == "falling":
         k *= (8.0 / (1.0 + blk))[None, :, None]
-    else:
+    elif pattern == "spiky":
         k[:, rng.integers(0, N, 16)] *= 40.0
+    else:
+        k[:, (lay.M_v - 2) * 128:(lay.M_v - 1) * 128] *= 12.0
     bits = np.ones((H, lay.M_v, lay.M_total), bool)
     qb, kb, vb = (_bf16(a) for a in (q, k, v))
     out = tcb.carve_attention(tcb.AttentionInputs(q=qb, k=kb, v=vb, layout=lay),
