@@ -114,7 +114,7 @@ def run_gpu(args):
 
     import paper_2505_16864_b200 as tcb
     from paper_2505_16864_b200 import _native
-    from paper_2505_16864_b200.attention import _workspace
+    from paper_2505_16864_b200.attention import _workspace, carve_work_bytes
     from paper_2505_16864_b200.masks import mask_scratch, launch_mask, mask_buffers
     from paper_2505_16864_b200.partition import mask_words
 
@@ -158,7 +158,7 @@ def run_gpu(args):
     pk = torch.empty_like(pq)
     bits, kv_cnt = mask_buffers(Hl, layout, dev)
     scratch = mask_scratch(Hl, layout, dev)
-    work = _workspace(dev)
+    work = _workspace(dev, carve_work_bytes(Hl, Mv, Mt, M, D))
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def layer(qh, kh, vh, out, marks=None, h0=0):
@@ -178,7 +178,7 @@ def run_gpu(args):
         if marks: marks[2].record()
         _native.call("tcb_carve_fwd", qh.data_ptr(), kh.data_ptr(), vh.data_ptr(), out.data_ptr(), 1,
                      sh, sn, bb.data_ptr(), words, bc.data_ptr(), Hc, D, M, Mv, Mt, layout.n_valid,
-                     layout.n_cond, 0.0, work.data_ptr(), sptr)
+                     layout.n_cond, 0.0, work.data_ptr(), work.numel(), sptr)
         if marks: marks[3].record()
         return out
 

@@ -29,7 +29,7 @@ sys.path.insert(0, ROOT)
 
 import paper_2505_16864_b200 as tcb  # noqa: E402
 from paper_2505_16864_b200 import _native  # noqa: E402
-from paper_2505_16864_b200.attention import _workspace  # noqa: E402
+from paper_2505_16864_b200.attention import _workspace, carve_work_bytes  # noqa: E402
 from paper_2505_16864_b200.masks import mask_scratch, launch_mask, mask_buffers  # noqa: E402
 from paper_2505_16864_b200.partition import mask_words  # noqa: E402
 
@@ -77,7 +77,7 @@ class Layer:
         self.words = mask_words(L.M_total)
         self.bits, self.kv_cnt = mask_buffers(H, L, self.q.device)
         self.scratch = mask_scratch(H, L, self.q.device)
-        self.work = _workspace(self.q.device)
+        self.work = _workspace(self.q.device, carve_work_bytes(H, L.M_v, L.M_total, 128, 128))
         self.s = torch.cuda.current_stream().cuda_stream
 
     def mask(self):
@@ -93,7 +93,8 @@ class Layer:
         _native.call("tcb_carve_fwd", self.q.data_ptr(), self.kk.data_ptr(), self.v.data_ptr(),
                      self.o.data_ptr(), 1, self.q.stride(0), self.q.stride(1),
                      self.bits.data_ptr(), self.words, self.kv_cnt.data_ptr(), self.H, 128, 128, L.M_v,
-                     L.M_total, L.n_valid, L.n_cond, float(self.beta), self.work.data_ptr(), self.s)
+                     L.M_total, L.n_valid, L.n_cond, float(self.beta), self.work.data_ptr(),
+                     self.work.numel(), self.s)
 
     def pairs(self):
         return int(self.kv_cnt.sum().item()) + self.H * self.lay.M_c * self.lay.M_total

@@ -133,11 +133,16 @@ int tcb_mask_unpack(const uint32_t* bits, int64_t rows, int M_total, int words, 
  * added on condition keys of vision rows, padding rows of o are zeroed.
  * dtype TCB_BF16 or TCB_F16 with m == 128 and d in {64,128} runs the tcgen05/TMEM/TMA
  * kernel; everything else runs the fp32 SIMT kernel (parity path).
- * work: caller-provided scratch of >= 16 bytes (scheduler counter). */
+ * work: caller-provided device scratch, 256-byte aligned, work_bytes long: >= 16 bytes
+ * (scheduler counter); with tcb_carve_workspace_bytes() bytes the tcgen05 kernel also splits
+ * each condition q-block into kv-range chunks that run beside their head's vision rows and
+ * merges their partials (less DRAM traffic; results within the same tolerance). */
+int64_t tcb_carve_workspace_bytes(int H, int M_v, int M_total, int m, int d);
 int tcb_carve_fwd(const void* q, const void* k, const void* v, void* o, int dtype,
                   int64_t stride_h, int64_t stride_n, const uint32_t* bits, int words,
                   const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
-                  int64_t n_valid, int64_t n_cond, float beta, int32_t* work, void* stream);
+                  int64_t n_valid, int64_t n_cond, float beta, int32_t* work, int64_t work_bytes,
+                  void* stream);
 
 /* Like tcb_carve_fwd but forces the fp32-math SIMT kernel for any shape. */
 int tcb_carve_fwd_simt(const void* q, const void* k, const void* v, void* o, int dtype,

@@ -40,8 +40,9 @@ SIGNATURES = {
     "tcb_block_mask_scratch": [_I, _I, _I],
     "tcb_mask_pack": [_P, _I64, _I, _I, _P, _P, _P],
     "tcb_mask_unpack": [_P, _I64, _I, _I, _P, _P],
+    "tcb_carve_workspace_bytes": [_I, _I, _I, _I, _I],
     "tcb_carve_fwd": [_P, _P, _P, _P, _I, _I64, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _I64,
-                      _I64, _F, _P, _P],
+                      _I64, _F, _P, _I64, _P],
     "tcb_carve_fwd_simt": [_P, _P, _P, _P, _I, _I64, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _I64,
                            _I64, _F, _P],
     "tcb_carve_f32_workspace_bytes": [_I, _I, _I, _I],
@@ -63,7 +64,7 @@ SIGNATURES = {
 }
 
 
-_I64_RESULT = ("tcb_block_mask_scratch", "tcb_carve_f32_workspace_bytes")
+_I64_RESULT = ("tcb_block_mask_scratch", "tcb_carve_f32_workspace_bytes", "tcb_carve_workspace_bytes")
 
 
 class NativeUnavailable(RuntimeError):

@@ -79,13 +79,21 @@ def compute_beta(numel_s: int, numel_S: int, rho: float) -> float:
 _work: dict = {}
 
 
-def _workspace(dev: torch.device) -> torch.Tensor:
-    """The carve kernel's work counter (reset by the launch itself), one per (device,
-    stream): launches on different streams may run concurrently and must not share it."""
+def carve_work_bytes(H: int, M_v: int, M_total: int, m: int, d: int) -> int:
+    """Workspace bytes tcb_carve_fwd wants for a shape (scheduler counter, plus the split
+    condition rows' partials when the tcgen05 kernel runs)."""
+    return int(_native.query("tcb_carve_workspace_bytes", H, M_v, M_total, m, d))
+
+
+def _workspace(dev: torch.device, nbytes: int = 256) -> torch.Tensor:
+    """The carve kernels' workspace (work counter + condition-row partials; the launch resets
+    what it needs), one per (device, stream): launches on different streams may run
+    concurrently and must not share it.  Grows to ``nbytes``; pass ``(t.data_ptr(),
+    t.numel())`` as (work, work_bytes)."""
     key = (dev, torch.cuda.current_stream(dev).cuda_stream)
     w = _work.get(key)
-    if w is None:
-        w = torch.zeros(16, dtype=torch.int32, device=dev)
+    if w is None or w.numel() < nbytes:
+        w = torch.zeros(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
         _work[key] = w
     return w
 
@@ -129,7 +137,8 @@ def launch_carve(q, k, v, out, words, kv_cnt, m, M_v, M_total, n_valid, n_cond, 
         _native.call("tcb_carve_fwd_f32", *args[:4], *args[5:], ws.data_ptr(), nb,
                      _workspace(q.device).data_ptr(), _dev.stream())
     else:
-        _native.call("tcb_carve_fwd", *args, _workspace(q.device).data_ptr(), _dev.stream())
+        w = _workspace(q.device, carve_work_bytes(H, M_v, M_total, m, d))
+        _native.call("tcb_carve_fwd", *args, w.data_ptr(), w.numel(), _dev.stream())
 
 
 def carve_attention(inputs: AttentionInputs, mask: BlockMask,

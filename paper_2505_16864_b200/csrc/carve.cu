@@ -347,9 +347,45 @@ struct Bars {
   uint64_t v_full[V_SLOTS], v_empty[V_SLOTS];
   uint64_t sched_full[2], sched_empty[2];
   int sched_item[2];
+  int last;  // condition-row split: the chunk count this CTA's chunk observed
   uint32_t tmem_base;
 };
 static_assert(sizeof(Bars) <= 256, "barrier block must fit the reserved smem");
+
+// Condition q-blocks attend all M_total kv blocks (~10x a vision row).  With a workspace,
+// each is split into C chunks of `len` kv blocks that run as ordinary work items next to
+// their head's vision rows (per-head item order: the head's K/V is read from DRAM about
+// once instead of once by a condition-row sweep ahead of everything and again by the vision
+// rows); each chunk leaves its unnormalised O, running max and sum in `part`, and the
+// chunk that completes a row (per-row counter `cnt`) merges the C partials in chunk order.
+// C == 1: no split, all condition rows first (longest-first order).
+struct CondSplit {
+  int C, len;
+  float* part;  // [H*M_c*C][BM][D] O partials, then [H*M_c*C][BM][2] (m, l)
+  int* cnt;     // [H*M_c] chunks finished per condition row
+};
+
+__device__ __forceinline__ void decode_tc(int item, const CarveShape& s, const CondSplit& cs, int& h,
+                                          int& qb, int& c0, int& c1) {
+  c0 = 0;
+  c1 = s.M_total;
+  if (cs.C <= 1) {
+    decode_item(item, s, h, qb);
+    return;
+  }
+  const int n_cc = (s.M_total - s.M_v) * cs.C;
+  const int per = n_cc + s.M_v;
+  h = item / per;
+  const int r = item - h * per;
+  if (r < n_cc) {
+    const int ci = r / cs.C;
+    qb = s.M_v + ci;
+    c0 = (r - ci * cs.C) * cs.len;
+    c1 = min(s.M_total, c0 + cs.len);
+  } else {
+    qb = r - n_cc;
+  }
+}
 
 // Timeline stamps for tools/carve_trace1.py: compiled only into trace builds
 // (TCB_NVCC_EXTRA=-DTCB_CARVE_TRACE python -m paper_2505_16864_b200._build), enabled at run
@@ -374,7 +410,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
                const __grid_constant__ CUtensorMap tm_v, E* __restrict__ o,
                CarveShape s, const uint32_t* __restrict__ bits,
                const int32_t* __restrict__ kv_cnt, int* __restrict__ counter, int total_items,
-               float scale_log2, float beta_log2, int dbg) {
+               float scale_log2, float beta_log2, int dbg, CondSplit cs) {
   using L = Smem<D>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + L::OFF_Q;
@@ -437,10 +473,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       }
       item = __shfl_sync(0xffffffffu, item, 0);
       if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
+      int h, qb, c0, c1;
+      decode_tc(item, s, cs, h, qb, c0, c1);
       const bool vis = qb < s.M_v;
-      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : s.M_total;
+      const int n = vis ? __ldg(kv_cnt + (int64_t)h * s.M_v + qb) : c1 - c0;
+      const uint64_t pol_cond = cs.C > 1 ? pol_kv : pol_q;  // split rows share the head's K/V
       const uint32_t* brow = bits + ((int64_t)h * s.M_v + (vis ? qb : 0)) * s.W;
       // K runs one half-step ahead of V: one walk per stream (cond rows never walk)
       WarpKvList wk(vis ? brow : nullptr, s.W, lane), wv(vis ? brow : nullptr, s.W, lane);
@@ -452,7 +489,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       }
       auto load = [&](const CUtensorMap* tm, uint8_t* base, uint64_t* full, uint64_t* empty,
                       int slots, uint32_t& cnt, int t, WarpKvList& walk) {
-        const int b = vis ? walk.block(t >> 1) : (t >> 1);
+        const int b = vis ? walk.block(t >> 1) : c0 + (t >> 1);
         if (lane == 0) {
           const int sl = cnt % slots;
           ptx::mbar_wait(&empty[sl], ((cnt / slots) & 1) ^ 1);
@@ -461,7 +498,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
           } else {
             ptx::mbar_arrive_expect_tx(&full[sl], L::HALF_BYTES);
             ptx::tma_load_4d(base + sl * L::HALF_BYTES, tm, &full[sl], 0, b * BK + (t & 1) * HN, 0, h,
-                             vis ? pol_kv : pol_q);
+                             vis ? pol_kv : pol_cond);
           }
         }
         ++cnt;
@@ -511,10 +548,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);
       if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
+      int h, qb, c0, c1;
+      decode_tc(item, s, cs, h, qb, c0, c1);
       const bool vis = qb < s.M_v;
-      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
+      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : c1 - c0;
       const int T = 2 * n;
       ptx::mbar_wait(&bars->q_full, it & 1);
       if (T == 0) {  // cannot come from build_block_mask (diagonal); keep the pipes consistent
@@ -574,12 +611,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&bars->sched_empty[slot]);
       if (item < 0) break;
-      int h, qb;
-      decode_item(item, s, h, qb);
+      int h, qb, c0, c1;
+      decode_tc(item, s, cs, h, qb, c0, c1);
       const bool vis = qb < s.M_v;
-      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : s.M_total;
+      const int n = vis ? kv_cnt[(int64_t)h * s.M_v + qb] : c1 - c0;
       // the block index itself is not needed here: only where condition keys start and
-      // which entries can be partial blocks (RowShape); condition q-blocks visit 0..M_total-1
+      // which entries can be partial blocks (RowShape); condition q-blocks visit c0..c1-1
       const RowShape rs = vis ? RowShape(bits + ((int64_t)h * s.M_v + qb) * s.W, s.W, lane, BK, s.M_v,
                                          s.M_total, s.n_valid, s.n_cond)
                               : RowShape();
@@ -594,7 +631,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
           kvalid = j == rs.n_vis - 1 ? rs.kv_last_vis : (j == n - 1 ? rs.kv_last : BK);
           bias = j >= rs.n_vis ? beta_log2 : 0.f;
         } else {
-          kvalid = block_valid(j, BK, s.M_v, s.n_valid, s.n_cond);
+          kvalid = block_valid(c0 + j, BK, s.M_v, s.n_valid, s.n_cond);
         }
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf, ++g) {
@@ -708,6 +745,76 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
       ptx::mbar_wait(&bars->o_full, it & 1);
       ptx::tc_fence_after();
       const int qvalid = block_valid(qb, BM, s.M_v, s.n_valid, s.n_cond);
+      if (!vis && cs.C > 1) {
+        // one chunk of a split condition row: leave (O unnormalised, m, l); the chunk that
+        // completes the row merges all C in chunk order (run-to-run deterministic)
+        const int64_t rid = (int64_t)h * (s.M_total - s.M_v) + (qb - s.M_v);
+        const int64_t n_part = (int64_t)s.H * (s.M_total - s.M_v) * cs.C;
+        const int64_t slot = rid * cs.C + c0 / cs.len;
+        float4* po = reinterpret_cast<float4*>(cs.part + (slot * BM + row) * D);
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t ov[32];
+          ptx::tmem_ld32(t_row + O_COL + c * 32, ov);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            __stcg(po + c * 8 + e, make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
+                                               __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3])));
+        }
+        ptx::tc_fence_before();
+        __stcg(reinterpret_cast<float2*>(cs.part + n_part * BM * D) + slot * BM + row,
+               make_float2(m_run, l_run));
+        __threadfence();
+        ptx::named_bar_sync(1, 128);
+        if (warp == 2 && lane == 0) bars->last = atomicAdd(cs.cnt + rid, 1);
+        ptx::named_bar_sync(1, 128);
+        // (`last` is rewritten only after the next split item's first barrier, which every
+        // softmax thread reaches after reading it here)
+        if (bars->last == cs.C - 1) {
+          __threadfence();
+          const float2* ml = reinterpret_cast<const float2*>(cs.part + n_part * BM * D) + rid * cs.C * BM + row;
+          float mx = -INFINITY;
+          for (int c = 0; c < cs.C; ++c) mx = fmaxf(mx, __ldcg(ml + c * BM).x);
+          float lsum = 0.f;
+          for (int c = 0; c < cs.C; ++c) {
+            const float2 v = __ldcg(ml + c * BM);
+            lsum += ptx::ex2(v.x - mx) * v.y;
+          }
+          const float inv_l = row < qvalid ? 1.f / lsum : 0.f;
+          const float4* pr = reinterpret_cast<const float4*>(cs.part + (rid * cs.C * BM + row) * D);
+          E* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
+#pragma unroll 1
+          for (int cc = 0; cc < D / 32; ++cc) {
+            float acc[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+#pragma unroll 1
+            for (int c = 0; c < cs.C; ++c) {
+              const float w = ptx::ex2(__ldcg(ml + c * BM).x - mx);
+              const float4* src = pr + (int64_t)c * BM * (D / 4) + cc * 8;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const float4 v = __ldcg(src + e);
+                acc[4 * e] = fmaf(w, v.x, acc[4 * e]);
+                acc[4 * e + 1] = fmaf(w, v.y, acc[4 * e + 1]);
+                acc[4 * e + 2] = fmaf(w, v.z, acc[4 * e + 2]);
+                acc[4 * e + 3] = fmaf(w, v.w, acc[4 * e + 3]);
+              }
+            }
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              pk[e] = row < qvalid ? Elem<E>::pack(acc[2 * e] * inv_l, acc[2 * e + 1] * inv_l) : 0u;
+            int4* dst = reinterpret_cast<int4*>(orow + cc * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              __stcs(dst + e, make_int4((int)pk[4 * e], (int)pk[4 * e + 1], (int)pk[4 * e + 2],
+                                        (int)pk[4 * e + 3]));
+          }
+        }
+        continue;
+      }
       const float inv_l = (row < qvalid && T > 0) ? 1.f / l_run : 0.f;
       E* orow = o + (int64_t)h * s.sh + ((int64_t)qb * BM + row) * s.sn;
 #pragma unroll 1
@@ -844,10 +951,37 @@ static int dbg_flags() {
   return v;
 }
 
+// Workspace of tcb_carve_fwd: [0, 256) scheduler counter; then, when condition rows are
+// split, the per-row chunk counters (256-aligned) and the partials (O, then (m, l)).
+constexpr int SPLIT_LEN = 128;  // target kv blocks per condition-row chunk (~a vision row)
+static void cond_split_plan(int M_v, int M_total, int& C, int& len) {
+  C = (M_total - M_v) > 0 ? (M_total + SPLIT_LEN - 1) / SPLIT_LEN : 1;
+  if (C < 2) C = 1;
+  len = (M_total + C - 1) / C;
+}
+static int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
+static int64_t split_cnt_bytes(int H, int M_c) { return align256((int64_t)H * M_c * 4); }
+static int64_t carve_work_bytes(int H, int M_v, int M_total, int d) {
+  int C, len;
+  cond_split_plan(M_v, M_total, C, len);
+  if (C == 1) return 256;
+  const int64_t parts = (int64_t)H * (M_total - M_v) * C * tc::BM;
+  return 256 + split_cnt_bytes(H, M_total - M_v) + parts * (d + 2) * 4;
+}
+
+static bool split_disabled() {  // TCB_CARVE_NOSPLIT=1: A/B of the unsplit order
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TCB_CARVE_NOSPLIT");
+    v = (e && atoi(e) != 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <int D, int EMU, typename E = __nv_bfloat16, int MAXFREE = 0>
 static int launch_tc(const void* q, const void* k, const void* v, void* o, const CarveShape& s,
                      const uint32_t* bits, const int32_t* kv_cnt, float beta, int32_t* work,
-                     cudaStream_t st) {
+                     int64_t work_bytes, cudaStream_t st) {
   CUtensorMap tq, tk, tv;
   const int64_t n_pad = (int64_t)s.M_total * s.m;
   int rc;
@@ -863,19 +997,31 @@ static int launch_tc(const void* q, const void* k, const void* v, void* o, const
     });
     if (e != cudaSuccess) return set_error(TCB_ECUDA, "carve smem attr: %s", cudaGetErrorString(e));
   }
-  cudaError_t e = cudaMemsetAsync(work, 0, sizeof(int32_t), st);
+  // split condition rows when the caller's workspace holds the partials (else all condition
+  // rows run first, unsplit)
+  tc::CondSplit cs{1, s.M_total, nullptr, nullptr};
+  int64_t zero_bytes = sizeof(int32_t);
+  if (work_bytes >= carve_work_bytes(s.H, s.M_v, s.M_total, D) && carve_work_bytes(s.H, s.M_v, s.M_total, D) > 256 &&
+      !split_disabled()) {
+    cond_split_plan(s.M_v, s.M_total, cs.C, cs.len);
+    uint8_t* base = reinterpret_cast<uint8_t*>(work);
+    cs.cnt = reinterpret_cast<int*>(base + 256);
+    cs.part = reinterpret_cast<float*>(base + 256 + split_cnt_bytes(s.H, s.M_total - s.M_v));
+    zero_bytes = 256 + split_cnt_bytes(s.H, s.M_total - s.M_v);
+  }
+  cudaError_t e = cudaMemsetAsync(work, 0, zero_bytes, st);
   if (e != cudaSuccess) return set_error(TCB_ECUDA, "memset counter: %s", cudaGetErrorString(e));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int total = s.H * s.M_total;
+  const int total = s.H * (s.M_v + (s.M_total - s.M_v) * cs.C);
   int grid = 2 * sms;
   if (grid > total) grid = total;
   const float LOG2E = 1.4426950408889634f;
   const float scale_log2 = (float)(1.0 / sqrt((double)s.d)) * LOG2E;
   tc::k_carve_tc<D, EMU, E, MAXFREE><<<grid, tc::NUM_THREADS, smem, st>>>(tq, tk, tv, (E*)o, s, bits,
                                                          kv_cnt, work, total, scale_log2,
-                                                         beta * LOG2E, dbg_flags());
+                                                         beta * LOG2E, dbg_flags(), cs);
   return check_launch("k_carve_tc");
 }
 
@@ -893,12 +1039,19 @@ extern "C" int tcb_carve_fwd_simt(const void* q, const void* k, const void* v, v
   return launch_simt(q, k, v, o, dtype, s, bits, kv_cnt, beta, as_stream(stream));
 }
 
+extern "C" int64_t tcb_carve_workspace_bytes(int H, int M_v, int M_total, int m, int d) {
+  if (H < 1 || M_v < 0 || M_total < M_v || M_total < 1) return 256;
+  if (m != 128 || (d != 64 && d != 128)) return 256;  // SIMT kernels: only the counter
+  return carve_work_bytes(H, M_v, M_total, d);
+}
+
 extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* o, int dtype,
                              int64_t stride_h, int64_t stride_n, const uint32_t* bits, int words,
                              const int32_t* kv_cnt, int H, int d, int m, int M_v, int M_total,
                              int64_t n_valid, int64_t n_cond, float beta, int32_t* work,
-                             void* stream) {
+                             int64_t work_bytes, void* stream) {
   CarveShape s{H, d, m, M_v, M_total, words, n_valid, n_cond, stride_h, stride_n};
+  if ((uintptr_t)work % 256 != 0) work_bytes = 0;  // partials need 256-byte alignment
   int rc = validate(q, k, v, o, dtype, bits, kv_cnt, s);
   if (rc) return rc;
   const bool aligned = ((uintptr_t)q % 16 == 0) && ((uintptr_t)k % 16 == 0) &&
@@ -919,17 +1072,17 @@ extern "C" int tcb_carve_fwd(const void* q, const void* k, const void* v, void* 
   }
   cudaStream_t st = as_stream(stream);
   if (dtype == TCB_F16)  // fp16 operands and P (kind::f16 with f16 inputs), f32 accumulation
-    return d == 128 ? launch_tc<128, 0, __half, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, st)
-                    : launch_tc<64, 0, __half, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
+    return d == 128 ? launch_tc<128, 0, __half, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, work_bytes, st)
+                    : launch_tc<64, 0, __half, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, work_bytes, st);
   if (d == 128) {
-    if (!maxfree) return launch_tc<128, 0, __nv_bfloat16, 0>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
+    if (!maxfree) return launch_tc<128, 0, __nv_bfloat16, 0>(q, k, v, o, s, bits, kv_cnt, beta, work, work_bytes, st);
     switch (emu) {
-      case 1: return launch_tc<128, 1, __nv_bfloat16, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
-      case 2: return launch_tc<128, 2, __nv_bfloat16, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
-      default: return launch_tc<128, 0, __nv_bfloat16, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
+      case 1: return launch_tc<128, 1, __nv_bfloat16, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, work_bytes, st);
+      case 2: return launch_tc<128, 2, __nv_bfloat16, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, work_bytes, st);
+      default: return launch_tc<128, 0, __nv_bfloat16, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, work_bytes, st);
     }
   }
-  return launch_tc<64, 0, __nv_bfloat16, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, st);
+  return launch_tc<64, 0, __nv_bfloat16, 1>(q, k, v, o, s, bits, kv_cnt, beta, work, work_bytes, st);
 }
 
 #ifdef TCB_CARVE_TRACE

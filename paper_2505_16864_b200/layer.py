@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _dev, _native
-from .attention import AmplifierBias, _workspace
+from .attention import AmplifierBias, _workspace, carve_work_bytes
 from .errors import ShapeError
 from .masks import BlockMask, SelectionParams, mask_scratch, launch_mask, mask_buffers
 from .partition import BlockLayout, StaticMasks
@@ -52,7 +52,7 @@ def _launch_chunk(q, k, v, o, pq, pk, bits, kv_cnt, scratch, adja, layout, param
     _native.call("tcb_carve_fwd", q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                  _dev.code_of(q.dtype), sh, sn, bits.data_ptr(), bits.shape[-1], kv_cnt.data_ptr(),
                  Hc, d, layout.m, Mv, Mt, layout.n_valid, layout.n_cond, float(beta), work.data_ptr(),
-                 sptr)
+                 work.numel(), sptr)
 
 
 def carve_layer(q, k, v, layout: BlockLayout, statics: StaticMasks, params: SelectionParams,
@@ -101,11 +101,11 @@ def carve_layer(q, k, v, layout: BlockLayout, statics: StaticMasks, params: Sele
     bits, kv_cnt = mask_buffers(H, layout, dev)
     scratch = mask_scratch(H, layout, dev)
     adja = statics.packed(layout)
-    work = _workspace(dev)
+    hc = heads_per_chunk or max(1, H // 12)  # C2: 2-head chunks (44.6 vs 45.2 ms at 3)
+    work = _workspace(dev, carve_work_bytes(min(hc, H), layout.M_v, Mt, layout.m, d))
 
     comp = torch.cuda.current_stream(dev)
     s_in, s_out = _copy_streams(dev)
-    hc = heads_per_chunk or max(1, H // 12)  # C2: 2-head chunks (44.6 vs 45.2 ms at 3)
     chunks = [(h0, min(H, h0 + hc)) for h0 in range(0, H, hc)]
     s_in.wait_stream(comp)  # device buffers may be recycled from work still queued on comp
     s_out.wait_stream(comp)
@@ -162,7 +162,9 @@ class CarveLayerGraph:
         self._bits, self._kv_cnt = mask_buffers(H, layout, dev)
         self._scratch = mask_scratch(H, layout, dev)
         self._adja = statics.packed(layout)
-        self._work = torch.zeros(16, dtype=torch.int32, device=dev)  # private: replays may overlap
+        # private (replays may overlap): counter + split condition-row partials
+        self._work = torch.zeros(carve_work_bytes(H, layout.M_v, Mt, layout.m, d), dtype=torch.uint8,
+                                 device=dev)
         self.mask = BlockMask(words=self._bits, kv_cnt=self._kv_cnt, M_total=Mt, nonempty=True)
         args = (self.q, self.k, self.v, self.out, self._pq, self._pk, self._bits, self._kv_cnt,
                 self._scratch, self._adja, layout, params, beta.beta, self._work)

@@ -51,19 +51,19 @@ def test_error_mapping_without_gpu():
         _native.call("tcb_block_pool", 1, None, 7, 0, 0, 1, 1, 1, 1, 1, 1, 0, 1, None, None)
     # carve: unknown dtype, shape errors, too many work items
     # (q, k, v, o, dtype, sh, sn, bits, words, kv_cnt, H, d, m, M_v, M_total, n_valid, n_cond,
-    #  beta, work, stream)
+    #  beta, work, work_bytes, stream)
     with pytest.raises(DomainError):
         _native.call("tcb_carve_fwd", 1, 1, 1, 1, 9, 128, 128, 1, 1, 1, 1, 128, 128, 1, 1, 1, 0,
-                     0.0, 1, None)
+                     0.0, 1, 256, None)
     with pytest.raises(ShapeError):
         _native.call("tcb_carve_fwd", None, 1, 1, 1, 1, 128, 128, 1, 1, 1, 1, 128, 128, 1, 1, 1, 0,
-                     0.0, 1, None)
+                     0.0, 1, 256, None)
     with pytest.raises(ShapeError):  # mask rows narrower than M_total columns
         _native.call("tcb_carve_fwd", 1, 1, 1, 1, 1, 128, 128, 1, 1, 1, 1, 128, 128, 40, 40, 1, 0,
-                     0.0, 1, None)
+                     0.0, 1, 256, None)
     with pytest.raises(SizeError):
         _native.call("tcb_carve_fwd", 1, 1, 1, 1, 1, 128, 128, 1, 128, 1, 1 << 20, 128, 128, 4096,
-                     4096, 1, 0, 0.0, 1, None)
+                     4096, 1, 0, 0.0, 1, 256, None)
     # selection: M_total beyond the supported range, n_floor < 1
     with pytest.raises(SizeError):
         _native.call("tcb_block_select", 1, 1, 9000, 9000, None, 300, 1, 0.0, 1, 1, 1, None)
