@@ -961,12 +961,17 @@ static void cond_split_plan(int M_v, int M_total, int& C, int& len) {
 }
 static int64_t align256(int64_t x) { return (x + 255) & ~(int64_t)255; }
 static int64_t split_cnt_bytes(int H, int M_c) { return align256((int64_t)H * M_c * 4); }
+constexpr int64_t SPLIT_MAX_BYTES = 256ll << 20;  // beyond this, condition rows run unsplit
 static int64_t carve_work_bytes(int H, int M_v, int M_total, int d) {
   int C, len;
   cond_split_plan(M_v, M_total, C, len);
   if (C == 1) return 256;
   const int64_t parts = (int64_t)H * (M_total - M_v) * C * tc::BM;
-  return 256 + split_cnt_bytes(H, M_total - M_v) + parts * (d + 2) * 4;
+  const int64_t items = (int64_t)H * (M_v + (int64_t)(M_total - M_v) * C);
+  const int64_t bytes = 256 + split_cnt_bytes(H, M_total - M_v) + parts * (d + 2) * 4;
+  // many condition blocks already give plenty of parallel items: a bounded workspace
+  if (bytes > SPLIT_MAX_BYTES || items >= ((int64_t)1 << 31)) return 256;
+  return bytes;
 }
 
 static bool split_disabled() {  // TCB_CARVE_NOSPLIT=1: A/B of the unsplit order

@@ -75,3 +75,5 @@ def test_workspace_query():
     assert carve_work_bytes(4, 32, 33, 64, 64) == 256
     nb = carve_work_bytes(24, 929, 931, 128, 128)
     assert nb == 256 + 256 + 24 * 2 * 8 * 128 * (128 + 2) * 4
+    # a bounded workspace: 600 text blocks x 64 chunks x 24 heads would need ~30 GB -> unsplit
+    assert carve_work_bytes(24, 7000, 7600, 128, 128) == 256
