@@ -134,3 +134,15 @@ def test_device_curve_math_named_shapes(curve_host):
     for i, fw in enumerate(got):
         sha = hashlib.sha256(fw.astype("<i8").tobytes()).hexdigest()[:16]
         assert sha == str(g["big_sha"][i]), big[i]
+
+
+def test_carve_workspace_query_host_only():
+    # pure host arithmetic (no GPU): the condition-row split's workspace
+    from paper_2505_16864_b200 import _native
+
+    q = lambda *a: _native.query("tcb_carve_workspace_bytes", *a)  # noqa: E731
+    assert q(40, 256, 256, 128, 128) == 256               # no text: counter only
+    assert q(4, 32, 33, 64, 64) == 256                    # SIMT shapes: counter only
+    assert q(24, 929, 931, 128, 128) == 256 + 256 + 24 * 2 * 8 * 128 * 130 * 4   # C2: 8 chunks
+    assert q(3, 929, 931, 128, 128) == 256 + 256 + 3 * 2 * 8 * 128 * 130 * 4
+    assert q(24, 7000, 7600, 128, 128) == 256             # > 256 MB of partials: unsplit
