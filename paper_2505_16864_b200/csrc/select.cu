@@ -1134,6 +1134,178 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
       with_union, adja, bits, kv_cnt, prog.nl, prog.nops, leaf_off, leaf_len, fold_ops);
 }
 
+// ---- p == 0 on raw scores, rows of <= 32 * NPL columns: registers only ----------------
+// The same decision as select_row<RAW, !SORT, MODE 1, FASTS> (top-n_floor set of the scores
+// under (value desc, column asc), exact iff the boundary is no near tie and clear of exp's
+// underflow range, else kv_cnt = -1 for the exact pass) without shared-memory radix passes:
+// lane l holds columns l, l + 32, ... as fp32 images (double -> float is monotone), a
+// bisection on those narrows the boundary to an interval (a, b] holding <= 32 columns (about
+// log2(M_total / 32) counting rounds of one FSETP per element and a warp reduction), the
+// candidates in it are ranked exactly by their float64 scores (ties: lower column first), and
+// mask word i is the ballot of register i.  Only the boundary candidates and the extreme
+// elements are ever compared in float64.  Rows with a non-finite or huge score, or whose
+// boundary cannot be narrowed to 32 candidates (mass ties), go to the exact pass.
+template <int NPL>
+__global__ void __launch_bounds__(128, 4) k_select_p0(const double* __restrict__ S, int64_t n_rows,
+                                                    int M_v, int M_total,
+                                                    const uint32_t* __restrict__ adja, int words,
+                                                    int n_floor, int with_union,
+                                                    uint32_t* __restrict__ bits,
+                                                    int32_t* __restrict__ kv_cnt) {
+  __shared__ double c_val[4][32];
+  __shared__ int c_col[4][32];
+  __shared__ uint32_t c_bits[4][NPL];  // chosen candidates: word i, bit l = column l + 32 i
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 4 + warp;
+  if (row >= n_rows) return;
+  const double* Sr = S + row * M_total;
+  float f[NPL];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    double x = j < M_total ? Sr[j] : 0.0;
+    bad |= !(fabs(x) < 1e30);  // NaN / inf / out of float range: exact pass
+    f[i] = j < M_total ? (float)x : -INFINITY;
+  }
+  auto redo = [&]() {
+    if (lane == 0) kv_cnt[row] = -1;
+  };
+  if (__any_sync(FULL, bad)) return redo();
+  float fmx = -INFINITY, fmn = INFINITY;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    fmx = fmaxf(fmx, f[i]);
+    if (lane + 32 * i < M_total) fmn = fminf(fmn, f[i]);
+  }
+  #pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    fmx = fmaxf(fmx, __shfl_xor_sync(FULL, fmx, o));
+    fmn = fminf(fmn, __shfl_xor_sync(FULL, fmn, o));
+  }
+  const int keep = min(max(n_floor, 1), M_total);
+  auto count_gt = [&](float x) {
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) c += f[i] > x ? 1 : 0;  // padding is -inf: never counted
+    return (int)__reduce_add_sync(FULL, (unsigned)c);
+  };
+  // invariant: count_gt(b) < keep <= count_gt(a): the keep-th element's image lies in (a, b]
+  float a = fmn, b = fmx;
+  int ca = count_gt(a), cb = 0;
+  if (ca >= keep) {
+    for (int itn = 0; itn < 40 && ca - cb > 32; ++itn) {
+      const float mid = a + 0.5f * (b - a);
+      if (!(mid > a && mid < b)) break;
+      const int c = count_gt(mid);
+      if (c >= keep) { a = mid; ca = c; } else { b = mid; cb = c; }
+    }
+  } else {  // the boundary image is the row minimum: the candidates are its ties
+    b = fmn;
+    cb = ca;
+    a = -INFINITY;
+    ca = M_total;
+  }
+  const int ncand = ca - cb;
+  if (ncand > 32) return redo();  // mass ties around the boundary: the exact pass sorts
+  // gather the candidates (a, b] in column order, with their float64 scores
+  for (int w = lane; w < NPL; w += 32) c_bits[warp][w] = 0u;
+  int base = 0;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    const bool c = f[i] > a && f[i] <= b && j < M_total;
+    const unsigned bal = __ballot_sync(FULL, c);
+    if (c) {
+      const int sl = base + __popc(bal & ((1u << lane) - 1u));
+      c_val[warp][sl] = Sr[j];
+      c_col[warp][sl] = j;
+    }
+    base += __popc(bal);
+  }
+  __syncwarp();
+  const int need = keep - cb;  // candidates to take, best (value desc, column asc) first
+  double cin = INFINITY, cout = -INFINITY;  // selected / unselected candidates' extremes
+  if (lane < ncand) {
+    const double mv = c_val[warp][lane];
+    const int mc = c_col[warp][lane];
+    int rank = 0;
+    for (int u = 0; u < ncand; ++u) {
+      const double uv = c_val[warp][u];
+      rank += (uv > mv || (uv == mv && c_col[warp][u] < mc)) ? 1 : 0;
+    }
+    const bool sel = rank < need;
+    if (sel) atomicOr(&c_bits[warp][mc >> 5], 1u << (mc & 31));
+    if (sel) cin = mv; else cout = mv;
+  }
+  __syncwarp();
+  // selected = {image > b} U chosen candidates; mask word i = ballot of register i
+  float fin = INFINITY, fout = -INFINITY;  // min image above b, max image at or below a
+  uint32_t mine = 0u;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    const bool sel = f[i] > b || ((c_bits[warp][i] >> lane) & 1u);
+    if (f[i] > b) fin = fminf(fin, f[i]);
+    if (f[i] <= a && j < M_total) fout = fmaxf(fout, f[i]);
+    const unsigned w = __ballot_sync(FULL, sel);
+    if (lane == i) mine = w;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    fin = fminf(fin, __shfl_xor_sync(FULL, fin, o));
+    fout = fmaxf(fout, __shfl_xor_sync(FULL, fout, o));
+    cin = fmin(cin, __shfl_xor_sync(FULL, cin, o));
+    cout = fmax(cout, __shfl_xor_sync(FULL, cout, o));
+  }
+  // float64 extremes: the row max (image fmx), the smallest selected value (min of the
+  // selected candidates and of the elements whose image is fin), the largest unselected
+  // (max of the unselected candidates and of the elements whose image is fout)
+  double mx = -INFINITY, vin = cin, vout = cout;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    if (j < M_total && (f[i] == fmx || (f[i] > b && f[i] == fin) || (f[i] <= a && f[i] == fout))) {
+      const double x = Sr[j];
+      if (f[i] == fmx) mx = fmax(mx, x);
+      if (f[i] > b && f[i] == fin) vin = fmin(vin, x);
+      if (f[i] <= a && f[i] == fout) vout = fmax(vout, x);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+    vin = fmin(vin, __shfl_xor_sync(FULL, vin, o));
+    vout = fmax(vout, __shfl_xor_sync(FULL, vout, o));
+  }
+  const double scale = fmax(1.0, fmax(fabs(vin - mx), fabs(vout - mx)));
+  const bool exact = vin - mx > -700.0 && (vout == -INFINITY || vin - vout > 1e-12 * scale);
+  if (!exact) return redo();
+  const int i_adj = (int)(row % M_v);
+  uint32_t* brow = bits + row * words;
+  int run = 0;
+  for (int w = lane; w < words; w += 32) {
+    uint32_t x = w == lane ? mine : 0u;
+    if (with_union) {
+      if (adja) x |= __ldg(adja + (int64_t)i_adj * words + w);
+      const int lo = w * 32;  // condition columns j >= M_v (masks.py:173)
+      if (lo + 32 <= M_total && lo >= M_v) {
+        x = ~0u;
+      } else {
+        for (int bb = 0; bb < 32; ++bb) {
+          const int j = lo + bb;
+          if (j >= M_v && j < M_total) x |= 1u << bb;
+        }
+      }
+    }
+    brow[w] = x;
+    run += __popc(x);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) run += __shfl_xor_sync(FULL, run, o);
+  if (lane == 0) kv_cnt[row] = run;
+}
+
 __global__ void __launch_bounds__(128) k_mask_pack(const uint8_t* __restrict__ dense, int M_total,
                                                    int words, uint32_t* __restrict__ bits,
                                                    int32_t* __restrict__ kv_cnt) {
@@ -1309,8 +1481,25 @@ static int launch_select(double* R, bool raw, int64_t n_rows, int M_v, int M_tot
   if (raw && !sort && fasts) {
     // p == 0 on scores nobody reads back as R: select on the scores (FASTS), then the exact
     // softmax program on the rows whose top-k boundary was a near tie (grid-stride, usually
-    // nothing to do)
-    int rc = go(k_select<true, false, 1, true>, 0);
+    // nothing to do).  Rows of <= 1024 columns take the register kernel (k_select_p0).
+    int rc;
+    static int legacy = -1;
+    if (legacy < 0) {
+      const char* e = getenv("TCB_SELECT_LEGACY");
+      legacy = (e && atoi(e) != 0) ? 1 : 0;
+    }
+    if (M_total <= 1024 && !legacy) {
+      const unsigned grid = (unsigned)ceil_div(n_rows, 4);
+      if (M_total <= 256)
+        k_select_p0<8><<<grid, 128, 0, s>>>(R, n_rows, M_v, M_total, adja, words, n_floor, with_union, bits, kv_cnt);
+      else if (M_total <= 512)
+        k_select_p0<16><<<grid, 128, 0, s>>>(R, n_rows, M_v, M_total, adja, words, n_floor, with_union, bits, kv_cnt);
+      else
+        k_select_p0<32><<<grid, 128, 0, s>>>(R, n_rows, M_v, M_total, adja, words, n_floor, with_union, bits, kv_cnt);
+      rc = check_launch("k_select_p0");
+    } else {
+      rc = go(k_select<true, false, 1, true>, 0);
+    }
     if (rc) return rc;
     return go(k_select<true, false, 2, false>, 0);
   }
