@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         float alpha = 1.f, sum;
         if (MAXFREE && !first) {
           // Max-free step: exponentiate against the running max first.  Every p <= sum, so a
-          // half whose sum stays <= 2^RESCALE_SUM_LOG2 has no p above that bound and needs no
+          // half whose sum stays <= RESCALE_SUM_LIMIT (2^12) has no p above it and needs no
           // max at all; otherwise (a new row maximum, or NaN/inf) redo it the classic way.
           sum = exps(bias - m_run);
           const bool over = !(sum <= RESCALE_SUM_LIMIT);
