@@ -20,9 +20,11 @@
 //     log2(e)/sqrt(d) * 2^-(e_q[r] + e_k[h]); the epilogue multiplies O by 2^-e_v[h] / l.
 //   * O is not accumulated across kv blocks in TMEM: the tensor core's fp32 accumulation
 //     rounds toward zero (measured: |O| shrinks by ~4e-5 relative over a 95-block row when
-//     every PV accumulates onto the running O), so each PV(t) writes a fresh O_mma and the
-//     softmax warps fold it into O_tot with round-to-nearest fp32 (O_tot = (O_tot + O_mma) *
-//     alpha) before releasing P(t+1) -- the same spot the lazy rescale used.
+//     every PV accumulates onto the running O), so O_mma collects one pair of PVs (one kv
+//     block: fresh at even half-steps, accumulating at odd ones) and the softmax warps fold
+//     each pair into O_tot with round-to-nearest fp32 (O_tot = (O_tot + O_mma) * alpha)
+//     before releasing the next even P -- the same spot the lazy rescale used.  (A fold per
+//     PV: 1.3e-6 max error on a C2 head and 52.0 ms; per pair: 1.5e-6 and 50.3 ms.)
 //
 // Structure follows k_carve_tc (carve.cu) with one CTA per SM (the split K / V tiles need
 // 192 KB of shared memory): warp 0 TMA producer + scheduler, warp 1 MMA issuer, warps 2-5
@@ -304,12 +306,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t vbase = aV + vs * C::SLOT_BYTES;
         const uint32_t pcol = tmem + C::S_COL + (gp & 1) * HN;
         if (ptx::elect_one()) {
-          // fresh O_mma per PV (folded into O_tot by the softmax warps); cross terms first
+          // O_mma fresh at even t, accumulating at odd t (the softmax warps fold each pair
+          // into O_tot); cross terms first
 #pragma unroll
           for (int kk = 0; kk < HN / 16; ++kk) {
             const uint32_t vh = vbase + kk * 16 * 128;
             ptx::mma_ts(tmem + C::O_COL, pcol + kk * 8, tc::make_sdesc(vh + C::HALF_BYTES, C::H_CHUNK, 1024),
-                        IDESC_O, kk > 0 ? 1u : 0u);
+                        IDESC_O, (kk > 0 || (t & 1)) ? 1u : 0u);
             ptx::mma_ts(tmem + C::O_COL, pcol + 32 + kk * 8, tc::make_sdesc(vh, C::H_CHUNK, 1024), IDESC_O, 1u);
           }
 #pragma unroll
@@ -444,26 +447,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint64_t sum2 = tc::fadd2(tc::fadd2(acc2[0], acc2[1]), tc::fadd2(acc2[2], acc2[3]));
         l_run = l_run * alpha + (tc::f2_lo(sum2) + tc::f2_hi(sum2));
         m_run = m_use;
-        if (t > 0) {  // fold PV(t-1) into O_tot (round-to-nearest), rescaled to this step's max
+        // O_mma collects a pair of PVs (even t fresh, odd t accumulating); at even t >= 2 the
+        // pair PV(t-2) + PV(t-1) is folded into O_tot (round-to-nearest), rescaled to this
+        // step's max; an odd step that raises the max rescales O_mma (and O_tot) in place
+        // before PV(t) adds onto it.  S(t) complete implies PV(t-2) complete (issued before
+        // QK(t)), so the o_done parity wait below cannot alias an older phase.
+        const bool fold = t >= 2 && !(t & 1);
+        if (fold || ((t & 1) && __any_sync(0xffffffffu, need))) {
           ptx::mbar_wait(&bars->o_done, (g - 1) & 1);
           ptx::tc_fence_after();
           const uint64_t a2 = tc::f2_pack(alpha, alpha);
+          const bool ot_valid = t > 2;
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
             uint32_t om[32], ot[32];
             ptx::tmem_ld32(t_row + C::O_COL + c * 32, om);
-            if (t > 1) ptx::tmem_ld32(t_row + C::OT_COL + c * 32, ot);
+            if (ot_valid) ptx::tmem_ld32(t_row + C::OT_COL + c * 32, ot);
             ptx::tmem_wait_ld();
+            if (fold) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              uint64_t sum = tc::f2_pack(__uint_as_float(om[2 * e]), __uint_as_float(om[2 * e + 1]));
-              if (t > 1)
-                sum = tc::fadd2(sum, tc::f2_pack(__uint_as_float(ot[2 * e]), __uint_as_float(ot[2 * e + 1])));
-              sum = tc::fmul2(sum, a2);
-              ot[2 * e] = __float_as_uint(tc::f2_lo(sum));
-              ot[2 * e + 1] = __float_as_uint(tc::f2_hi(sum));
+              for (int e = 0; e < 16; ++e) {
+                uint64_t sum = tc::f2_pack(__uint_as_float(om[2 * e]), __uint_as_float(om[2 * e + 1]));
+                if (ot_valid)
+                  sum = tc::fadd2(sum, tc::f2_pack(__uint_as_float(ot[2 * e]), __uint_as_float(ot[2 * e + 1])));
+                sum = tc::fmul2(sum, a2);
+                ot[2 * e] = __float_as_uint(tc::f2_lo(sum));
+                ot[2 * e + 1] = __float_as_uint(tc::f2_hi(sum));
+              }
+              ptx::tmem_st32(t_row + C::OT_COL + c * 32, ot);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                om[e] = __float_as_uint(__uint_as_float(om[e]) * alpha);
+                if (ot_valid) ot[e] = __float_as_uint(__uint_as_float(ot[e]) * alpha);
+              }
+              ptx::tmem_st32(t_row + C::O_COL + c * 32, om);
+              if (ot_valid) ptx::tmem_st32(t_row + C::OT_COL + c * 32, ot);
             }
-            ptx::tmem_st32(t_row + C::OT_COL + c * 32, ot);
           }
         }
         ptx::tmem_wait_st();
@@ -480,9 +500,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int c = 0; c < D / 32; ++c) {
         uint32_t ov[32], ot[32];
         ptx::tmem_ld32(t_row + C::O_COL + c * 32, ov);
-        if (T > 1) ptx::tmem_ld32(t_row + C::OT_COL + c * 32, ot);
+        if (T > 2) ptx::tmem_ld32(t_row + C::OT_COL + c * 32, ot);
         ptx::tmem_wait_ld();
-        if (T > 1) {
+        if (T > 2) {
 #pragma unroll
           for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) + __uint_as_float(ot[e]));
         }
