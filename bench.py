@@ -16,6 +16,7 @@ metric (the oracle port stands in only when baseline/_ref is absent).
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import math
 import os
@@ -52,17 +53,22 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """nvidia-smi sampler (every 50 ms) started before the warm-up, so that it is already
+    producing when the timed region begins; only the samples whose timestamps fall inside
+    the timed region (host clock, marked around the barriers) are summarised -- the nearest
+    earlier sample stands in when the region is shorter than one sampling period."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.t0 = self.t1 = None
+        self.result = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -72,32 +78,51 @@ class Clocks:
             self.proc = None
         return self
 
-    def __exit__(self, *a):
-        self.result = None
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def stop(self):
         if self.proc is None:
-            return
+            return None
         self.proc.terminate()
         try:
             out, _ = self.proc.communicate(timeout=5)
         except Exception:
-            return
-        rows = [r.split(", ") for r in out.strip().splitlines() if r.count(",") >= 6]
-        if not rows:
-            return
-        sm = [float(r[0]) for r in rows]
-        mx = max(float(r[1]) for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].strip() == "Active"})
-        load = [s for s in sm if s > 0.5 * mx] or sm
-        pw = []
-        for r in rows:
+            return None
+        rows = []
+        for line in out.strip().splitlines():
+            r = line.split(", ")
+            if len(r) < 8:
+                continue
             try:
-                pw.append(float(r[2]))
+                ts = datetime.datetime.strptime(r[0].strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(r[1]), float(r[2]), r[3], r[4:8]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        inside = [r for r in rows if self.t0 is not None and self.t0 <= r[0] <= self.t1]
+        if not inside:  # region shorter than a sampling period: the last sample before its end
+            before = [r for r in rows if self.t1 is not None and r[0] <= self.t1]
+            inside = before[-1:] or rows[-1:]
+        sm = [r[1] for r in inside]
+        mx = max(r[2] for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in inside for i in range(4) if r[4][i].strip() == "Active"})
+        pw = []
+        for r in inside:
+            try:
+                pw.append(float(r[3]))
             except ValueError:
                 pass
-        self.result = {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": reasons,
-                       "samples": len(rows),
+        self.result = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": reasons,
+                       "samples": len(inside),
+                       "window_s": round(self.t1 - self.t0, 3) if self.t0 and self.t1 else None,
                        "power_w_median": statistics.median(pw) if pw else None}
+        return self.result
 
 
 def dist_env():
@@ -221,6 +246,7 @@ def run_gpu(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    clk = Clocks(local).start()  # sampling before the timed region starts (see Clocks)
     for _ in range(args.warmup):
         step()
     barrier()
@@ -235,12 +261,14 @@ def run_gpu(args):
     marks = [[ev() for _ in range(4)] for _ in range(args.steps)]
     t0, t1 = ev(), ev()
     barrier()
-    with Clocks(local) as clk:
-        t0.record()
-        for i in range(args.steps):
-            step(marks[i])
-        t1.record()
-        barrier()
+    clk.mark_start()
+    t0.record()
+    for i in range(args.steps):
+        step(marks[i])
+    t1.record()
+    barrier()
+    clk.mark_end()
+    clk.stop()
     total_ms = t0.elapsed_time(t1)
     per = np.array([[marks[i][j].elapsed_time(marks[i][j + 1]) for j in range(3)]
                     for i in range(args.steps)])
