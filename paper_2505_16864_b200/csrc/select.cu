@@ -445,6 +445,13 @@ struct PwProg {
   int2 ops[SEL_MAX_LEAVES];
 };
 
+// Sort-buffer entries per warp of the complete / exact passes: the shared-memory sort needs
+// the row's power of two (>= the 544-slot register-window staging), and rows of <= 1024
+// columns stage their register-sorted keys with one pad slot per 32 (33 x 32 entries).
+__host__ __device__ constexpr int sel_full_sort(int np2, int M_total) {
+  return (np2 > 544 ? np2 : 544) < 1056 && M_total <= 1024 ? 1056 : (np2 > 544 ? np2 : 544);
+}
+
 // ---- warp-per-row selection ------------------------------------------------------
 constexpr int SW_WARPS = 4;  // rows (one warp each) per CTA
 constexpr unsigned FULL = 0xffffffffu;
@@ -1123,7 +1130,7 @@ __global__ void __launch_bounds__(SW_WARPS * 32) k_select(double* __restrict__ R
   const int M_pad = (M_total + 1) & ~1;
   double* vals = reinterpret_cast<double*>(base);
   const RowScratch sc = carve_scratch(base + (size_t)M_pad * 8, words, nslots,
-                                      MODE == 1 ? 544 : (np2 > 544 ? np2 : 544));
+                                      MODE == 1 ? 544 : sel_full_sort(np2, M_total));
   double* Rr = R + row * M_total;
   for (int j = lane; j < M_total; j += 32) vals[j] = Rr[j];
   __syncwarp();
@@ -1306,6 +1313,243 @@ __global__ void __launch_bounds__(128, 4) k_select_p0(const double* __restrict__
   if (lane == 0) kv_cnt[row] = run;
 }
 
+// ---- p > 0 on raw scores, rows of <= 32 * NPL columns: the cutoff without sorting -------
+// Same decision as select_row<RAW, SORT, MODE 1> (R = exp(S - max) / numpy-pairwise sum, in
+// the same operations, so R is bitwise the shared-memory path's; n_cut = 1 + #(sorted
+// sequential prefix <= p); keep = min(max(n_cut, n_floor), M_total) top columns under
+// (R desc, column asc)), but instead of a radix-selected 512-wide window sorted in
+// registers: a bisection on fp32 images of R brackets the prefix crossing to <= 32 candidate
+// columns (a, b] with the tree-summed mass above b <= p < the mass above a; the candidates are
+// ranked exactly and their prefixes formed from that mass.  Every prefix within 1e-12 of p
+// (where the tree and np.cumsum's sequential order could round to different sides), a
+// boundary that cannot be narrowed to 32 candidates (mass ties), or a non-finite score sends
+// the row to the exact pass (kv_cnt = -1, R written back for it; with write_r every row's R
+// is written, as tcb_block_select_scores returns it).
+template <int NPL>
+__global__ void __launch_bounds__(128) k_select_cut(double* __restrict__ S, int64_t n_rows, int M_v,
+                                                     int M_total, const uint32_t* __restrict__ adja,
+                                                     int words, int n_floor, double p, int with_union,
+                                                     int write_r, uint32_t* __restrict__ bits,
+                                                     int32_t* __restrict__ kv_cnt,
+                                                     const __grid_constant__ PwProg prog) {
+  __shared__ int leaf_off[SEL_MAX_LEAVES], leaf_len[SEL_MAX_LEAVES];
+  __shared__ int2 fold_ops[SEL_MAX_LEAVES];
+  __shared__ double vals[4][NPL * 32];
+  __shared__ double leafv[4][64];
+  __shared__ double c_val[4][32];
+  __shared__ int c_col[4][32];
+  __shared__ uint32_t c_bits[4][NPL];
+  load_prog(prog, leaf_off, leaf_len, fold_ops);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 4 + warp;
+  if (row >= n_rows) return;
+  double* Sr = S + row * M_total;
+  double* vs = vals[warp];
+  // ---- R, exactly as select_row<RAW>: max, exp, pairwise sum, divide
+  double r[NPL];
+  bool bad = false;
+  double mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    r[i] = j < M_total ? Sr[j] : 0.0;
+    if (j < M_total) {
+      bad |= !isfinite(r[i]);
+      mx = fmax(mx, r[i]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    if (j < M_total) vs[j] = r[i] = exp(r[i] - mx);
+  }
+  __syncwarp();
+  for (int l = lane; l < prog.nl; l += 32) leafv[warp][l] = pw_leaf(vs + leaf_off[l], leaf_len[l]);
+  __syncwarp();
+  double tot = 0.0;
+  if (lane == 0) {
+    for (int q = 0; q < prog.nops; ++q)
+      leafv[warp][prog.nl + q] = leafv[warp][fold_ops[q].x] + leafv[warp][fold_ops[q].y];
+    tot = leafv[warp][prog.nops ? prog.nl + prog.nops - 1 : 0];
+  }
+  tot = __shfl_sync(FULL, tot, 0);
+  float f[NPL];
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const int j = lane + 32 * i;
+    r[i] = j < M_total ? r[i] / tot : 0.0;
+    f[i] = j < M_total ? (float)r[i] : -INFINITY;
+    if (j < M_total && write_r) Sr[j] = r[i];
+  }
+  auto redo = [&]() {
+    if (!write_r) {
+#pragma unroll
+      for (int i = 0; i < NPL; ++i)
+        if (lane + 32 * i < M_total) Sr[lane + 32 * i] = r[i];
+    }
+    if (lane == 0) kv_cnt[row] = -1;
+  };
+  if (__any_sync(FULL, bad)) return redo();
+  // mass and count of the columns whose image exceeds x (tree order: bracketing only)
+  auto mass_gt = [&](float x, int& cnt) {
+    double m = 0.0;
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i)
+      if (f[i] > x) {
+        m += r[i];
+        ++c;
+      }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(FULL, m, o);
+    cnt = (int)__reduce_add_sync(FULL, (unsigned)c);
+    return m;
+  };
+  // ---- n_cut: bracket the prefix crossing, mass(b) <= p < mass(a)
+  float a = -1.0f, b = 2.0f;  // R in [0, 1]
+  int na = M_total, nb = 0;
+  double ma = 0.0, mb = 0.0;
+  ma = mass_gt(a, na);
+  if (!(ma > p + 1e-12)) return redo();  // the row total does not clear p: exact pass
+  {
+    float fmx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) fmx = fmaxf(fmx, f[i]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(FULL, fmx, o));
+    b = fmx;  // nothing exceeds the maximum image
+  }
+  for (int itn = 0; itn < 48 && na - nb > 32; ++itn) {
+    const float mid = a + 0.5f * (b - a);
+    if (!(mid > a && mid < b)) break;
+    int c;
+    const double m = mass_gt(mid, c);
+    if (m <= p) { b = mid; mb = m; nb = c; } else { a = mid; ma = m; na = c; }
+  }
+  auto gather = [&](float lo, float hi, int base_cnt) -> int {  // candidates (lo, hi] in column order
+    int base = 0;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) {
+      const bool c = f[i] > lo && f[i] <= hi;
+      const unsigned bal = __ballot_sync(FULL, c);
+      if (c) {
+        const int sl = base + __popc(bal & ((1u << lane) - 1u));
+        c_val[warp][sl] = r[i];
+        c_col[warp][sl] = lane + 32 * i;
+      }
+      base += __popc(bal);
+    }
+    __syncwarp();
+    return base;
+  };
+  int ncand = na - nb;
+  if (ncand > 32 || p - mb <= 1e-12) return redo();
+  gather(a, b, 0);
+  // candidate t's rank under (R desc, column asc) and the prefix through it
+  int cut_count = 0;
+  bool ambiguous = false;
+  {
+    int rank = 1 << 30;
+    double pre = 0.0;
+    if (lane < ncand) {
+      const double mv = c_val[warp][lane];
+      const int mc = c_col[warp][lane];
+      rank = 0;
+      for (int u = 0; u < ncand; ++u) {
+        const double uv = c_val[warp][u];
+        rank += (uv > mv || (uv == mv && c_col[warp][u] < mc)) ? 1 : 0;
+      }
+      double ssum = 0.0;  // candidates up to and including this one, in rank order
+      for (int u = 0; u < ncand; ++u) {
+        const double uv = c_val[warp][u];
+        const bool before = uv > mv || (uv == mv && c_col[warp][u] <= mc);
+        if (before) ssum += uv;
+      }
+      pre = mb + ssum;
+      ambiguous = fabs(pre - p) <= 1e-12;
+    }
+    cut_count = (int)__reduce_add_sync(FULL, (unsigned)(lane < ncand && pre <= p));
+    ambiguous = __any_sync(FULL, ambiguous);
+  }
+  if (ambiguous) return redo();
+  const int n_cut = nb + cut_count + 1;
+  const int keep = min(max(n_cut, n_floor), M_total);
+  // ---- the top-keep set: count-bracket its boundary (a2, b2] to <= 32 candidates
+  float a2 = a, b2 = b;
+  int na2 = na, nb2 = nb;
+  if (!(nb2 < keep && keep <= na2)) {  // keep outside the cutoff bracket: re-bracket by count
+    a2 = -1.0f;
+    na2 = M_total;
+    {
+      float fmx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < NPL; ++i) fmx = fmaxf(fmx, f[i]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(FULL, fmx, o));
+      b2 = fmx;
+      nb2 = 0;
+    }
+    for (int itn = 0; itn < 48 && na2 - nb2 > 32; ++itn) {
+      const float mid = a2 + 0.5f * (b2 - a2);
+      if (!(mid > a2 && mid < b2)) break;
+      int c;
+      mass_gt(mid, c);
+      if (c >= keep) { a2 = mid; na2 = c; } else { b2 = mid; nb2 = c; }
+    }
+    if (na2 - nb2 > 32) return redo();
+    __syncwarp();
+    gather(a2, b2, 0);
+  }
+  const int ncand2 = na2 - nb2;
+  const int need = keep - nb2;
+  for (int w = lane; w < NPL; w += 32) c_bits[warp][w] = 0u;
+  __syncwarp();
+  if (lane < ncand2) {
+    const double mv = c_val[warp][lane];
+    const int mc = c_col[warp][lane];
+    int rank = 0;
+    for (int u = 0; u < ncand2; ++u) {
+      const double uv = c_val[warp][u];
+      rank += (uv > mv || (uv == mv && c_col[warp][u] < mc)) ? 1 : 0;
+    }
+    if (rank < need) atomicOr(&c_bits[warp][mc >> 5], 1u << (mc & 31));
+  }
+  __syncwarp();
+  uint32_t mine = 0u;
+#pragma unroll
+  for (int i = 0; i < NPL; ++i) {
+    const bool sel = f[i] > b2 || ((c_bits[warp][i] >> lane) & 1u);
+    const unsigned w = __ballot_sync(FULL, sel);
+    if (lane == i) mine = w;
+  }
+  const int i_adj = (int)(row % M_v);
+  uint32_t* brow = bits + row * words;
+  int run = 0;
+  for (int w = lane; w < words; w += 32) {
+    uint32_t x = w == lane ? mine : 0u;
+    if (with_union) {
+      if (adja) x |= __ldg(adja + (int64_t)i_adj * words + w);
+      const int lo = w * 32;  // condition columns j >= M_v (masks.py:173)
+      if (lo + 32 <= M_total && lo >= M_v) {
+        x = ~0u;
+      } else {
+        for (int bb = 0; bb < 32; ++bb) {
+          const int j = lo + bb;
+          if (j >= M_v && j < M_total) x |= 1u << bb;
+        }
+      }
+    }
+    brow[w] = x;
+    run += __popc(x);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) run += __shfl_xor_sync(FULL, run, o);
+  if (lane == 0) kv_cnt[row] = run;
+}
+
 __global__ void __launch_bounds__(128) k_mask_pack(const uint8_t* __restrict__ dense, int M_total,
                                                    int words, uint32_t* __restrict__ bits,
                                                    int32_t* __restrict__ kv_cnt) {
@@ -1452,9 +1696,12 @@ static size_t scratch_bytes(const SelPlan& pl, int sortn) {
 constexpr size_t SMEM_CAP = 232448 - 8192;  // opt-in limit minus the static leaf tables
 
 // n_rows rows of R (row r uses adjacency row r % M_v; chunk callers offset the pointers)
+// write_r: the raw scores must come back as R for every row (tcb_block_select_scores returns
+// them); tcb_block_mask's scratch only needs R for the rows left to the exact pass.
 static int launch_select(double* R, bool raw, int64_t n_rows, int M_v, int M_total,
                          const uint32_t* adja, int words, int n_floor, double p, int with_union,
-                         uint32_t* bits, int32_t* kv_cnt, cudaStream_t s, bool fasts = false) {
+                         uint32_t* bits, int32_t* kv_cnt, cudaStream_t s, bool fasts = false,
+                         bool write_r = true) {
   TCB_CHECK_ARG(R && bits && kv_cnt, TCB_ESHAPE, "null tensor");
   TCB_CHECK_ARG(n_rows >= 0 && M_v >= 0 && M_total >= 1, TCB_ESHAPE, "bad select shape");
   TCB_CHECK_ARG(words >= ceil_div(M_total, 32), TCB_ESHAPE, "words too small");
@@ -1463,7 +1710,7 @@ static int launch_select(double* R, bool raw, int64_t n_rows, int M_v, int M_tot
   const SelPlan pl = plan_select(M_total, words);
   if (n_rows == 0) return TCB_OK;
   const bool sort = !raw || p > 0.0;
-  const int full_sort = pl.np2 > 544 ? pl.np2 : 544;
+  const int full_sort = sel_full_sort(pl.np2, M_total);
   // rows (warps) per CTA: SW_WARPS while their shared memory fits, fewer for long rows
   // (M_total = 8192 with the sort buffers needs 163 KB for one warp)
   auto go = [&](auto kern, int sortn) -> int {
@@ -1504,6 +1751,26 @@ static int launch_select(double* R, bool raw, int64_t n_rows, int M_v, int M_tot
     return go(k_select<true, false, 2, false>, 0);
   }
   if (raw && !sort) return go(k_select<true, false>, 0);
+  // cutoff path on raw scores of <= 1024 columns: the register kernel (k_select_cut, no sort)
+  // decides almost every row; the full-sort pass takes the rows it left (kv_cnt = -1)
+  static int legacy_cut = -1;
+  if (legacy_cut < 0) {
+    const char* e = getenv("TCB_SELECT_LEGACY");
+    legacy_cut = (e && atoi(e) != 0) ? 1 : 0;
+  }
+  if (raw && p > 0.0 && M_total <= 1024 && !legacy_cut) {
+    const unsigned grid = (unsigned)ceil_div(n_rows, 4);
+    const int wr = write_r ? 1 : 0;
+    if (M_total <= 256)
+      k_select_cut<8><<<grid, 128, 0, s>>>(R, n_rows, M_v, M_total, adja, words, n_floor, p, with_union, wr, bits, kv_cnt, pl.prog);
+    else if (M_total <= 512)
+      k_select_cut<16><<<grid, 128, 0, s>>>(R, n_rows, M_v, M_total, adja, words, n_floor, p, with_union, wr, bits, kv_cnt, pl.prog);
+    else
+      k_select_cut<32><<<grid, 128, 0, s>>>(R, n_rows, M_v, M_total, adja, words, n_floor, p, with_union, wr, bits, kv_cnt, pl.prog);
+    int rc = check_launch("k_select_cut");
+    if (rc) return rc;
+    return go(k_select<false, true, 2>, full_sort);
+  }
   // cutoff path: slim pass (register sort of the top-512 window, ~35 % less shared memory
   // per warp -> 1.5x the resident warps), then the full-sort pass over the rows it left
   int rc = raw ? go(k_select<true, true, 1>, 544) : go(k_select<false, true, 1>, 544);
@@ -1568,7 +1835,7 @@ extern "C" int tcb_block_mask(const double* pq, int pq_blocks, const double* pk,
                          nh, M_v, M_total, d, scratch, s);
       if (rc) return rc;
       rc = launch_select(scratch, true, (int64_t)nh * M_v, M_v, M_total, adja, words, n_floor, p, 1,
-                         bits + (int64_t)h0 * M_v * words, kv_cnt + (int64_t)h0 * M_v, s, fasts);
+                         bits + (int64_t)h0 * M_v * words, kv_cnt + (int64_t)h0 * M_v, s, fasts, false);
       if (rc) return rc;
     }
     return TCB_OK;
@@ -1583,7 +1850,7 @@ extern "C" int tcb_block_mask(const double* pq, int pq_blocks, const double* pk,
       if (rc) return rc;
       rc = launch_select(scratch, true, nr, M_v, M_total, adja ? adja + (int64_t)r0 * words : nullptr,
                          words, n_floor, p, 1, bits + ((int64_t)h * M_v + r0) * words,
-                         kv_cnt + (int64_t)h * M_v + r0, s, fasts);
+                         kv_cnt + (int64_t)h * M_v + r0, s, fasts, false);
       if (rc) return rc;
     }
   }
