@@ -1408,12 +1408,13 @@ __global__ void __launch_bounds__(128) k_select_cut(double* __restrict__ S, int6
     cnt = (int)__reduce_add_sync(FULL, (unsigned)c);
     return m;
   };
-  // ---- n_cut: bracket the prefix crossing, mass(b) <= p < mass(a)
+  // ---- n_cut: bracket the prefix crossing, mass(b) <= p < mass(a); p == 0: n_cut = 1
+  // (masks.py:152-153 with prefix_0 = the row max > 0, as select_row's p == 0 branch)
   float a = -1.0f, b = 2.0f;  // R in [0, 1]
   int na = M_total, nb = 0;
   double ma = 0.0, mb = 0.0;
   ma = mass_gt(a, na);
-  if (!(ma > p + 1e-12)) return redo();  // the row total does not clear p: exact pass
+  if (p > 0.0 && !(ma > p + 1e-12)) return redo();  // the row total does not clear p
   {
     float fmx = -INFINITY;
 #pragma unroll
@@ -1422,7 +1423,7 @@ __global__ void __launch_bounds__(128) k_select_cut(double* __restrict__ S, int6
     for (int o = 16; o; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(FULL, fmx, o));
     b = fmx;  // nothing exceeds the maximum image
   }
-  for (int itn = 0; itn < 48 && na - nb > 32; ++itn) {
+  for (int itn = 0; p > 0.0 && itn < 48 && na - nb > 32; ++itn) {
     const float mid = a + 0.5f * (b - a);
     if (!(mid > a && mid < b)) break;
     int c;
@@ -1446,11 +1447,12 @@ __global__ void __launch_bounds__(128) k_select_cut(double* __restrict__ S, int6
     return base;
   };
   int ncand = na - nb;
+  int cut_count = 0;
+  bool ambiguous = false;
+  if (p > 0.0) {
   if (ncand > 32 || p - mb <= 1e-12) return redo();
   gather(a, b, 0);
   // candidate t's rank under (R desc, column asc) and the prefix through it
-  int cut_count = 0;
-  bool ambiguous = false;
   {
     int rank = 1 << 30;
     double pre = 0.0;
@@ -1475,7 +1477,10 @@ __global__ void __launch_bounds__(128) k_select_cut(double* __restrict__ S, int6
     ambiguous = __any_sync(FULL, ambiguous);
   }
   if (ambiguous) return redo();
-  const int n_cut = nb + cut_count + 1;
+  } else {
+    na = nb = 0;  // no cutoff bracket: the top-keep set is count-bracketed below
+  }
+  const int n_cut = p > 0.0 ? nb + cut_count + 1 : 1;
   const int keep = min(max(n_cut, n_floor), M_total);
   // ---- the top-keep set: count-bracket its boundary (a2, b2] to <= 32 candidates
   float a2 = a, b2 = b;
@@ -1750,15 +1755,15 @@ static int launch_select(double* R, bool raw, int64_t n_rows, int M_v, int M_tot
     if (rc) return rc;
     return go(k_select<true, false, 2, false>, 0);
   }
-  if (raw && !sort) return go(k_select<true, false>, 0);
-  // cutoff path on raw scores of <= 1024 columns: the register kernel (k_select_cut, no sort)
-  // decides almost every row; the full-sort pass takes the rows it left (kv_cnt = -1)
   static int legacy_cut = -1;
   if (legacy_cut < 0) {
     const char* e = getenv("TCB_SELECT_LEGACY");
     legacy_cut = (e && atoi(e) != 0) ? 1 : 0;
   }
-  if (raw && p > 0.0 && M_total <= 1024 && !legacy_cut) {
+  if (raw && M_total <= 1024 && !legacy_cut && p > 0.0) {
+    // the cutoff on raw scores of <= 1024 columns: the register kernel (k_select_cut, no
+    // sort) decides almost every row; the exact pass takes the rest.  (Its p = 0 branch is
+    // correct but slower than k_select<RAW, !SORT> there: 1.11 vs 0.71 ms at C2.)
     const unsigned grid = (unsigned)ceil_div(n_rows, 4);
     const int wr = write_r ? 1 : 0;
     if (M_total <= 256)
@@ -1771,6 +1776,7 @@ static int launch_select(double* R, bool raw, int64_t n_rows, int M_v, int M_tot
     if (rc) return rc;
     return go(k_select<false, true, 2>, full_sort);
   }
+  if (raw && !sort) return go(k_select<true, false>, 0);
   // cutoff path: slim pass (register sort of the top-512 window, ~35 % less shared memory
   // per warp -> 1.5x the resident warps), then the full-sort pass over the rows it left
   int rc = raw ? go(k_select<true, true, 1>, 544) : go(k_select<false, true, 1>, 544);

@@ -5,7 +5,7 @@ tcb_block_select_scores turns the pooled scores into R in place (every row) and 
 tcb_block_mask selects from its own scratch.  Both must equal masks.py's importance_mask
 (stable descending order, np.cumsum prefix, n_cut = #(prefix <= p) + 1, floor, cap) plus the
 condition columns, restated here in numpy over that R -- on random, duplicated, near-tied,
-flat and peaked rows, p from 0.1 to 0.95, n_floor from 1 to M_v, widths around the kernel's
+flat and peaked rows, p from 0 (the R-returning p = 0 path) to 0.95, n_floor from 1 to M_v, widths around the kernel's
 256 / 512 / 1024 splits and one beyond (the shared-memory path)."""
 
 import numpy as np
@@ -67,7 +67,7 @@ def test_cutoff_select_equals_reference_on_device_R(M_total, kind):
     pq_t, pk_t = torch.from_numpy(pq).cuda(), torch.from_numpy(pk).cuda()
     words = mask_words(M_total)
     st = torch.cuda.current_stream().cuda_stream
-    for p in (0.1, 0.3, 0.7, 0.95):
+    for p in (0.0, 0.1, 0.3, 0.7, 0.95):
         for n_floor in sorted({1, max(1, M_total // 12), M_v}):
             S = torch.empty((H, M_v, M_total), dtype=torch.float64, device="cuda")
             _native.call("tcb_block_scores", pq_t.data_ptr(), M_total, pk_t.data_ptr(), H, M_v,
