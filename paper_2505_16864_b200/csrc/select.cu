@@ -1346,26 +1346,19 @@ __global__ void __launch_bounds__(128) k_select_cut(double* __restrict__ S, int6
   if (row >= n_rows) return;
   double* Sr = S + row * M_total;
   double* vs = vals[warp];
-  // ---- R, exactly as select_row<RAW>: max, exp, pairwise sum, divide
-  double r[NPL];
+  // ---- R, exactly as select_row<RAW>: max, exp, pairwise sum, divide (R kept in shared
+  // memory, only its fp32 images in registers: occupancy for the fp64 exp / divide latency)
   bool bad = false;
   double mx = -INFINITY;
-#pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    const int j = lane + 32 * i;
-    r[i] = j < M_total ? Sr[j] : 0.0;
-    if (j < M_total) {
-      bad |= !isfinite(r[i]);
-      mx = fmax(mx, r[i]);
-    }
+  for (int j = lane; j < M_total; j += 32) {
+    const double x = Sr[j];
+    vs[j] = x;
+    bad |= !isfinite(x);
+    mx = fmax(mx, x);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
-#pragma unroll
-  for (int i = 0; i < NPL; ++i) {
-    const int j = lane + 32 * i;
-    if (j < M_total) vs[j] = r[i] = exp(r[i] - mx);
-  }
+  for (int j = lane; j < M_total; j += 32) vs[j] = exp(vs[j] - mx);
   __syncwarp();
   for (int l = lane; l < prog.nl; l += 32) leafv[warp][l] = pw_leaf(vs + leaf_off[l], leaf_len[l]);
   __syncwarp();
@@ -1380,16 +1373,17 @@ __global__ void __launch_bounds__(128) k_select_cut(double* __restrict__ S, int6
 #pragma unroll
   for (int i = 0; i < NPL; ++i) {
     const int j = lane + 32 * i;
-    r[i] = j < M_total ? r[i] / tot : 0.0;
-    f[i] = j < M_total ? (float)r[i] : -INFINITY;
-    if (j < M_total && write_r) Sr[j] = r[i];
+    double rv = 0.0;
+    if (j < M_total) {
+      rv = vs[j] / tot;
+      vs[j] = rv;
+      if (write_r) Sr[j] = rv;
+    }
+    f[i] = j < M_total ? (float)rv : -INFINITY;
   }
   auto redo = [&]() {
-    if (!write_r) {
-#pragma unroll
-      for (int i = 0; i < NPL; ++i)
-        if (lane + 32 * i < M_total) Sr[lane + 32 * i] = r[i];
-    }
+    if (!write_r)
+      for (int j = lane; j < M_total; j += 32) Sr[j] = vs[j];
     if (lane == 0) kv_cnt[row] = -1;
   };
   if (__any_sync(FULL, bad)) return redo();
@@ -1400,7 +1394,7 @@ __global__ void __launch_bounds__(128) k_select_cut(double* __restrict__ S, int6
 #pragma unroll
     for (int i = 0; i < NPL; ++i)
       if (f[i] > x) {
-        m += r[i];
+        m += vs[lane + 32 * i];
         ++c;
       }
 #pragma unroll
@@ -1438,7 +1432,7 @@ __global__ void __launch_bounds__(128) k_select_cut(double* __restrict__ S, int6
       const unsigned bal = __ballot_sync(FULL, c);
       if (c) {
         const int sl = base + __popc(bal & ((1u << lane) - 1u));
-        c_val[warp][sl] = r[i];
+        c_val[warp][sl] = vs[lane + 32 * i];
         c_col[warp][sl] = lane + 32 * i;
       }
       base += __popc(bal);
