@@ -1757,7 +1757,7 @@ static int launch_select(double* R, bool raw, int64_t n_rows, int M_v, int M_tot
   if (raw && M_total <= 1024 && !legacy_cut && p > 0.0) {
     // the cutoff on raw scores of <= 1024 columns: the register kernel (k_select_cut, no
     // sort) decides almost every row; the exact pass takes the rest.  (Its p = 0 branch is
-    // correct but slower than k_select<RAW, !SORT> there: 1.11 vs 0.71 ms at C2.)
+    // correct but slower than k_select<RAW, !SORT> there: 0.78 vs 0.71 ms at C2.)
     const unsigned grid = (unsigned)ceil_div(n_rows, 4);
     const int wr = write_r ? 1 : 0;
     if (M_total <= 256)
