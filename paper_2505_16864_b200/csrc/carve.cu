@@ -340,7 +340,7 @@ struct Smem {
 };
 
 struct Bars {
-  uint64_t q_full, q_empty, o_full, o_done;
+  uint64_t q_full, q_empty, o_full;
   uint64_t p_full[2];  // by half-step parity: softmax(t+1) may finish before PV(t) is issued
   uint64_t s_full[2];
   uint64_t k_full[K_SLOTS], k_empty[K_SLOTS];
@@ -425,7 +425,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
     ptx::mbar_init(&bars->q_full, 1);
     ptx::mbar_init(&bars->q_empty, 1);
     ptx::mbar_init(&bars->o_full, 1);
-    ptx::mbar_init(&bars->o_done, 1);
     for (int i = 0; i < 2; ++i) ptx::mbar_init(&bars->p_full[i], 128);
     for (int i = 0; i < 2; ++i) ptx::mbar_init(&bars->s_full[i], 1);
     for (int i = 0; i < K_SLOTS; ++i) {
@@ -588,7 +587,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
                         (t > 0 || kk > 0) ? 1u : 0u);
           }
           ptx::mma_commit(&bars->v_empty[vs]);
-          ptx::mma_commit(&bars->o_done);
         }
         __syncwarp();
         if (lane == 0) TRACE(5, gp);
@@ -722,8 +720,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 2)
         ptx::tmem_st32(t_row + (g & 1) * HN, pk);
         l_run = l_run * alpha + sum;
         if (__any_sync(0xffffffffu, need)) {
-          // O is final only once PV(t-1) retired: o_done completes once per PV
-          ptx::mbar_wait(&bars->o_done, (g - 1) & 1);
+          // O is final only once PV(t-1) retired: its commit to the V slot's empty barrier
+          // (the k-th PV on a slot completes that barrier's phase k).  S(t) being ready means
+          // PV(t-2), issued before QK(t), is complete, so the parity cannot alias.
+          ptx::mbar_wait(&bars->v_empty[(g - 1) % V_SLOTS], ((g - 1) / V_SLOTS) & 1);
           ptx::tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < D / 32; ++c) {
