@@ -59,7 +59,7 @@ struct Cfg {
 };
 
 struct Bars {
-  uint64_t q_full, o_full, o_done;
+  uint64_t q_full, o_full;
   uint64_t p_full[2], s_full[2];
   uint64_t k_full[K_SLOTS], k_empty[K_SLOTS];
   uint64_t v_full[V_SLOTS], v_empty[V_SLOTS];
@@ -170,7 +170,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (ptx::smem_u32(smem) & 1023u) __trap();
     ptx::mbar_init(&bars->q_full, 128);
     ptx::mbar_init(&bars->o_full, 1);
-    ptx::mbar_init(&bars->o_done, 1);
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&bars->p_full[i], 128);
       ptx::mbar_init(&bars->s_full[i], 1);
@@ -320,7 +319,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mma_ts(tmem + C::O_COL, pcol + kk * 8, tc::make_sdesc(vbase + kk * 16 * 128, C::H_CHUNK, 1024),
                         IDESC_O, 1u);
           ptx::mma_commit(&bars->v_empty[vs]);
-          ptx::mma_commit(&bars->o_done);
         }
         __syncwarp();
         ++gv;
@@ -450,11 +448,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // O_mma collects a pair of PVs (even t fresh, odd t accumulating); at even t >= 2 the
         // pair PV(t-2) + PV(t-1) is folded into O_tot (round-to-nearest), rescaled to this
         // step's max; an odd step that raises the max rescales O_mma (and O_tot) in place
-        // before PV(t) adds onto it.  S(t) complete implies PV(t-2) complete (issued before
-        // QK(t)), so the o_done parity wait below cannot alias an older phase.
+        // before PV(t) adds onto it.  PV(t-1) is waited for on its V slot's empty barrier (the
+        // k-th PV on a slot completes phase k); S(t) complete implies PV(t-2) -- and so the
+        // slot's previous PV(t-4) -- complete (issued before QK(t)): the parity cannot alias.
         const bool fold = t >= 2 && !(t & 1);
         if (fold || ((t & 1) && __any_sync(0xffffffffu, need))) {
-          ptx::mbar_wait(&bars->o_done, (g - 1) & 1);
+          ptx::mbar_wait(&bars->v_empty[(g - 1) % V_SLOTS], ((g - 1) / V_SLOTS) & 1);
           ptx::tc_fence_after();
           const uint64_t a2 = tc::f2_pack(alpha, alpha);
           const bool ot_valid = t > 2;
