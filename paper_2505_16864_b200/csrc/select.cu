@@ -1424,7 +1424,7 @@ __global__ void __launch_bounds__(128) k_select_cut(double* __restrict__ S, int6
     const double m = mass_gt(mid, c);
     if (m <= p) { b = mid; mb = m; nb = c; } else { a = mid; ma = m; na = c; }
   }
-  auto gather = [&](float lo, float hi, int base_cnt) -> int {  // candidates (lo, hi] in column order
+  auto gather = [&](float lo, float hi) -> int {  // candidates (lo, hi] in column order
     int base = 0;
 #pragma unroll
     for (int i = 0; i < NPL; ++i) {
@@ -1445,7 +1445,7 @@ __global__ void __launch_bounds__(128) k_select_cut(double* __restrict__ S, int6
   bool ambiguous = false;
   if (p > 0.0) {
   if (ncand > 32 || p - mb <= 1e-12) return redo();
-  gather(a, b, 0);
+  gather(a, b);
   // candidate t's rank under (R desc, column asc) and the prefix through it
   {
     int rank = 1 << 30;
@@ -1500,7 +1500,7 @@ __global__ void __launch_bounds__(128) k_select_cut(double* __restrict__ S, int6
     }
     if (na2 - nb2 > 32) return redo();
     __syncwarp();
-    gather(a2, b2, 0);
+    gather(a2, b2);
   }
   const int ncand2 = na2 - nb2;
   const int need = keep - nb2;

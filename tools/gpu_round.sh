@@ -1,5 +1,6 @@
 #!/bin/bash
 # One gpurun call: tests + profiles.  Usage: gpurun -- bash tools/gpu_round.sh <what...>
+# (what: tests ref fullsize hbm hbmncu bench benchq launches carvencu sanitize)
 set -o pipefail
 mkdir -p gpurun_out
 for w in "$@"; do
@@ -13,6 +14,7 @@ for w in "$@"; do
     benchq)    python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench.json 2>gpurun_out/bench.err; tail -c 300 gpurun_out/bench.json; tail -3 gpurun_out/bench.err ;;
     launches)  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1; wc -l gpurun_out/launches.csv ;;
     carvencu)  ncu --set full --clock-control none --import-source on -k regex:k_carve_tc -c 1 -f -o gpurun_out/carve python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/carvencu.log 2>&1; tail -2 gpurun_out/carvencu.log ;;
+    sanitize)  for t in memcheck racecheck synccheck; do timeout 1500 compute-sanitizer --tool $t --print-limit 5 python -m pytest tests/test_gpu_parity.py tests/test_gpu_carve_split.py tests/test_gpu_select_p0.py tests/test_gpu_select_cut.py -q -p no:cacheprovider -x -k "split or extremes or fuzz or select or 931 or 256" 2>&1 | grep -E "SUMMARY|passed|failed" | sed "s/^/[$t] /"; done ;;
     *) echo "unknown $w" ;;
   esac
 done
