@@ -7,7 +7,12 @@ holds a curve-order token shard, and ``carve_layer_sp`` / the pipelined
 each rank's head shard, consumed in place as token-major (N, H/G, d) strided views and
 written straight into the return exchange's send buffer.  The gathered output must equal
 the single-rank layer bitwise (carved attention is independent per head, and neither kernel
-depends on the strides)."""
+depends on the strides).
+
+A 1-GPU box cannot host two NCCL ranks (NCCL rejects two ranks on one device), so the NCCL
+code path -- ``all_to_all_single`` on device tensors, its ``async_op`` works waited on the
+compute stream in the pipelined exchange -- runs as a world of one: every collective is a
+self-exchange, but the streams, waits and buffer lifetimes are the ones a node uses."""
 
 import os
 import socket
@@ -41,10 +46,13 @@ def _inputs(tcb):
     return lay, st, q, k, v
 
 
-def _worker(rank, world, port, out_path, chunks, pre_layout):
+def _worker(rank, world, port, out_path, chunks, pre_layout, backend="gloo"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_2505_16864_b200 as tcb
     from paper_2505_16864_b200.ulysses import (carve_layer_sp, carve_layer_sp_chunked,
                                                from_exchange_layout, to_exchange_layout)
@@ -77,9 +85,10 @@ def _worker(rank, world, port, out_path, chunks, pre_layout):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,chunks,pre_layout", [(2, 1, False), (2, 2, False), (4, 1, False),
-                                                      (4, 2, False), (4, 2, True)])
-def test_ulysses_real_kernels_bitwise(tmp_path, world, chunks, pre_layout):
+@pytest.mark.parametrize("world,chunks,pre_layout,backend", [
+    (2, 1, False, "gloo"), (2, 2, False, "gloo"), (4, 1, False, "gloo"), (4, 2, False, "gloo"),
+    (4, 2, True, "gloo"), (1, 1, False, "nccl"), (1, 2, False, "nccl"), (1, 4, True, "nccl")])
+def test_ulysses_real_kernels_bitwise(tmp_path, world, chunks, pre_layout, backend):
     import paper_2505_16864_b200 as tcb
 
     lay, st, q, k, v = _inputs(tcb)
@@ -87,7 +96,8 @@ def test_ulysses_real_kernels_bitwise(tmp_path, world, chunks, pre_layout):
     mask, _ = tcb.build_block_mask(q, k, lay, st, tcb.SelectionParams(k=0.3, p=0.0))
     full = tcb.carve_raw(q, k, v, mask, lay, 0.2).permute(1, 0, 2).cpu()  # (N, H, d)
     out = str(tmp_path / "o")
-    mp.spawn(_worker, args=(world, _free_port(), out, chunks, pre_layout), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, chunks, pre_layout, backend), nprocs=world,
+             join=True)
     got = torch.cat([torch.load(f"{out}.{r}") for r in range(world)], dim=0)
     assert got.shape == full.shape
     assert torch.equal(got, full)
