@@ -40,9 +40,14 @@ __all__ = ["to_exchange_layout", "from_exchange_layout", "default_chunks", "seq_
 
 
 def default_chunks(heads_per_rank: int) -> int:
-    """Head chunks of the pipelined exchange: 2 whenever a rank has >= 2 heads (the second
-    chunk's collective overlaps the first chunk's compute), else 1."""
-    return 2 if heads_per_rank >= 2 and heads_per_rank % 2 == 0 else 1
+    """Head chunks of the pipelined exchange: the smallest divisor >= 2 of the rank's head
+    count (C2 / 24 heads: 2 chunks at G = 2 and 4, 3 single-head chunks at G = 8; C3 / 40
+    heads: 5 at G = 8), so the next chunk's collective always overlaps this chunk's compute;
+    1 for a single head."""
+    for c in range(2, heads_per_rank + 1):
+        if heads_per_rank % c == 0:
+            return c
+    return 1
 
 
 def to_exchange_layout(x: torch.Tensor, G: int, chunks: int = 1) -> torch.Tensor:
