@@ -23,8 +23,8 @@ def _free_port():
     return port
 
 
-def _case():
-    dims, m, nc, H, d = (2, 6, 8), 8, 5, 4, 16
+def _case(H=4):
+    dims, m, nc, d = (2, 6, 8), 8, 5, 16
     L = oracle.layout_scalars(dims, m, nc)
     rng = np.random.default_rng(3)
     q, k, v = (rng.standard_normal((H, L["padded_total"], d)).astype(np.float32) for _ in range(3))
@@ -33,13 +33,13 @@ def _case():
     return dims, L, q, k, v, adja
 
 
-def _worker(rank, world, port, out_path, chunks=0):
+def _worker(rank, world, port, out_path, chunks=0, heads=4):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2505_16864_b200.ulysses import (carve_layer_sp, carve_layer_sp_chunked,
                                                from_exchange_layout, to_exchange_layout)
 
-    dims, L, q, k, v, adja = _case()
+    dims, L, q, k, v, adja = _case(heads)
     N = L["padded_total"]
     n_loc = N // world
 
@@ -56,6 +56,8 @@ def _worker(rank, world, port, out_path, chunks=0):
     if chunks == -1:  # inputs already in the exchange layout: no packing at all
         xs = [to_exchange_layout(shard(x), world, 2) for x in (q, k, v)]
         o = carve_layer_sp(*xs, None, local, chunks=None)
+    elif chunks is None:  # default chunking (an odd head count per rank: single-head chunks)
+        o = carve_layer_sp(shard(q), shard(k), shard(v), None, local, chunks=None)
     elif chunks:
         o = carve_layer_sp_chunked(shard(q), shard(k), shard(v), None, local, chunks=chunks)
     else:
@@ -64,16 +66,16 @@ def _worker(rank, world, port, out_path, chunks=0):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("chunks", [0, 1, 2, -1])
-def test_ulysses_roundtrip_world2(tmp_path, chunks):
+@pytest.mark.parametrize("chunks,heads", [(0, 4), (1, 4), (2, 4), (-1, 4), (None, 6)])
+def test_ulysses_roundtrip_world2(tmp_path, chunks, heads):
     if not dist.is_gloo_available():
         pytest.skip("gloo missing")
-    N_pad = _case()[1]["padded_total"]
+    N_pad = _case(heads)[1]["padded_total"]
     assert N_pad % 2 == 0
     port = _free_port()
     out = str(tmp_path / "o")
-    mp.spawn(_worker, args=(2, port, out, chunks), nprocs=2, join=True)
-    dims, L, q, k, v, adja = _case()
+    mp.spawn(_worker, args=(2, port, out, chunks, heads), nprocs=2, join=True)
+    dims, L, q, k, v, adja = _case(heads)
     bits, _ = oracle.block_mask(q, k, L, adja, 0.3, 0.3)
     full = oracle.carve(q, k, v, bits, L, 0.25).transpose(1, 0, 2)  # (N, H, d)
     got = np.concatenate([torch.load(f"{out}.{r}").numpy() for r in range(2)], axis=0)
