@@ -1,8 +1,8 @@
 """Every head of a BASELINE layer against the oracle (an exhaustive version of
 tests/test_gpu_fullsize_configs.py's sampled whole heads, too slow for the test suite):
 --config C2 (default: 720p, H=24, k=0.08, p=0, bf16, the bench's seed), C3 (Wan 480p, H=40,
-no text) or C4s1 (stage 1 of the 2-stage plan: 33x34x60 + 256 text, k=0.3, p=0.3 cutoff,
-beta=0.284).  For each head: the device mask vs the
+no text), C4s1 (stage 1 of the 2-stage plan: 33x34x60 + 256 text, k=0.3, p=0.3 cutoff,
+beta=0.284) or the C5 sweep endpoints on C2 (C5k01: k=0.01, C5k30: k=0.30).  For each head: the device mask vs the
 oracle's mask (bit-exact expected) and the carve output of every q-block vs the oracle's fp32
 carve on the device mask (north_star bf16 tolerance 2e-2 of max|ref|).  One JSON line per
 head to --out, a summary line on stdout.
@@ -34,13 +34,15 @@ M = D = 128
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", required=True)
-    ap.add_argument("--config", default="C2", choices=["C2", "C3", "C4s1"])
+    ap.add_argument("--config", default="C2", choices=["C2", "C3", "C4s1", "C5k01", "C5k30"])
     ap.add_argument("--seed", type=int, default=1234)
     a = ap.parse_args()
     cfg = {"C2": ((33, 45, 80), 256, 24, 0.08, 0.0, 0.0),
            "C3": ((21, 30, 52), 0, 40, 0.08, 0.0, 0.0),
            "C4s1": ((33, 34, 60), 256, 24, 0.3, 0.3,
-                    -0.5 * math.log((33 * 34 * 60) / (33 * 45 * 80)) + 0.0)}[a.config]
+                    -0.5 * math.log((33 * 34 * 60) / (33 * 45 * 80)) + 0.0),
+           "C5k01": ((33, 45, 80), 256, 24, 0.01, 0.0, 0.0),
+           "C5k30": ((33, 45, 80), 256, 24, 0.30, 0.0, 0.0)}[a.config]
     dims, nc, H, kr, pc, beta = cfg
     g = tcb.GridDims(*dims)
     lay = tcb.build_layout(g, M, nc)
