@@ -5,14 +5,17 @@
 //                    under mbarriers, one elected lane of the MMA warp issues
 //                    tcgen05.mma for S = Q K^T into TMEM (64-key half-steps, S
 //                    double-buffered), four softmax warps read S with tcgen05.ld, do
-//                    the online softmax in registers (exp2, lazy rescale), write P as
-//                    16-bit back into TMEM over S, and the MMA warp issues O += P V with
-//                    A read from TMEM.  Two CTAs per SM interleave so one CTA's softmax
-//                    overlaps the other's MMAs.  Work items (head, q-block) come from a
-//                    global atomic counter, condition q-blocks (full rows, ~10x longer)
-//                    first, then vision q-blocks head-major so concurrently running
-//                    items share a head's K/V in L2.  DESIGN.md §4.1 has the measured
-//                    bounds and the rejected variants.
+//                    the online softmax in registers (exp2; max-free half-steps that
+//                    take a block max only on a row's first half or when the p-sum says
+//                    the running max moved), write P as 16-bit back into TMEM over S, and
+//                    the MMA warp issues O += P V with A read from TMEM.  Two CTAs per SM
+//                    interleave so one CTA's softmax overlaps the other's MMAs.  Work
+//                    items (head, q-block) come from a global atomic counter, vision
+//                    q-blocks head-major so concurrently running items share a head's
+//                    K/V in L2; condition q-blocks (full rows, ~10x longer) run as kv-range
+//                    chunks in their head's slot, merged by the last chunk, when the
+//                    workspace allows (else all of them first, unsplit).
+//                    has the measured bounds and the rejected variants.
 //  * k_carve_f32t -- fp32 math on shared-memory tiles with register-blocked S / O for
 //                    the common (m, d): fp32 inputs and shapes the tcgen05 kernel does
 //                    not take; mirrors the reference's per-block streaming order (1e-5).
